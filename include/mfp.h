@@ -1,0 +1,250 @@
+/*
+ * mfp.h — C ABI of the B200-native distributed Mosaic Flow Predictor (MFP).
+ *
+ * The library implements ONE thing: the data-parallel hot path of arXiv 2308.14258
+ * ("Physics-informed neural PDE solvers at scale", the distributed MF predictor):
+ *
+ *   iterate  { for each of the 4 subdomain classes (phases):
+ *                gather the boundaries of every non-overlapping atomic subdomain of
+ *                the class, run ONE batched SDNet forward, scatter the centre-line
+ *                predictions back onto the line lattice }
+ *              exchange halo strips with the 3x3 stencil of neighbour ranks (once)
+ *              every c iterations: global max-norm update test }
+ *   final phase: predict every interior point of each atomic subdomain, gather.
+ *
+ * Paper passages (PAPER.md line numbers, "P:n"):
+ *   P:23  (§4.1)  atomic subdomains of one iteration do not overlap -> one batch
+ *   P:29  (§4.2)  Cartesian grid of subdomain boundaries with spacing m/2
+ *   P:39-40       row-major 2-D processor grid, processor subdomain + halo
+ *   P:43  (§4.2)  Algorithm 2: inputs t, eps, g, SDNet, n; predict only centre
+ *                 lines; pack overlap boundaries into a contiguous buffer; send
+ *   P:44          final phase: predict every grid point, all_gather, average
+ *   P:48          relaxed synchronisation: communicate once per iteration,
+ *                 immediate updates inside a processor subdomain
+ *   P:53-61 (§4.3) alpha-beta cost model
+ *   P:239-241 (§3.1) SDNet: 1-D convolutions over g, split layer, GELU MLP
+ *   P:261-274 (§3.2, Eq. 5) U = phi(g W1^T (+) X W2^T), broadcasted sum
+ *   P:512-519 (§2.1) Dirichlet Laplace BVP (defines the exact subsolver)
+ *
+ * Readings where the paper is silent are fixed in DESIGN.md §2 (G1..G7 of
+ * SURVEY.md §0.3): m = 32 intervals per subdomain side (33 points), perimeter
+ * of 4m = 128 values walked counter-clockwise from the lower-left corner
+ * (bottom L->R, right B->T, top R->L, left T->B), 2m-3 = 61 centre-line
+ * queries per prediction (vertical line bottom->top, then horizontal line
+ * left->right without the centre), class order (0,0),(1,0),(0,1),(1,1),
+ * distributed convention D1 (a rank computes every subdomain whose centre lies
+ * in its CLOSED block; owner values overwrite halo copies once per iteration),
+ * convergence delta = max over owned interior line points of |U_k - U_{k-1}|.
+ *
+ * Conventions for every entry point
+ *   - Every call returns mfp_status; 0 == MFP_OK.  Errors other than
+ *     MFP_NOT_CONVERGED leave a message readable with mfp_last_error().
+ *   - CUDA/NCCL failures are sticky: the context enters MFP_ERR_STATE and every
+ *     later call except mfp_destroy/mfp_last_error returns MFP_ERR_STATE.
+ *   - Host pointers are read (copied) during the call; the caller keeps them.
+ *   - Device buffers (workspace, g_dev, u_dev, gb, out) are caller-owned
+ *     (allocated with torch); the context only keeps views into the workspace
+ *     and never frees them.  The NCCL communicator is caller-owned as well.
+ *   - All fields are fp32, row-major with x fastest: u[y*(nx+1)+x].
+ *   - There is no CPU fallback: every numeric step runs in the library's
+ *     sm_100a kernels; without a CUDA device calls return MFP_ERR_CUDA.
+ */
+#ifndef MFP_H
+#define MFP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MFP_ABI_VERSION 1u
+/* rank argument meaning "this process drives every rank of the processor grid
+ * on its one device" (exchange by device copies instead of NCCL). */
+#define MFP_ALL_RANKS (-1)
+#define MFP_NCCL_UNIQUE_ID_BYTES 128
+
+typedef enum {
+  MFP_OK = 0,
+  MFP_ERR_INVALID = 1,      /* bad argument / config / length mismatch            */
+  MFP_ERR_NOT_TILEABLE = 2, /* nx or ny not a multiple of m, or grid not aligned  */
+  MFP_ERR_NONFINITE = 3,    /* NaN/Inf in g, params, or in a prediction           */
+  MFP_NOT_CONVERGED = 4,    /* non-fatal: u is written, report filled             */
+  MFP_ERR_CUDA = 5,
+  MFP_ERR_NCCL = 6,
+  MFP_ERR_WORKSPACE = 7,    /* workspace too small or misaligned (256 B)          */
+  MFP_ERR_STATE = 8         /* context poisoned by an earlier CUDA/NCCL error     */
+} mfp_status;
+
+enum { MFP_FP32 = 0, MFP_BF16 = 1 };            /* precision of the SDNet chain    */
+enum { MFP_SDNET = 0, MFP_EXACT_LAPLACE = 1 };  /* subdomain solver   */
+enum { MFP_QUERY_CENTRE = 0, MFP_QUERY_INTERIOR = 1 };
+
+/* Problem + decomposition.  P:39 (row-major processor grid), P:29 (stride m/2). */
+typedef struct {
+  uint32_t abi;        /* must be MFP_ABI_VERSION                                   */
+  int32_t nx, ny;      /* global grid intervals per side; (nx+1)x(ny+1) points      */
+  int32_t m;           /* subdomain intervals per side; must be 32 (G1)             */
+  int32_t stride;      /* must be m/2 (paper d = 2)                           */
+  int32_t grid_rows;   /* Py: processor rows    ((ny/m) % Py == 0)                  */
+  int32_t grid_cols;   /* Px: processor columns ((nx/m) % Px == 0)                  */
+  int32_t precision;   /* MFP_FP32 (SIMT, exact-erf GELU) | MFP_BF16 (tcgen05)      */
+  int32_t subsolver;   /* MFP_SDNET | MFP_EXACT_LAPLACE                              */
+  int32_t check_every; /* c >= 1: convergence test every c iterations                */
+} mfp_config;
+
+/* SDNet shape (sizes are reading G7).  Round 1 supports
+ * n_conv = 2, conv_k = {5,5}, conv_ch = {1,8,1}, d = 128, 1 <= n_hidden <= 3. */
+typedef struct {
+  int32_t n_conv;
+  int32_t conv_k[4];
+  int32_t conv_ch[5];
+  int32_t d;
+  int32_t n_hidden;
+  int32_t gelu;        /* 0: exact erf; 1: tanh approximation (bf16 path only)      */
+} mfp_sdnet_desc;
+
+typedef struct {
+  int32_t iterations;          /* iterations executed                                */
+  int32_t converged;           /* 1 if delta <= tol was observed                     */
+  float last_delta;            /* last computed delta (max over ranks)               */
+  float pad_;
+  double predictions;          /* UNIQUE subdomain predictions, (2Kx-1)(2Ky-1)/iter  */
+  double predictions_computed; /* including D1's redundant straddlers, all ranks     */
+  double ms_total;             /* device time of the solve (events), this rank       */
+  double ms_final;             /* device time of the final phase + gather            */
+  int64_t halo_bytes_sent;     /* this rank (all ranks for MFP_ALL_RANKS), whole run */
+  int32_t halo_msgs_per_iter;  /* messages sent per iteration by this rank (max)     */
+  int32_t gpu_launches;        /* kernels launched by the library during the solve   */
+} mfp_report;
+
+/* Per-kernel device time, measured with CUDA events on the launching stream. */
+typedef struct {
+  int32_t iterations;
+  int32_t launches_per_iter;
+  double ms_per_iter;          /* whole iteration (4 phases + exchange)              */
+  double ms_gather_embed;      /* per launch average                                 */
+  double ms_chain;             /* per launch average (SDNet chain, incl. scatter)    */
+  double ms_exact;             /* per launch average (exact subsolver phase kernel)  */
+  double ms_halo;              /* per iteration (pack + exchange + unpack)           */
+  double ms_delta;             /* per launch                                         */
+  int64_t chain_launches, chain_rows; /* rows = predictions * queries, all launches */
+  double chain_ms_total;
+  int64_t gather_launches, gather_subdomains;
+  double gather_ms_total;
+} mfp_profile;
+
+typedef struct mfp_ctx mfp_ctx;
+
+/* Host-only view of a rank's plan (no GPU needed).  P:39-43.  Coordinates are
+ * global grid indices.  Owned block: X0 <= x < X1 (x <= nx for the last column),
+ * same in y.  Read region (block + m/2 halo, clipped): RX0..RX1 closed. */
+typedef struct {
+  int32_t rank, ry, rx;
+  int32_t X0, X1, Y0, Y1;
+  int32_t RX0, RX1, RY0, RY1;
+  int64_t phase_count[4];      /* subdomains computed per phase (D1, closed block)   */
+  int64_t final_count;         /* owned atomic subdomains (final phase)              */
+  int32_t n_peers;
+  int32_t peers[8];            /* neighbour ranks in row-major order                 */
+  int64_t send_count[8];       /* lattice cells sent to peers[i] per iteration       */
+  int64_t recv_count[8];       /* lattice cells received from peers[i]               */
+  int64_t lattice_cells;       /* horizontal + vertical line cells held locally      */
+  int32_t n_hlines, n_vlines;  /* local line counts (y = RY0 + 16 i, x = RX0 + 16 j)  */
+  int32_t hline_len, vline_len;/* RX1-RX0+1, RY1-RY0+1                               */
+} mfp_plan_info;
+
+/* ---- sizing / lifetime ------------------------------------------------------ */
+
+/* Bytes of device workspace mfp_init needs for `rank` (or MFP_ALL_RANKS). */
+mfp_status mfp_workspace_size(const mfp_config* cfg, const mfp_sdnet_desc* net,
+                              int rank, size_t* bytes);
+
+/* Number of fp32 parameters `params` must hold, in SPEC MFCK declaration order
+ * (S:387): for each conv layer l: w_l (cout,cin,k), b_l (cout); W1 (d, 4m*ch_last);
+ * W2 (d,2); b1 (d); for each hidden layer: Wh (d,d), bh (d); wo (d); bo (1). */
+mfp_status mfp_param_count(const mfp_sdnet_desc* net, int32_t m, size_t* n);
+
+/* Validate, build the plan (N1), carve `workspace`, upload weights (and the
+ * exact-solver matrices when subsolver == MFP_EXACT_LAPLACE), precompute the
+ * per-query tables Q = X W2^T + b1 (Eq. 5).  `params` may be NULL iff
+ * subsolver == MFP_EXACT_LAPLACE.  rank in [0, Py*Px) with a caller-owned
+ * ncclComm_t (`nccl_comm`, NULL iff Py*Px == 1), or MFP_ALL_RANKS with
+ * nccl_comm == NULL.  `stream` is a caller-owned cudaStream_t (NULL = legacy).
+ * Errors: INVALID, NOT_TILEABLE, NONFINITE (params), WORKSPACE, CUDA. */
+mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net,
+                    const float* params, size_t n_params,
+                    int rank, void* nccl_comm,
+                    void* workspace, size_t ws_bytes,
+                    void* stream, mfp_ctx** out);
+
+void mfp_destroy(mfp_ctx* ctx);
+const char* mfp_last_error(const mfp_ctx* ctx);  /* never NULL */
+
+/* ---- the hot path ----------------------------------------------------------- */
+
+/* Algorithm 2.  g: HOST, 2(nx+ny) fp32 values walked counter-clockwise
+ * from (0,0) (bottom x=0..nx-1, right y=0..ny-1, top x=nx..1, left y=ny..1;
+ * reading G6).  g == NULL resumes from the current lattice (no init).
+ * max_iters = t >= 1.  tol = eps >= 0; tol == 0 runs exactly max_iters
+ * iterations (parity mode).  u_out: HOST (ny+1)*(nx+1) fp32, required on rank 0
+ * (and for MFP_ALL_RANKS), ignored elsewhere; may be NULL to skip the final
+ * phase.  rep nullable.  Collective over the communicator.
+ * Returns OK, NOT_CONVERGED (u written), NONFINITE, CUDA, NCCL, STATE. */
+mfp_status mfp_solve(mfp_ctx* ctx, const float* g, int32_t max_iters, float tol,
+                     float* u_out, mfp_report* rep);
+
+/* Same as mfp_solve with DEVICE g_dev / u_dev (inputs already resident). */
+mfp_status mfp_solve_device(mfp_ctx* ctx, const float* g_dev, int32_t max_iters,
+                            float tol, float* u_dev, mfp_report* rep);
+
+/* Batched SDNet forward only (P:23 batching; forward_many).
+ * gb: DEVICE B x 4m boundary vectors (G1 order); out: DEVICE B x q with
+ * q = 61 (MFP_QUERY_CENTRE, G3 order) or 961 (MFP_QUERY_INTERIOR, row-major
+ * (i/m, j/m), i,j = 1..31, i fastest).  Uses the context's weights and
+ * precision; `stream` NULL = the context stream.  No communication. */
+mfp_status mfp_sdnet_batch(mfp_ctx* ctx, const float* gb, int64_t B,
+                           int32_t query_set, float* out, void* stream);
+
+/* Run ONE phase (class 0..3 in G2 order) on the current lattice of every local
+ * rank, without exchange (debug / sampled parity at full size). */
+mfp_status mfp_step_phase(mfp_ctx* ctx, int32_t phase);
+
+/* Copy the local line lattice of `rank` (0 for single-rank contexts) to/from
+ * HOST buffers: hl[n_hlines][hline_len], vl[n_vlines][vline_len] (plan info). */
+mfp_status mfp_export_lines(mfp_ctx* ctx, int32_t rank, float* hl, float* vl);
+mfp_status mfp_import_lines(mfp_ctx* ctx, int32_t rank, const float* hl, const float* vl);
+
+/* Run `iters` iterations from the current lattice with CUDA events around each
+ * kernel (bench roofline).  Not collective-free: exchanges like mfp_solve. */
+mfp_status mfp_profile_iterations(mfp_ctx* ctx, int32_t iters, mfp_profile* out);
+
+/* ---- host-only plan introspection (no GPU) ----------------------------------- */
+
+mfp_status mfp_plan_query(const mfp_config* cfg, int32_t rank, mfp_plan_info* out);
+/* Anchors (lower-left corners, global) computed by `rank` in `phase` (0..3) or
+ * owned atomic subdomains (phase == 4), sorted by (ay, ax).  cap = array size. */
+mfp_status mfp_plan_anchors(const mfp_config* cfg, int32_t rank, int32_t phase,
+                            int32_t* ax, int32_t* ay, int64_t cap, int64_t* count);
+/* Halo cells exchanged with peers[peer_idx] in canonical order: kind 0 = cell of
+ * a horizontal line, 1 = vertical line; (x, y) global.  dir 0 = sent, 1 = recv. */
+mfp_status mfp_plan_halo(const mfp_config* cfg, int32_t rank, int32_t peer_idx,
+                         int32_t dir, int32_t* kind, int32_t* x, int32_t* y,
+                         int64_t cap, int64_t* count);
+
+/* alpha-beta model of §4.3: subdomains per processor (dN)^2/(m^2 P),
+ * C_comm = 8 I alpha + (I/beta) 16 N d / sqrt(P), C_comp = c (dN)^2/(m^2 P). */
+mfp_status mfp_cost_model(double N, double P, double m, double d, double I,
+                          double alpha, double beta, double c,
+                          double* subdomains_per_proc, double* c_comm, double* c_comp);
+
+/* ---- NCCL bootstrap (the unique id travels through torch.distributed) -------- */
+mfp_status mfp_nccl_get_unique_id(void* id_out /* MFP_NCCL_UNIQUE_ID_BYTES */);
+mfp_status mfp_nccl_comm_init(int32_t nranks, const void* id, int32_t rank, void** comm_out);
+mfp_status mfp_nccl_comm_destroy(void* comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MFP_H */
