@@ -1,0 +1,312 @@
+#!/usr/bin/env python
+"""bench.py — atomic-subdomain predictions/s of the distributed MFP (arXiv 2308.14258).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--iters T] [--impl ours|reference]
+
+One STEP = one complete mfp_solve of the C5 workload (4097 x 4097 grid points,
+m = 32, 65,025 subdomain predictions per iteration = 4 phases) for T fixed
+iterations (tol = 0, parity mode), i.e. every row of SURVEY §8(a): init (a0),
+T x [4 x (gather a1, embed a2, split expansion a3, hidden GEMM chain a4, head
+a5, scatter a6), halo exchange a7, delta a8 every 16 iterations], final phase
+(a9).  N = 1: the whole domain on one B200.  N > 1 (torchrun): the same domain
+on a Py x Px processor grid (1x2, 2x2, 2x4), NCCL halo exchange — strong scaling.
+
+value = UNIQUE predictions (T x 65,025) x K / max-over-ranks device time of the
+K timed steps (CUDA events on the solve stream, L2 flushed between steps, outside
+the events).  e2e = the same metric through mfp_solve with HOST g / u buffers
+(H2D of g and D2H of the full field inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "atomic-subdomain predictions/sec and MFP time-to-converge at 1/2/4/8 B200"
+GRIDS = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
+NX = NY = 4096
+PRED_PER_ITER = (2 * (NX // 32) - 1) * (2 * (NY // 32) - 1)   # 65,025
+HIDDEN_FLOP_PER_ROW = 3 * 2 * 128 * 128                        # a4: three d x d GEMM rows
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--iters", type=int, default=64, help="MFP iterations per step (T)")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    p.add_argument("--no-converge", action="store_true")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle-reason sampling (NVML) during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self.stop_ev.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ reference arm (oracle)
+def cpu_oracle_rate(target_s: float = 12.0):
+    """The oracle (fp64 C, OpenMP) as it stands, on a bounded sample of C5: SDNet
+    predictions of phase-0 subdomains from the initial lattice, one by one."""
+    import oracle
+    from mfp_inputs import gp_boundary, random_weights
+
+    w = random_weights(0).astype(np.float64)
+    cfg = oracle.MfpConfig(NX, NY)
+    U = np.zeros((NY + 1, NX + 1))
+    from mfp_inputs import boundary_points
+    bp = boundary_points(NX, NY)
+    U[bp[:, 1], bp[:, 0]] = gp_boundary(NX, NY, 0)
+    anc = oracle.anchors(NX, NY, 0)
+    n = 16
+    t0 = time.perf_counter()
+    oracle.predict_from_field(cfg, U, anc[:n], 0, w)
+    dt = time.perf_counter() - t0
+    n = int(min(len(anc), max(16, n * target_s / max(dt, 1e-3))))
+    t0 = time.perf_counter()
+    oracle.predict_from_field(cfg, U, anc[:n], 0, w)
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt, oracle.num_threads()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle  # noqa: F401
+    times, n_last, thr = [], 0, 1
+    for i in range(args.warmup + args.steps):
+        rate, n, dt, thr = cpu_oracle_rate(target_s=4.0)
+        if i >= args.warmup:
+            times.append((n, dt))
+        n_last = n
+    tot_n = sum(n for n, _ in times)
+    tot_t = sum(t for _, t in times)
+    v = tot_n / tot_t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "predictions/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (GP boundary, W-rand SDNet weights)",
+            "config": {"workload": "C5: 4097x4097 points, m=32, SDNet d=128 L_h=3, phase-0 subdomains",
+                       "nx": NX, "ny": NY, "m": 32, "subsolver": "sdnet"},
+            "cpu_baseline": {"value": v, "unit": "predictions/s", "cores": thr, "kind": "oracle",
+                             "sample": f"{n_last} C5 phase-0 subdomain predictions per step (fp64 oracle)"},
+            "e2e": {"value": v, "unit": "predictions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2308_14258_b200 as mfp
+    from mfp_inputs import gp_boundary, random_weights
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    assert world in GRIDS, "supported GPU counts: 1, 2, 4, 8"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [mfp.mfp_nccl_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = mfp.mfp_nccl_comm_init(world, obj[0], rank)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    grid = GRIDS[world]
+    prec = mfp.BF16 if args.precision == "bf16" else mfp.FP32
+    cfg = mfp.make_config(NX, NY, grid, precision=prec, subsolver=mfp.SDNET, check_every=16)
+    net = mfp.make_net(gelu=1 if prec == mfp.BF16 else 0)
+    w = random_weights(0)
+    stream = torch.cuda.Stream(device=dev)
+    m = mfp.Mfp(cfg, net, w, rank=rank, nccl_comm=comm, stream=stream)
+    g_host = gp_boundary(NX, NY, 0)
+    g_dev = torch.from_numpy(g_host).to(dev)
+    u_dev = torch.empty((NY + 1, NX + 1), dtype=torch.float32, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    T = args.iters
+
+    def step_device():
+        return m.solve_device(g_dev, T, 0.0, u_dev)
+
+    # warm-up
+    for _ in range(args.warmup):
+        rep = step_device()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches = 0
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(float(i))                     # L2 flush, outside the events
+                ev[i][0].record(stream)
+            rep = step_device()
+            launches += rep.gpu_launches
+            with torch.cuda.stream(stream):
+                ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    ms = max_over_ranks(ms)
+    preds = PRED_PER_ITER * T * args.steps
+    value = preds / (ms / 1000.0)
+
+    # e2e through the public host API: H2D of g + D2H of u inside the timed region
+    u_host = np.empty((NY + 1, NX + 1), np.float32) if rank == 0 else np.empty((1, 1), np.float32)
+    for _ in range(1):
+        mfp.mfp_solve(m.ctx, g_host, T, 0.0, u_host)
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        mfp.mfp_solve(m.ctx, g_host, T, 0.0, u_host)
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    barrier()
+    e2e = {"value": preds / e2e_s, "unit": "predictions/s", "h2d_bytes_per_step": g_host.nbytes,
+           "d2h_bytes_per_step": (NX + 1) * (NY + 1) * 4 if rank == 0 else 0}
+
+    # roofline of the dominant kernel (the tcgen05 chain), events on its stream
+    prof = m.profile(8)
+    chain_ms = prof.chain_ms_total / max(prof.chain_launches, 1)
+    flop_per_launch = prof.chain_rows / max(prof.chain_launches, 1) * HIDDEN_FLOP_PER_ROW
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("bf16_tflops_sustained", 1400.0) if prec == mfp.BF16 else 75.0
+    achieved = flop_per_launch / (chain_ms / 1000.0) / 1e12
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get("chain_tc_dram_bytes_per_launch")
+    roofline = {"bound": "tensor" if prec == mfp.BF16 else "alu", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "kernel": "k_chain_tc (hidden GEMM chain a4 + epilogues a3/a5/a6)",
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"
+                if prec == mfp.BF16 else "derived fp32 SIMT peak (DESIGN.md §7)",
+                "chain_ms_per_launch": chain_ms, "chain_share_of_iteration":
+                    prof.chain_ms_total / (prof.ms_per_iter * prof.iterations)}
+
+    # time-to-converge (SDNet bf16, tol 1e-3 max|g|, c = 16)
+    ttc = None
+    if not args.no_converge:
+        tol = 1e-3 * float(np.max(np.abs(g_host)))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+        rc = m.solve_device(g_dev, 20000, tol, u_dev)
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ttc = {"ms": max_over_ranks(e0.elapsed_time(e1)), "iterations": rc.iterations,
+               "converged": bool(rc.converged), "tol": tol, "last_delta": rc.last_delta,
+               "note": "W-rand SDNet weights: the fixed point is not physically meaningful (SURVEY exp-5)"}
+
+    cpu = None
+    if rank == 0 and world == 1:
+        rate, n, dt, thr = cpu_oracle_rate()
+        cpu = {"value": rate, "unit": "predictions/s", "cores": thr, "kind": "oracle",
+               "sample": f"{n} C5 phase-0 SDNet predictions (fp64 oracle, {dt:.1f} s)"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "predictions/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+                "config": {"workload": "C5: 4097x4097 points, m=32 (65,025 predictions/iteration), "
+                                       f"{T} MFP iterations + final phase per step",
+                           "nx": NX, "ny": NY, "m": 32, "iters_per_step": T, "grid": list(grid),
+                           "subsolver": "sdnet d=128 L_h=3 (W-rand)", "gelu": "tanh" if prec == mfp.BF16 else "erf",
+                           "l2": "flushed between steps (512 MB write, outside the events)",
+                           "parallelism": f"domain {grid[0]}x{grid[1]}"},
+                "points_iter_per_s": (NX + 1) * (NY + 1) * T * args.steps / (ms / 1000.0),
+                "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
+                "time_to_converge": ttc, "clocks": clk.summary(),
+                "halo": {"bytes_per_iter_rank0": rep.halo_bytes_sent / max(rep.iterations, 1),
+                         "msgs_per_iter": rep.halo_msgs_per_iter}}
+        print(json.dumps(line), flush=True)
+    m.close()
+    if comm is not None:
+        mfp.mfp_nccl_comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

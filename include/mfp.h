@@ -77,7 +77,11 @@ typedef enum {
   MFP_ERR_STATE = 8         /* context poisoned by an earlier CUDA/NCCL error     */
 } mfp_status;
 
-enum { MFP_FP32 = 0, MFP_BF16 = 1 };            /* precision of the SDNet chain    */
+/* Arithmetic of the SDNet MLP chain: FP32 = SIMT fp32 with exact-erf GELU (the
+ * parity twin); BF16 / FP16 = tcgen05 tensor cores with operands rounded to
+ * bf16 / fp16 and fp32 accumulation in TMEM (same throughput; fp16 has 8x
+ * smaller unit roundoff). */
+enum { MFP_FP32 = 0, MFP_BF16 = 1, MFP_FP16 = 2 };
 enum { MFP_SDNET = 0, MFP_EXACT_LAPLACE = 1 };  /* subdomain solver   */
 enum { MFP_QUERY_CENTRE = 0, MFP_QUERY_INTERIOR = 1 };
 
@@ -89,7 +93,7 @@ typedef struct {
   int32_t stride;      /* must be m/2 (paper d = 2)                           */
   int32_t grid_rows;   /* Py: processor rows    ((ny/m) % Py == 0)                  */
   int32_t grid_cols;   /* Px: processor columns ((nx/m) % Px == 0)                  */
-  int32_t precision;   /* MFP_FP32 (SIMT, exact-erf GELU) | MFP_BF16 (tcgen05)      */
+  int32_t precision;   /* MFP_FP32 | MFP_BF16 | MFP_FP16                             */
   int32_t subsolver;   /* MFP_SDNET | MFP_EXACT_LAPLACE                              */
   int32_t check_every; /* c >= 1: convergence test every c iterations                */
 } mfp_config;

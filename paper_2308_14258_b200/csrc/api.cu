@@ -1,0 +1,747 @@
+// api.cu — the C ABI of include/mfp.h: validation, workspace carving, device
+// preparation, the Algorithm-2 driver and its two transports:
+//   * NCCL (one process per GPU; grouped ncclSend/ncclRecv to the <= 8 stencil
+//     neighbours once per iteration; ncclAllReduce(MAX) for the
+//     convergence test; point-to-point gather of the owned blocks), and
+//   * local (MFP_ALL_RANKS: every rank of the processor grid on one device,
+//     exchange by device-to-device copies of the same packed buffers).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mfp_internal.h"
+
+
+using namespace mfp;
+
+namespace {
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base((char*)b) {}
+  template <class T>
+  T* take(size_t n) {
+    off = (off + 255) & ~(size_t)255;
+    T* p = base ? (T*)(base + off) : nullptr;
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+struct RankState {
+  RankPlan plan;
+  float* lat = nullptr;
+  float* snap = nullptr;
+  float* z = nullptr;
+  int64_t zcap = 0;
+  uint32_t* anchors[4] = {nullptr, nullptr, nullptr, nullptr};
+  uint32_t* final_anchor = nullptr;
+  uint32_t* final_lat_anchor = nullptr;
+  int64_t* segs = nullptr;
+  int nseg = 0;
+  int32_t* send_idx = nullptr;
+  int32_t* recv_idx = nullptr;
+  float* sendbuf = nullptr;
+  float* recvbuf = nullptr;
+  std::vector<int64_t> send_off, recv_off;
+  int64_t nsend = 0, nrecv = 0;
+  float* block = nullptr;  // owned block field (NCCL transport with R > 1)
+};
+
+}  // namespace
+
+struct mfp_ctx {
+  mfp_config cfg;
+  mfp_sdnet_desc net;
+  int rank = 0;          // this process's rank, or MFP_ALL_RANKS
+  int R = 1;
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr;
+  std::vector<RankState> ranks;
+  DevNet dn{};
+  float* params = nullptr;
+  float* full = nullptr;     // (ny+1)(nx+1) device field (rank 0 / ALL)
+  float* gstage = nullptr;   // 2(nx+ny)
+  float* gather = nullptr;   // rank 0, NCCL: other ranks' blocks
+  unsigned int* delta = nullptr;  // [2]
+  unsigned int* hdelta = nullptr;  // pinned
+  int num_sms = 148;
+  int launches = 0;
+  bool poisoned = false;
+  std::string err;
+  // profiling
+  bool profiling = false;
+  std::vector<cudaEvent_t> evpool;
+  size_t evnext = 0;
+  struct Span { cudaEvent_t a, b; int kind; int64_t units; };
+  std::vector<Span> spans;
+};
+
+namespace {
+
+const int kKindGather = 0, kKindChain = 1, kKindExact = 2, kKindHalo = 3, kKindDelta = 4;
+
+mfp_status fail(mfp_ctx* c, mfp_status st, const std::string& msg) {
+  if (c) {
+    c->err = msg;
+    if (st == MFP_ERR_CUDA || st == MFP_ERR_NCCL) c->poisoned = true;
+  }
+  return st;
+}
+
+#define CK(call)                                                                           \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(c, MFP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+#define NK(call)                                                                           \
+  do {                                                                                     \
+    ncclResult_t r_ = (call);                                                              \
+    if (r_ != ncclSuccess) {                                                               \
+      if (c && c->comm) ncclCommAbort(c->comm), c->comm = nullptr;                         \
+      return fail(c, MFP_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));    \
+    }                                                                                      \
+  } while (0)
+
+mfp_status check_net(const mfp_sdnet_desc* n, std::string* err) {
+  if (!n) { *err = "net is NULL"; return MFP_ERR_INVALID; }
+  if (n->n_conv != 2 || n->conv_k[0] != kK || n->conv_k[1] != kK || n->conv_ch[0] != 1 ||
+      n->conv_ch[1] != kC1 || n->conv_ch[2] != 1) {
+    *err = "round-1 SDNet: conv 1->8->1, k=5 (reading G7)";
+    return MFP_ERR_INVALID;
+  }
+  if (n->d != kD) { *err = "round-1 SDNet: d must be 128"; return MFP_ERR_INVALID; }
+  if (n->n_hidden < 1 || n->n_hidden > kMaxHidden) { *err = "n_hidden must be 1..3"; return MFP_ERR_INVALID; }
+  if (n->gelu != 0 && n->gelu != 1) { *err = "gelu must be 0 or 1"; return MFP_ERR_INVALID; }
+  return MFP_OK;
+}
+
+size_t param_count_of(const mfp_sdnet_desc* n) {
+  size_t p = 0;
+  for (int l = 0; l < n->n_conv; l++) {
+    p += (size_t)n->conv_ch[l + 1] * n->conv_ch[l] * n->conv_k[l];
+    p += (size_t)n->conv_ch[l + 1];
+  }
+  p += (size_t)n->d * n->conv_ch[n->n_conv] * kNB + (size_t)n->d * 2 + n->d;
+  p += (size_t)n->n_hidden * ((size_t)n->d * n->d + n->d);
+  p += (size_t)n->d + 1;
+  return p;
+}
+
+// Carve (or size, when base == nullptr) the workspace.
+void carve(mfp_ctx* c, void* base, size_t* total) {
+  Carver cv(base);
+  const int nh = c->net.n_hidden;
+  DevNet& dn = c->dn;
+  c->params = cv.take<float>(param_count_of(&c->net));
+  const float* P = c->params;
+  // parameter views (MFCK order)
+  dn.conv1_w = P; dn.conv1_b = P + 40; dn.conv2_w = P + 48; dn.conv2_b = P + 88;
+  const int64_t oW1 = 89, oW2 = oW1 + kD * kNB, ob1 = oW2 + 2 * kD, oWh0 = ob1 + kD;
+  const int64_t owo = oWh0 + (int64_t)nh * (kD * kD + kD);
+  dn.b1 = P ? P + ob1 : nullptr;
+  dn.wo = P ? P + owo : nullptr;
+  dn.bo = P ? P + owo + kD : nullptr;
+  dn.n_hidden = nh;
+  dn.gelu_tanh = c->net.gelu;
+  dn.f16 = c->cfg.precision == MFP_FP16 ? 1 : 0;
+  dn.W1T = cv.take<float>((size_t)kNB * kD);
+  dn.WhT = cv.take<float>((size_t)nh * kD * kD);
+  dn.bh = cv.take<float>((size_t)nh * kD);
+  dn.QTc = cv.take<float>((size_t)kD * 64);
+  dn.QTf = cv.take<float>((size_t)kD * kQF);
+  dn.Qc = cv.take<float>((size_t)64 * kD);
+  dn.Qf = cv.take<float>((size_t)kQF * kD);
+  dn.Wh_sw = cv.take<uint16_t>((size_t)nh * kD * kD);
+  dn.HcT = cv.take<float>((size_t)kNB * 64);
+  dn.HfT = cv.take<float>((size_t)kNB * kQF);
+  c->gstage = cv.take<float>((size_t)2 * (c->cfg.nx + c->cfg.ny));
+  c->delta = cv.take<unsigned int>(4);
+  const bool need_full = (c->rank == MFP_ALL_RANKS || c->rank == 0);
+  c->full = need_full ? cv.take<float>((size_t)(c->cfg.nx + 1) * (c->cfg.ny + 1)) : nullptr;
+  if (c->rank == 0 && c->R > 1) c->gather = cv.take<float>((size_t)(c->cfg.nx + 1) * (c->cfg.ny + 1));
+  for (auto& rs : c->ranks) {
+    const RankPlan& p = rs.plan;
+    rs.lat = cv.take<float>(p.lat.cells);
+    rs.snap = cv.take<float>(p.lat.cells);
+    int64_t zc = 1;
+    for (int k = 0; k < 4; k++) zc = std::max<int64_t>(zc, p.phase_anchor[k].size());
+    zc = std::max<int64_t>(zc, p.final_anchor.size());
+    zc = std::max<int64_t>(zc, 4096);  // staging for mfp_sdnet_batch chunks
+    rs.zcap = zc;
+    rs.z = cv.take<float>((size_t)zc * kD);
+    for (int k = 0; k < 4; k++) rs.anchors[k] = cv.take<uint32_t>(std::max<size_t>(1, p.phase_anchor[k].size()));
+    rs.final_anchor = cv.take<uint32_t>(std::max<size_t>(1, p.final_anchor.size()));
+    rs.final_lat_anchor = cv.take<uint32_t>(std::max<size_t>(1, p.final_lat_anchor.size()));
+    rs.nseg = (int)p.delta_seg.size();
+    rs.segs = cv.take<int64_t>(std::max<size_t>(1, p.delta_seg.size()));
+    rs.nsend = rs.nrecv = 0;
+    rs.send_off.clear(); rs.recv_off.clear();
+    for (auto& pp : p.peers) {
+      rs.send_off.push_back(rs.nsend); rs.nsend += pp.send_idx.size();
+      rs.recv_off.push_back(rs.nrecv); rs.nrecv += pp.recv_idx.size();
+    }
+    rs.send_idx = cv.take<int32_t>(std::max<int64_t>(1, rs.nsend));
+    rs.recv_idx = cv.take<int32_t>(std::max<int64_t>(1, rs.nrecv));
+    rs.sendbuf = cv.take<float>(std::max<int64_t>(1, rs.nsend));
+    rs.recvbuf = cv.take<float>(std::max<int64_t>(1, rs.nrecv));
+    rs.block = (c->rank != MFP_ALL_RANKS && c->R > 1) ? cv.take<float>((size_t)p.bw * p.bh) : nullptr;
+  }
+  *total = cv.off + 256;
+}
+
+Sink lattice_sink(RankState& rs, int kphase) {
+  Sink s{};
+  s.mode = 0; s.q = kQC; s.lat = rs.lat; s.offV = rs.plan.lat.offV;
+  s.strideH = rs.plan.lat.strideH; s.strideV = rs.plan.lat.strideV;
+  s.anchors = rs.anchors[kphase];
+  return s;
+}
+
+cudaEvent_t ev(mfp_ctx* c) {
+  if (c->evnext >= c->evpool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->evpool.push_back(e);
+  }
+  return c->evpool[c->evnext++];
+}
+
+struct SpanGuard {
+  mfp_ctx* c; int kind; int64_t units; cudaEvent_t a = nullptr;
+  SpanGuard(mfp_ctx* c_, int k, int64_t u) : c(c_), kind(k), units(u) {
+    if (c->profiling) { a = ev(c); cudaEventRecord(a, c->stream); }
+  }
+  ~SpanGuard() {
+    if (c->profiling) {
+      cudaEvent_t b = ev(c);
+      cudaEventRecord(b, c->stream);
+      c->spans.push_back({a, b, kind, units});
+    }
+  }
+};
+
+void chain(mfp_ctx* c, const float* z, int64_t B, int q, const Sink& sk) {
+  SpanGuard g(c, kKindChain, B * q);
+  if (c->cfg.precision != MFP_FP32) launch_chain_tc(z, B, q, c->dn, sk, c->num_sms, c->stream);
+  else launch_chain_fp32(z, B, q, c->dn, sk, c->stream);
+  c->launches++;
+}
+
+void run_phase(mfp_ctx* c, RankState& rs, int ph) {
+  const int64_t B = (int64_t)rs.plan.phase_anchor[ph].size();
+  if (B == 0) return;
+  if (c->cfg.subsolver == MFP_EXACT_LAPLACE) {
+    SpanGuard g(c, kKindExact, B);
+    launch_exact_phase(rs.lat, rs.plan.lat, rs.anchors[ph], B, c->dn.HcT, c->stream);
+    c->launches++;
+  } else {
+    {
+      SpanGuard g(c, kKindGather, B);
+      launch_gather_embed(rs.lat, rs.plan.lat, rs.anchors[ph], nullptr, B, c->dn, rs.z, c->stream);
+      c->launches++;
+    }
+    chain(c, rs.z, B, kQC, lattice_sink(rs, ph));
+  }
+}
+
+// communicate_new_boundaries: pack -> exchange -> unpack, once per iteration
+mfp_status exchange(mfp_ctx* c) {
+  if (c->R == 1) return MFP_OK;
+  SpanGuard g(c, kKindHalo, 0);
+  for (auto& rs : c->ranks) {
+    launch_pack(rs.lat, rs.send_idx, rs.nsend, rs.sendbuf, c->stream);
+    c->launches++;
+  }
+  if (c->rank == MFP_ALL_RANKS) {
+    for (auto& dst : c->ranks)
+      for (size_t i = 0; i < dst.plan.peers.size(); i++) {
+        const RankState& src = c->ranks[dst.plan.peers[i].rank];
+        // find dst in src's peer list
+        size_t j = 0;
+        while (j < src.plan.peers.size() && src.plan.peers[j].rank != dst.plan.rank) j++;
+        const int64_t n = (int64_t)dst.plan.peers[i].recv_idx.size();
+        if (n == 0) continue;
+        CK(cudaMemcpyAsync(dst.recvbuf + dst.recv_off[i], src.sendbuf + src.send_off[j],
+                           n * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+      }
+  } else {
+    RankState& rs = c->ranks[0];
+    NK(ncclGroupStart());
+    for (size_t i = 0; i < rs.plan.peers.size(); i++) {
+      const auto& pp = rs.plan.peers[i];
+      if (!pp.send_idx.empty())
+        NK(ncclSend(rs.sendbuf + rs.send_off[i], pp.send_idx.size(), ncclFloat32, pp.rank, c->comm, c->stream));
+      if (!pp.recv_idx.empty())
+        NK(ncclRecv(rs.recvbuf + rs.recv_off[i], pp.recv_idx.size(), ncclFloat32, pp.rank, c->comm, c->stream));
+    }
+    NK(ncclGroupEnd());
+  }
+  for (auto& rs : c->ranks) {
+    launch_unpack(rs.lat, rs.recv_idx, rs.nrecv, rs.recvbuf, c->stream);
+    c->launches++;
+  }
+  return MFP_OK;
+}
+
+// delta_k (reading G5) -> host, max over ranks; returns nonfinite flag
+mfp_status reduce_delta(mfp_ctx* c, float* delta, bool* nonfinite) {
+  CK(cudaMemsetAsync(c->delta, 0, 2 * sizeof(unsigned int), c->stream));
+  {
+    SpanGuard g(c, kKindDelta, 0);
+    for (auto& rs : c->ranks) {
+      launch_delta(rs.lat, rs.snap, rs.segs, rs.nseg, c->delta, c->stream);
+      c->launches++;
+    }
+  }
+  if (c->comm) NK(ncclAllReduce(c->delta, c->delta, 2, ncclUint32, ncclMax, c->comm, c->stream));
+  CK(cudaMemcpyAsync(c->hdelta, c->delta, 2 * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  uint32_t bits = c->hdelta[0];
+  float d;
+  memcpy(&d, &bits, 4);
+  *delta = d;
+  *nonfinite = c->hdelta[1] != 0;
+  return MFP_OK;
+}
+
+// Final phase into the device field u (row-major, ld = nx+1).
+mfp_status final_phase(mfp_ctx* c, float* u) {
+  const int W = c->cfg.nx + 1;
+  for (auto& rs : c->ranks) {
+    const RankPlan& p = rs.plan;
+    float* field;
+    int ld;
+    if (rs.block) { field = rs.block; ld = p.bw; }
+    else { field = u + (int64_t)p.Y0 * W + p.X0; ld = W; }
+    launch_final_lines(rs.lat, p.lat, p.X0, p.Y0, p.bw, p.bh, field, ld, c->stream);
+    c->launches++;
+    const int64_t B = (int64_t)p.final_anchor.size();
+    if (B == 0) continue;
+    Sink sk{};
+    sk.mode = 1; sk.q = kQF; sk.anchors = rs.final_anchor; sk.field = field; sk.ld = ld;
+    if (c->cfg.subsolver == MFP_EXACT_LAPLACE) {
+      launch_exact_general(rs.lat, p.lat, rs.final_lat_anchor, nullptr, B, kQF, c->dn.HfT, sk, c->stream);
+      c->launches++;
+    } else {
+      for (int64_t s0 = 0; s0 < B; s0 += rs.zcap) {
+        const int64_t nb = std::min(rs.zcap, B - s0);
+        launch_gather_embed(rs.lat, p.lat, rs.final_lat_anchor + s0, nullptr, nb, c->dn, rs.z, c->stream);
+        Sink sk2 = sk;
+        sk2.anchors = rs.final_anchor + s0;
+        c->launches++;
+        chain(c, rs.z, nb, kQF, sk2);
+      }
+    }
+  }
+  if (c->rank != MFP_ALL_RANKS && c->R > 1) {
+    // gather of the owned blocks to rank 0 (the paper's all_gather)
+    RankState& rs = c->ranks[0];
+    if (c->rank == 0) {
+      GlobalPlan gp;
+      std::string err;
+      build_plan(&c->cfg, MFP_ALL_RANKS, &gp, &err);
+      std::vector<int64_t> off(c->R, 0);
+      int64_t o = 0;
+      for (int r = 1; r < c->R; r++) { off[r] = o; o += (int64_t)gp.ranks[r].bw * gp.ranks[r].bh; }
+      NK(ncclGroupStart());
+      for (int r = 1; r < c->R; r++)
+        NK(ncclRecv(c->gather + off[r], (size_t)gp.ranks[r].bw * gp.ranks[r].bh, ncclFloat32, r, c->comm, c->stream));
+      NK(ncclGroupEnd());
+      CK(cudaMemcpy2DAsync(u + (int64_t)rs.plan.Y0 * W + rs.plan.X0, W * sizeof(float), rs.block,
+                           rs.plan.bw * sizeof(float), rs.plan.bw * sizeof(float), rs.plan.bh,
+                           cudaMemcpyDeviceToDevice, c->stream));
+      for (int r = 1; r < c->R; r++) {
+        const RankPlan& q = gp.ranks[r];
+        CK(cudaMemcpy2DAsync(u + (int64_t)q.Y0 * W + q.X0, W * sizeof(float), c->gather + off[r],
+                             q.bw * sizeof(float), q.bw * sizeof(float), q.bh, cudaMemcpyDeviceToDevice,
+                             c->stream));
+      }
+    } else {
+      NK(ncclSend(rs.block, (size_t)rs.plan.bw * rs.plan.bh, ncclFloat32, 0, c->comm, c->stream));
+    }
+  }
+  return MFP_OK;
+}
+
+mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, float* u_dev, bool do_final,
+                      mfp_report* rep) {
+  if (c->poisoned) return MFP_ERR_STATE;
+  if (t < 1 || !(tol >= 0.f)) return fail(c, MFP_ERR_INVALID, "max_iters >= 1 and tol >= 0 required");
+  cudaEvent_t e0, e1, e2;
+  CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1)); CK(cudaEventCreate(&e2));
+  c->launches = 0;
+  CK(cudaEventRecord(e0, c->stream));
+  if (g_dev) {
+    for (auto& rs : c->ranks) {
+      launch_init_lattice(rs.lat, rs.plan.lat, c->cfg.nx, c->cfg.ny, g_dev, c->stream);
+      c->launches += 1;
+    }
+  }
+  const int ce = c->cfg.check_every;
+  int it = 0;
+  bool converged = false;
+  float delta = -1.f;
+  for (it = 1; it <= t; it++) {
+    const bool check = (tol > 0.f && it % ce == 0) || it == t;
+    if (check)
+      for (auto& rs : c->ranks)
+        CK(cudaMemcpyAsync(rs.snap, rs.lat, rs.plan.lat.cells * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    for (int ph = 0; ph < 4; ph++)
+      for (auto& rs : c->ranks) run_phase(c, rs, ph);
+    mfp_status st = exchange(c);
+    if (st) return st;
+    if (check) {
+      bool bad = false;
+      st = reduce_delta(c, &delta, &bad);
+      if (st) return st;
+      if (bad) return fail(c, MFP_ERR_NONFINITE, "non-finite prediction (S:345)");
+      if (tol > 0.f && it % ce == 0 && delta <= tol) { converged = true; break; }
+    }
+  }
+  if (it > t) it = t;
+  CK(cudaEventRecord(e1, c->stream));
+  if (do_final) {
+    mfp_status st = final_phase(c, u_dev);
+    if (st) return st;
+  }
+  CK(cudaEventRecord(e2, c->stream));
+  CK(cudaEventSynchronize(e2));
+  CK(cudaGetLastError());
+  if (rep) {
+    memset(rep, 0, sizeof(*rep));
+    rep->iterations = it;
+    rep->converged = converged ? 1 : 0;
+    rep->last_delta = delta;
+    const double Kx = c->cfg.nx / kM, Ky = c->cfg.ny / kM;
+    rep->predictions = (2 * Kx - 1) * (2 * Ky - 1) * it;
+    double comp = 0;
+    for (auto& rs : c->ranks)
+      for (int k = 0; k < 4; k++) comp += rs.plan.phase_anchor[k].size();
+    rep->predictions_computed = comp * it;
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e2); rep->ms_total = ms;
+    cudaEventElapsedTime(&ms, e1, e2); rep->ms_final = ms;
+    int64_t bytes = 0;
+    int msgs = 0;
+    for (auto& rs : c->ranks) {
+      bytes += rs.nsend * 4;
+      int m = 0;
+      for (auto& pp : rs.plan.peers) m += !pp.send_idx.empty();
+      msgs = std::max(msgs, m);
+    }
+    rep->halo_bytes_sent = bytes * it;
+    rep->halo_msgs_per_iter = msgs;
+    rep->gpu_launches = c->launches;
+  }
+  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
+  if (tol > 0.f && !converged) return MFP_NOT_CONVERGED;
+  return MFP_OK;
+}
+
+}  // namespace
+
+// ============================================================== C ABI
+extern "C" {
+
+mfp_status mfp_param_count(const mfp_sdnet_desc* net, int32_t m, size_t* n) {
+  std::string err;
+  if (!n || m != kM) return MFP_ERR_INVALID;
+  mfp_status st = check_net(net, &err);
+  if (st) return st;
+  *n = param_count_of(net);
+  return MFP_OK;
+}
+
+mfp_status mfp_workspace_size(const mfp_config* cfg, const mfp_sdnet_desc* net, int rank, size_t* bytes) {
+  if (!bytes) return MFP_ERR_INVALID;
+  std::string err;
+  mfp_ctx tmp;
+  mfp_status st = check_net(net, &err);
+  if (st) return st;
+  GlobalPlan gp;
+  st = build_plan(cfg, rank, &gp, &err);
+  if (st) return st;
+  tmp.cfg = *cfg; tmp.net = *net; tmp.rank = rank; tmp.R = gp.R;
+  tmp.ranks.resize(gp.ranks.size());
+  for (size_t i = 0; i < gp.ranks.size(); i++) tmp.ranks[i].plan = std::move(gp.ranks[i]);
+  carve(&tmp, nullptr, bytes);
+  return MFP_OK;
+}
+
+const char* mfp_last_error(const mfp_ctx* c) { return c ? c->err.c_str() : "ctx is NULL"; }
+
+mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const float* params,
+                    size_t n_params, int rank, void* nccl_comm, void* workspace, size_t ws_bytes,
+                    void* stream, mfp_ctx** out) {
+  if (!out) return MFP_ERR_INVALID;
+  *out = nullptr;
+  mfp_ctx* c = new mfp_ctx();
+  *out = c;
+  std::string err;
+  mfp_status st = check_net(net, &err);
+  if (st) return fail(c, st, err);
+  GlobalPlan gp;
+  st = build_plan(cfg, rank, &gp, &err);
+  if (st) return fail(c, st, err);
+  c->cfg = *cfg; c->net = *net; c->rank = rank; c->R = gp.R;
+  if (gp.R > 1 && rank != MFP_ALL_RANKS && !nccl_comm)
+    return fail(c, MFP_ERR_INVALID, "nccl_comm required for a multi-rank grid");
+  if ((gp.R == 1 || rank == MFP_ALL_RANKS) && nccl_comm)
+    return fail(c, MFP_ERR_INVALID, "nccl_comm must be NULL for single-rank / MFP_ALL_RANKS");
+  c->comm = (ncclComm_t)nccl_comm;
+  c->stream = (cudaStream_t)stream;
+  if (cfg->subsolver == MFP_SDNET) {
+    if (!params) return fail(c, MFP_ERR_INVALID, "params required for the SDNet subsolver");
+    if (n_params != param_count_of(net)) return fail(c, MFP_ERR_INVALID, "n_params mismatch (S:387 order)");
+    for (size_t i = 0; i < n_params; i++)
+      if (!std::isfinite(params[i])) return fail(c, MFP_ERR_NONFINITE, "non-finite parameter");
+  }
+  if (cfg->precision != MFP_FP32 && cfg->subsolver == MFP_SDNET && !chain_tc_available())
+    return fail(c, MFP_ERR_INVALID, "tcgen05 chain not built into this library");
+  int dev = 0;
+  cudaDeviceProp prop;
+  CK(cudaGetDevice(&dev));
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10) return fail(c, MFP_ERR_CUDA, "libmfp requires an sm_100 (B200) device");
+  c->num_sms = prop.multiProcessorCount;
+  c->ranks.resize(gp.ranks.size());
+  for (size_t i = 0; i < gp.ranks.size(); i++) c->ranks[i].plan = std::move(gp.ranks[i]);
+  size_t need = 0;
+  carve(c, nullptr, &need);
+  if (!workspace || ws_bytes < need || ((uintptr_t)workspace & 255))
+    return fail(c, MFP_ERR_WORKSPACE, "workspace too small or not 256-byte aligned");
+  carve(c, workspace, &need);
+  CK(cudaMallocHost(&c->hdelta, 4 * sizeof(unsigned int)));
+  cudaStream_t s = c->stream;
+  // upload plan tables
+  for (auto& rs : c->ranks) {
+    const RankPlan& p = rs.plan;
+    for (int k = 0; k < 4; k++)
+      if (!p.phase_anchor[k].empty())
+        CK(cudaMemcpyAsync(rs.anchors[k], p.phase_anchor[k].data(), p.phase_anchor[k].size() * 4, cudaMemcpyHostToDevice, s));
+    if (!p.final_anchor.empty()) {
+      CK(cudaMemcpyAsync(rs.final_anchor, p.final_anchor.data(), p.final_anchor.size() * 4, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(rs.final_lat_anchor, p.final_lat_anchor.data(), p.final_lat_anchor.size() * 4, cudaMemcpyHostToDevice, s));
+    }
+    if (!p.delta_seg.empty())
+      CK(cudaMemcpyAsync(rs.segs, p.delta_seg.data(), p.delta_seg.size() * 8, cudaMemcpyHostToDevice, s));
+    for (size_t i = 0; i < p.peers.size(); i++) {
+      const auto& pp = p.peers[i];
+      if (!pp.send_idx.empty())
+        CK(cudaMemcpyAsync(rs.send_idx + rs.send_off[i], pp.send_idx.data(), pp.send_idx.size() * 4, cudaMemcpyHostToDevice, s));
+      if (!pp.recv_idx.empty())
+        CK(cudaMemcpyAsync(rs.recv_idx + rs.recv_off[i], pp.recv_idx.data(), pp.recv_idx.size() * 4, cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaMemsetAsync(rs.lat, 0, p.lat.cells * sizeof(float), s));
+  }
+  if (cfg->subsolver == MFP_SDNET) {
+    CK(cudaMemcpyAsync(c->params, params, n_params * sizeof(float), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync((void*)c->dn.Wh_sw, 0, (size_t)net->n_hidden * kD * kD * 2, s));
+    PrepArgs a;
+    a.P = c->params; a.n_hidden = net->n_hidden; a.f16 = cfg->precision == MFP_FP16 ? 1 : 0;
+    a.oW1 = 89; a.oW2 = 89 + kD * kNB; a.oWh0 = a.oW2 + 2 * kD + kD;
+    a.W1T = (float*)c->dn.W1T; a.WhT = (float*)c->dn.WhT; a.bh = (float*)c->dn.bh;
+    a.QTc = (float*)c->dn.QTc; a.QTf = (float*)c->dn.QTf; a.Qc = (float*)c->dn.Qc; a.Qf = (float*)c->dn.Qf;
+    a.Wsw = (uint16_t*)c->dn.Wh_sw;
+    launch_prep(a, s);
+  } else {
+    launch_harmonic(kQC, (float*)c->dn.HcT, s);
+    launch_harmonic(kQF, (float*)c->dn.HfT, s);
+  }
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  return MFP_OK;
+}
+
+void mfp_destroy(mfp_ctx* c) {
+  if (!c) return;
+  for (auto e : c->evpool) cudaEventDestroy(e);
+  if (c->hdelta) cudaFreeHost(c->hdelta);
+  delete c;
+}
+
+// u pointers: the final phase runs iff the caller passes a non-NULL field
+// pointer; the call is collective, so with NCCL every rank passes non-NULL
+// (only rank 0's buffer is written) or every rank passes NULL.
+mfp_status mfp_solve_device(mfp_ctx* c, const float* g_dev, int32_t max_iters, float tol, float* u_dev,
+                            mfp_report* rep) {
+  if (!c) return MFP_ERR_INVALID;
+  if (c->poisoned) return MFP_ERR_STATE;
+  const bool root = (c->rank == 0 || c->rank == MFP_ALL_RANKS);
+  float* u = u_dev ? (root ? u_dev : c->ranks[0].block) : nullptr;
+  return solve_impl(c, g_dev, max_iters, tol, u, u_dev != nullptr, rep);
+}
+
+mfp_status mfp_solve(mfp_ctx* c, const float* g, int32_t max_iters, float tol, float* u_out, mfp_report* rep) {
+  if (!c) return MFP_ERR_INVALID;
+  if (c->poisoned) return MFP_ERR_STATE;
+  const size_t ng = 2 * (size_t)(c->cfg.nx + c->cfg.ny);
+  const float* gd = nullptr;
+  if (g) {
+    for (size_t i = 0; i < ng; i++)
+      if (!std::isfinite(g[i])) return fail(c, MFP_ERR_NONFINITE, "non-finite boundary value");
+    CK(cudaMemcpyAsync(c->gstage, g, ng * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    gd = c->gstage;
+  }
+  const bool root = (c->rank == 0 || c->rank == MFP_ALL_RANKS);
+  float* u = u_out ? (root ? c->full : c->ranks[0].block) : nullptr;
+  mfp_status st = solve_impl(c, gd, max_iters, tol, u, u_out != nullptr, rep);
+  if (st != MFP_OK && st != MFP_NOT_CONVERGED) return st;
+  if (root && u_out) {
+    const size_t nu = (size_t)(c->cfg.nx + 1) * (c->cfg.ny + 1);
+    CK(cudaMemcpyAsync(u_out, c->full, nu * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  return st;
+}
+
+mfp_status mfp_sdnet_batch(mfp_ctx* c, const float* gb, int64_t B, int32_t query_set, float* out, void* stream) {
+  if (!c) return MFP_ERR_INVALID;
+  if (c->poisoned) return MFP_ERR_STATE;
+  if (B < 0 || (B > 0 && (!gb || !out)) || (query_set != MFP_QUERY_CENTRE && query_set != MFP_QUERY_INTERIOR))
+    return fail(c, MFP_ERR_INVALID, "bad sdnet_batch arguments");
+  cudaStream_t saved = c->stream;
+  if (stream) c->stream = (cudaStream_t)stream;
+  const int q = query_set == MFP_QUERY_CENTRE ? kQC : kQF;
+  RankState& rs = c->ranks[0];
+  for (int64_t s0 = 0; s0 < B; s0 += rs.zcap) {
+    const int64_t nb = std::min(rs.zcap, B - s0);
+    Sink sk{};
+    sk.mode = 2; sk.q = q; sk.out = out + s0 * q;
+    if (c->cfg.subsolver == MFP_EXACT_LAPLACE) {
+      launch_exact_general(nullptr, rs.plan.lat, nullptr, gb + s0 * kNB, nb, q,
+                           q == kQC ? c->dn.HcT : c->dn.HfT, sk, c->stream);
+    } else {
+      {
+        SpanGuard g(c, kKindGather, nb);
+        launch_gather_embed(nullptr, rs.plan.lat, nullptr, gb + s0 * kNB, nb, c->dn, rs.z, c->stream);
+      }
+      chain(c, rs.z, nb, q, sk);
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  c->stream = saved;
+  if (e != cudaSuccess) return fail(c, MFP_ERR_CUDA, cudaGetErrorString(e));
+  return MFP_OK;
+}
+
+mfp_status mfp_step_phase(mfp_ctx* c, int32_t phase) {
+  if (!c) return MFP_ERR_INVALID;
+  if (c->poisoned) return MFP_ERR_STATE;
+  if (phase < 0 || phase > 3) return fail(c, MFP_ERR_INVALID, "phase must be 0..3");
+  for (auto& rs : c->ranks) run_phase(c, rs, phase);
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaGetLastError());
+  return MFP_OK;
+}
+
+static mfp_status lines_io(mfp_ctx* c, int32_t rank, float* hl, float* vl, const float* hin, const float* vin) {
+  if (!c) return MFP_ERR_INVALID;
+  if (c->poisoned) return MFP_ERR_STATE;
+  int idx = c->rank == MFP_ALL_RANKS ? rank : 0;
+  if (idx < 0 || idx >= (int)c->ranks.size()) return fail(c, MFP_ERR_INVALID, "rank out of range");
+  RankState& rs = c->ranks[idx];
+  const LatticeGeom& L = rs.plan.lat;
+  if (hl || hin) {
+    if (hin) CK(cudaMemcpy2DAsync(rs.lat, L.strideH * 4, hin, L.lenH * 4, L.lenH * 4, L.nH, cudaMemcpyHostToDevice, c->stream));
+    else CK(cudaMemcpy2DAsync(hl, L.lenH * 4, rs.lat, L.strideH * 4, L.lenH * 4, L.nH, cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (vl || vin) {
+    if (vin) CK(cudaMemcpy2DAsync(rs.lat + L.offV, L.strideV * 4, vin, L.lenV * 4, L.lenV * 4, L.nV, cudaMemcpyHostToDevice, c->stream));
+    else CK(cudaMemcpy2DAsync(vl, L.lenV * 4, rs.lat + L.offV, L.strideV * 4, L.lenV * 4, L.nV, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return MFP_OK;
+}
+
+mfp_status mfp_export_lines(mfp_ctx* c, int32_t rank, float* hl, float* vl) {
+  return lines_io(c, rank, hl, vl, nullptr, nullptr);
+}
+mfp_status mfp_import_lines(mfp_ctx* c, int32_t rank, const float* hl, const float* vl) {
+  if (!hl || !vl) return MFP_ERR_INVALID;
+  return lines_io(c, rank, nullptr, nullptr, hl, vl);
+}
+
+mfp_status mfp_profile_iterations(mfp_ctx* c, int32_t iters, mfp_profile* o) {
+  if (!c || !o || iters < 1) return MFP_ERR_INVALID;
+  if (c->poisoned) return MFP_ERR_STATE;
+  memset(o, 0, sizeof(*o));
+  c->profiling = true;
+  c->spans.clear();
+  c->evnext = 0;
+  c->launches = 0;
+  cudaEvent_t a = ev(c), b = ev(c);
+  CK(cudaEventRecord(a, c->stream));
+  for (int it = 0; it < iters; it++) {
+    for (int ph = 0; ph < 4; ph++)
+      for (auto& rs : c->ranks) run_phase(c, rs, ph);
+    mfp_status st = exchange(c);
+    if (st) { c->profiling = false; return st; }
+  }
+  CK(cudaEventRecord(b, c->stream));
+  CK(cudaEventSynchronize(b));
+  c->profiling = false;
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  o->iterations = iters;
+  o->ms_per_iter = ms / iters;
+  o->launches_per_iter = c->launches / iters;
+  double tg = 0, tc = 0, te = 0, th = 0, td = 0;
+  int64_t ng = 0, nc = 0, ne = 0, nhh = 0, nd = 0;
+  for (auto& sp : c->spans) {
+    cudaEventElapsedTime(&ms, sp.a, sp.b);
+    switch (sp.kind) {
+      case kKindGather: tg += ms; ng++; o->gather_subdomains += sp.units; break;
+      case kKindChain: tc += ms; nc++; o->chain_rows += sp.units; break;
+      case kKindExact: te += ms; ne++; break;
+      case kKindHalo: th += ms; nhh++; break;
+      default: td += ms; nd++; break;
+    }
+  }
+  o->ms_gather_embed = ng ? tg / ng : 0;
+  o->ms_chain = nc ? tc / nc : 0;
+  o->ms_exact = ne ? te / ne : 0;
+  o->ms_halo = nhh ? th / nhh : 0;
+  o->ms_delta = nd ? td / nd : 0;
+  o->chain_launches = nc; o->chain_ms_total = tc;
+  o->gather_launches = ng; o->gather_ms_total = tg;
+  c->spans.clear();
+  c->evnext = 0;
+  CK(cudaGetLastError());
+  return MFP_OK;
+}
+
+// ------------------------------------------------------------ NCCL bootstrap
+mfp_status mfp_nccl_get_unique_id(void* id_out) {
+  if (!id_out) return MFP_ERR_INVALID;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return MFP_ERR_NCCL;
+  memcpy(id_out, &id, sizeof(id));
+  return MFP_OK;
+}
+
+mfp_status mfp_nccl_comm_init(int32_t nranks, const void* id, int32_t rank, void** comm_out) {
+  if (!id || !comm_out || nranks < 1 || rank < 0 || rank >= nranks) return MFP_ERR_INVALID;
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclComm_t comm;
+  if (ncclCommInitRank(&comm, nranks, uid, rank) != ncclSuccess) return MFP_ERR_NCCL;
+  *comm_out = comm;
+  return MFP_OK;
+}
+
+mfp_status mfp_nccl_comm_destroy(void* comm) {
+  if (!comm) return MFP_ERR_INVALID;
+  return ncclCommDestroy((ncclComm_t)comm) == ncclSuccess ? MFP_OK : MFP_ERR_NCCL;
+}
+
+}  // extern "C"

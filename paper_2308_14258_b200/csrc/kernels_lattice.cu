@@ -1,0 +1,224 @@
+// kernels_lattice.cu — line-lattice kernels of libmfp: init (a0), exact
+// discrete-Laplace subsolver phase (N9), convergence reduction (N6, a8), halo
+// pack/unpack (N7, a7), final-phase line copy (a9).  HBM-bound or latency-bound
+// work: coalesced line segments, grids sized in multiples of the SM count.
+#include "device_common.cuh"
+
+namespace mfp {
+
+// ---------------------------------------------------------------- a0: init
+// g (2(nx+ny), reading G6) onto the boundary lines of the local lattice; the
+// interior lines were zeroed by cudaMemsetAsync (initial guess 0).
+__global__ void k_init_boundary(float* __restrict__ lat, LatticeGeom L, int nx, int ny,
+                                const float* __restrict__ g) {
+  const int n = 2 * (nx + ny);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    int x, y;
+    if (k < nx) { x = k; y = 0; }
+    else if (k < nx + ny) { x = nx; y = k - nx; }
+    else if (k < 2 * nx + ny) { x = nx - (k - nx - ny); y = ny; }
+    else { x = 0; y = ny - (k - 2 * nx - ny); }
+    if (x < L.RX0 || x > L.RX1 || y < L.RY0 || y > L.RY1) continue;
+    const float v = __ldg(g + k);
+    if (y % kH == 0) lat[(int64_t)((y - L.RY0) / kH) * L.strideH + (x - L.RX0)] = v;
+    if (x % kH == 0) lat[L.offV + (int64_t)((x - L.RX0) / kH) * L.strideV + (y - L.RY0)] = v;
+  }
+}
+
+void launch_init_lattice(float* lat, const LatticeGeom& L, int nx, int ny, const float* g,
+                         cudaStream_t s) {
+  cudaMemsetAsync(lat, 0, sizeof(float) * L.cells, s);
+  int n = 2 * (nx + ny);
+  int blocks = (n + 255) / 256;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  k_init_boundary<<<blocks, 256, 0, s>>>(lat, L, nx, ny, g);
+}
+
+// ---------------------------------------------------- N9: exact subsolver phase
+// One warp per subdomain: gather the 128 perimeter values (4 coalesced 128 B
+// edge segments), y = H_c g (61 x 128, H_c^T resident in shared memory), write
+// the centre lines.  Reads and writes of one class are disjoint,
+// so gather and scatter fuse into one kernel without a grid barrier.
+constexpr int kExactWarps = 8;
+
+__global__ void __launch_bounds__(kExactWarps * 32)
+k_exact_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ anchors,
+              int64_t B, const float* __restrict__ HcT) {
+  __shared__ float sH[kNB * 64];               // H_c^T [k][p], p padded to 64
+  __shared__ float sg[kExactWarps][kNB];
+  for (int i = threadIdx.x; i < kNB * 64; i += blockDim.x) sH[i] = __ldg(HcT + i);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * kExactWarps;
+  for (int64_t s = (int64_t)blockIdx.x * kExactWarps + warp; s < B; s += nwarps) {
+    int a, b;
+    unpack_anchor(__ldg(anchors + s), a, b);
+#pragma unroll
+    for (int e = 0; e < 4; e++)
+      sg[warp][e * 32 + lane] = lat[perim_cell(a, b, e * 32 + lane, L.strideH, L.strideV, L.offV)];
+    __syncwarp();
+    float y0 = 0.f, y1 = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < kNB; k++) {
+      const float gk = sg[warp][k];
+      y0 = fmaf(sH[k * 64 + lane], gk, y0);
+      y1 = fmaf(sH[k * 64 + 32 + lane], gk, y1);
+    }
+    __syncwarp();
+    int64_t dup;
+    int64_t c0 = centre_cell(a, b, lane, L.strideH, L.strideV, L.offV, &dup);
+    lat[c0] = y0;
+    if (dup >= 0) lat[dup] = y0;
+    if (lane + 32 < kQC) {
+      int64_t c1 = centre_cell(a, b, lane + 32, L.strideH, L.strideV, L.offV, &dup);
+      lat[c1] = y1;
+    }
+  }
+}
+
+void launch_exact_phase(float* lat, const LatticeGeom& L, const uint32_t* anchors, int64_t B,
+                        const float* HcT, cudaStream_t s) {
+  if (B <= 0) return;
+  int64_t blocks = (B + kExactWarps - 1) / kExactWarps;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_exact_phase<<<(int)blocks, kExactWarps * 32, 0, s>>>(lat, L, anchors, B, HcT);
+}
+
+// Exact subsolver, general query set (final phase / batch API): a block takes
+// up to 8 subdomains so every H^T element read from L2 is reused 8 times.
+constexpr int kExactGroup = 8;
+
+__global__ void __launch_bounds__(256)
+k_exact_general(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ lat_anchors,
+                const float* __restrict__ gb, int64_t B, int q, const float* __restrict__ HT,
+                Sink sink) {
+  __shared__ float sg[kExactGroup][kNB];
+  for (int64_t s0 = (int64_t)blockIdx.x * kExactGroup; s0 < B; s0 += (int64_t)gridDim.x * kExactGroup) {
+    const int ns = (int)min((int64_t)kExactGroup, B - s0);
+    for (int i = threadIdx.x; i < kExactGroup * kNB; i += blockDim.x) {
+      int j = i / kNB, k = i % kNB;
+      float v = 0.f;
+      if (j < ns) {
+        if (gb) v = __ldg(gb + (s0 + j) * kNB + k);
+        else {
+          int a, b;
+          unpack_anchor(__ldg(lat_anchors + s0 + j), a, b);
+          v = lat[perim_cell(a, b, k, L.strideH, L.strideV, L.offV)];
+        }
+      }
+      sg[j][k] = v;
+    }
+    __syncthreads();
+    const int ld = (q == kQC) ? 64 : q;  // H_c^T is stored [128][64]
+    for (int p = threadIdx.x; p < q; p += blockDim.x) {
+      float acc[kExactGroup];
+#pragma unroll
+      for (int j = 0; j < kExactGroup; j++) acc[j] = 0.f;
+      for (int k = 0; k < kNB; k++) {
+        const float h = __ldg(HT + (int64_t)k * ld + p);
+#pragma unroll
+        for (int j = 0; j < kExactGroup; j++) acc[j] = fmaf(h, sg[j][k], acc[j]);
+      }
+      for (int j = 0; j < ns; j++) sink_store(sink, s0 + j, p, acc[j]);
+    }
+    __syncthreads();
+  }
+}
+
+void launch_exact_general(const float* lat, const LatticeGeom& L, const uint32_t* lat_anchors,
+                          const float* gb, int64_t B, int q, const float* HT, const Sink& sink,
+                          cudaStream_t s) {
+  if (B <= 0) return;
+  int64_t blocks = (B + kExactGroup - 1) / kExactGroup;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_exact_general<<<(int)blocks, 256, 0, s>>>(lat, L, lat_anchors, gb, B, q, HT, sink);
+}
+
+// ------------------------------------------------------ N6: convergence delta
+// delta = max |U_k - U_{k-1}| over the owned interior line cells (reading G5),
+// one block per contiguous line segment, warp-shuffle max, one atomicMax on the
+// fp32 bit pattern (non-negative floats order like unsigned ints).
+__global__ void __launch_bounds__(256)
+k_delta(const float* __restrict__ lat, const float* __restrict__ snap,
+        const int64_t* __restrict__ segs, int nseg, unsigned int* out) {
+  __shared__ float red[8];
+  float m = 0.f;
+  bool bad = false;
+  for (int sgi = blockIdx.x; sgi < nseg; sgi += gridDim.x) {
+    const int64_t sd = __ldg(segs + sgi);
+    const int64_t off = sd >> 20;
+    const int len = (int)(sd & 0xfffff);
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      const float d = fabsf(lat[off + i] - snap[off + i]);
+      if (!(d <= 3.0e38f)) bad = true;   // NaN or Inf
+      else m = fmaxf(m, d);
+    }
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(out + 1, 1u);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_max(v);
+    if (threadIdx.x == 0) atomicMax(out, __float_as_uint(v));
+  }
+}
+
+void launch_delta(const float* lat, const float* snap, const int64_t* segs, int nseg,
+                  unsigned int* out, cudaStream_t s) {
+  // out is zeroed by the caller once per check (max accumulates over local ranks)
+  if (nseg <= 0) return;
+  int blocks = nseg < 148 * 4 ? nseg : 148 * 4;
+  k_delta<<<blocks, 256, 0, s>>>(lat, snap, segs, nseg, out);
+}
+
+// --------------------------------------------------------- N7: halo pack/unpack
+__global__ void k_pack(const float* __restrict__ lat, const int32_t* __restrict__ idx, int64_t n,
+                       float* __restrict__ buf) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = lat[__ldg(idx + i)];
+}
+__global__ void k_unpack(float* __restrict__ lat, const int32_t* __restrict__ idx, int64_t n,
+                         const float* __restrict__ buf) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    lat[__ldg(idx + i)] = buf[i];
+}
+
+static int grid_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 4) b = 148 * 4;
+  return b < 1 ? 1 : (int)b;
+}
+
+void launch_pack(const float* lat, const int32_t* idx, int64_t n, float* buf, cudaStream_t s) {
+  if (n > 0) k_pack<<<grid_for(n), 256, 0, s>>>(lat, idx, n, buf);
+}
+void launch_unpack(float* lat, const int32_t* idx, int64_t n, const float* buf, cudaStream_t s) {
+  if (n > 0) k_unpack<<<grid_for(n), 256, 0, s>>>(lat, idx, n, buf);
+}
+
+// ---------------------------------------------------------- a9: final lines
+// Atomic-subdomain boundary lines (x or y a multiple of m) of the owned block
+// take the lattice values (DESIGN.md §2 reading F1); interior points are
+// written by the final-phase predictions.
+__global__ void k_final_lines(const float* __restrict__ lat, LatticeGeom L, int X0, int Y0, int bw,
+                              int bh, float* __restrict__ field, int ld) {
+  const int64_t n = (int64_t)bw * bh;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(t / bw), i = (int)(t % bw);
+    const int x = X0 + i, y = Y0 + j;
+    float v;
+    if (y % kM == 0) v = lat[(int64_t)((y - L.RY0) / kH) * L.strideH + (x - L.RX0)];
+    else if (x % kM == 0) v = lat[L.offV + (int64_t)((x - L.RX0) / kH) * L.strideV + (y - L.RY0)];
+    else continue;
+    field[(int64_t)j * ld + i] = v;
+  }
+}
+
+void launch_final_lines(const float* lat, const LatticeGeom& L, int X0, int Y0, int bw, int bh,
+                        float* field, int ld, cudaStream_t s) {
+  k_final_lines<<<148 * 4, 256, 0, s>>>(lat, L, X0, Y0, bw, bh, field, ld);
+}
+
+}  // namespace mfp

@@ -1,0 +1,131 @@
+// kernels_prep.cu — one-time device-side preparation in mfp_init (a0):
+// weight layout transforms, the query tables Q = X W2^T of the split layer
+// (Eq. 5), the bf16 SW128 K-major images of the hidden weights for the
+// tcgen05 chain, and the exact harmonic-extension matrices of the discrete
+// Laplace subsolver (N9), evaluated from the closed-form discrete sine
+// expansion of the 5-point Dirichlet problem on the (m+1)^2 patch.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "device_common.cuh"
+
+namespace mfp {
+
+// Query coordinates: centre lines (G3) and interior grid.
+__device__ __forceinline__ void query_xy(int q, int p, float* x, float* y) {
+  if (q == kQC) {
+    if (p < kM - 1) { *x = 0.5f; *y = (float)(p + 1) / kM; }
+    else {
+      int j = p - (kM - 1);
+      int k = j + 1 + (j >= kH - 1 ? 1 : 0);
+      *x = (float)k / kM; *y = 0.5f;
+    }
+  } else {
+    *x = (float)(p % (kM - 1) + 1) / kM;
+    *y = (float)(p / (kM - 1) + 1) / kM;
+  }
+}
+
+// Byte offset of element (row r, k) in a 128 x 128 bf16 K-major tile stored as
+// two SW128 atoms-columns (k < 64, k >= 64) of 16 KB each: 128 B rows, the
+// 16-byte chunk index XOR-ed with (r mod 8) — the layout tcgen05 smem
+// descriptors with layout type SWIZZLE_128B expect.
+__host__ __device__ __forceinline__ uint32_t sw128_offset(int r, int k) {
+  const int kb = k >> 6, kk = k & 63;
+  const int chunk = kk >> 3, within = kk & 7;
+  return (uint32_t)(kb * 16384 + r * 128 + ((chunk ^ (r & 7)) << 4) + within * 2);
+}
+
+__global__ void k_prep(PrepArgs a) {
+  const int d = kD;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  // W1T[k][c] = W1[c][k]
+  for (int64_t i = tid; i < (int64_t)kNB * d; i += nth) {
+    int k = (int)(i / d), c = (int)(i % d);
+    a.W1T[i] = a.P[a.oW1 + (int64_t)c * kNB + k];
+  }
+  // hidden layers
+  for (int64_t i = tid; i < (int64_t)a.n_hidden * d * d; i += nth) {
+    int l = (int)(i / (d * d));
+    int rem = (int)(i % (d * d));
+    int k = rem / d, n = rem % d;
+    const float* Wl = a.P + a.oWh0 + (int64_t)l * (d * d + d);
+    const float w = Wl[(int64_t)n * d + k];
+    a.WhT[i] = w;                                    // [l][k][n]
+    uint8_t* img = reinterpret_cast<uint8_t*>(a.Wsw + (int64_t)l * d * d);
+    // B operand row n = output feature, K-major
+    if (a.f16) *reinterpret_cast<__half*>(img + sw128_offset(n, k)) = __float2half_rn(w);
+    else *reinterpret_cast<__nv_bfloat16*>(img + sw128_offset(n, k)) = __float2bfloat16_rn(w);
+  }
+  for (int64_t i = tid; i < (int64_t)a.n_hidden * d; i += nth) {
+    int l = (int)(i / d), c = (int)(i % d);
+    a.bh[i] = a.P[a.oWh0 + (int64_t)l * (d * d + d) + (int64_t)d * d + c];
+  }
+  // Q = X W2^T (b1 is folded into z): centre (64 padded) and interior (961)
+  for (int64_t i = tid; i < (int64_t)64 * d; i += nth) {
+    int p = (int)(i / d), c = (int)(i % d);
+    float v = 0.f;
+    if (p < kQC) {
+      float x, y;
+      query_xy(kQC, p, &x, &y);
+      v = fmaf(a.P[a.oW2 + 2 * c], x, a.P[a.oW2 + 2 * c + 1] * y);
+    }
+    a.Qc[i] = v;
+    a.QTc[(int64_t)c * 64 + p] = v;
+  }
+  for (int64_t i = tid; i < (int64_t)kQF * d; i += nth) {
+    int p = (int)(i / d), c = (int)(i % d);
+    float x, y;
+    query_xy(kQF, p, &x, &y);
+    float v = fmaf(a.P[a.oW2 + 2 * c], x, a.P[a.oW2 + 2 * c + 1] * y);
+    a.Qf[i] = v;
+    a.QTf[(int64_t)c * kQF + p] = v;
+  }
+}
+
+void launch_prep(const PrepArgs& a, cudaStream_t s) { k_prep<<<148 * 2, 256, 0, s>>>(a); }
+
+// Harmonic-extension matrix H^T [k][q] for the 5-point Dirichlet problem on the
+// (m+1)^2 patch: separation of variables with the DST-I basis,
+//   u(i,j) = sum_k (2/m) f^_k sin(pi k i/m) sinh(l_k (m-j)) / sinh(l_k m),
+// cosh(l_k) = 2 - cos(pi k/m), for data on the bottom side; the other three
+// sides by symmetry.  fp64 evaluation, stored fp32.  Corners never enter the
+// 5-point stencil: their columns are 0.
+__global__ void k_harmonic(int q, int ld, float* __restrict__ HT) {
+  const int total = kNB * q;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int kb = t / q, p = t % q;
+    int qi, qj;  // query grid point (i, j) in the patch
+    if (q == kQC) {
+      if (p < kM - 1) { qi = kH; qj = p + 1; }
+      else { int j = p - (kM - 1); qi = j + 1 + (j >= kH - 1 ? 1 : 0); qj = kH; }
+    } else { qi = p % (kM - 1) + 1; qj = p / (kM - 1) + 1; }
+    const int side = kb >> 5, pos = kb & 31;
+    // s_b: position of the boundary point along its side (0 or m = corner);
+    // along: the query's coordinate along that side; dist: the query's
+    // distance from that side.  Factor sinh(l (m - dist)) / sinh(l m).
+    int s_b, along, dist;
+    switch (side) {
+      case 0: s_b = pos;      along = qi; dist = qj;      break;  // bottom, point (pos, 0)
+      case 1: s_b = pos;      along = qj; dist = kM - qi; break;  // right,  point (m, pos)
+      case 2: s_b = kM - pos; along = qi; dist = kM - qj; break;  // top,    point (m - pos, m)
+      default: s_b = kM - pos; along = qj; dist = qi;     break;  // left,   point (0, m - pos)
+    }
+    double v = 0.0;
+    if (s_b > 0 && s_b < kM) {
+      for (int k = 1; k < kM; k++) {
+        const double th = M_PI * k / kM;
+        const double lk = acosh(2.0 - cos(th));
+        v += (2.0 / kM) * sin(th * s_b) * sin(th * along) * sinh(lk * (kM - dist)) / sinh(lk * kM);
+      }
+    }
+    HT[(int64_t)kb * ld + p] = (float)v;
+  }
+}
+
+void launch_harmonic(int q, float* HT, cudaStream_t s) {
+  k_harmonic<<<148, 256, 0, s>>>(q, q == kQC ? 64 : q, HT);
+}
+
+}  // namespace mfp

@@ -1,0 +1,144 @@
+// mfp_internal.h — internal types of libmfp (plan, rank state, kernel entry points).
+// Not part of the ABI; include/mfp.h is.  See DESIGN.md §5 for the HBM layout.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/mfp.h"
+
+namespace mfp {
+
+constexpr int kM = 32;             // subdomain intervals per side (reading G1)
+constexpr int kH = kM / 2;         // lattice spacing m/2
+constexpr int kNB = 4 * kM;        // perimeter length 4m = 128 (G1)
+constexpr int kQC = 2 * kM - 3;    // centre-line queries 61 (G3)
+constexpr int kQF = (kM - 1) * (kM - 1);  // interior queries 961
+constexpr int kD = 128;            // SDNet width (G7)
+constexpr int kC1 = 8;             // conv channels 1 -> 8 -> 1, k = 5 (G7)
+constexpr int kK = 5;
+constexpr int kMaxHidden = 3;
+
+// Local lattice of one rank: horizontal lines y = RY0 + 16 i
+// (x-contiguous, RX0..RX1) then vertical lines x = RX0 + 16 j (y-contiguous,
+// RY0..RY1); row strides padded to 32 floats (128 B).  Crossing points exist in
+// both arrays and are always written to both.
+struct LatticeGeom {
+  int RX0, RX1, RY0, RY1;
+  int nH, nV, lenH, lenV, strideH, strideV;
+  int64_t offV, cells;  // cells incl. padding
+};
+
+struct PeerPlan {
+  int rank;
+  std::vector<int32_t> send_idx, recv_idx;        // flat local lattice cells
+  std::vector<int32_t> send_kind, send_x, send_y;  // canonical global keys (plan API)
+  std::vector<int32_t> recv_kind, recv_x, recv_y;
+};
+
+struct RankPlan {
+  int rank, ry, rx;
+  int X0, X1, Y0, Y1;           // owned block (half-open; last col/row closed at nx/ny)
+  int bw, bh;                   // owned block extent in points
+  LatticeGeom lat;
+  std::vector<uint32_t> phase_anchor[4];  // packed (a | b << 16), local line indices
+  std::vector<int32_t> phase_ax[4], phase_ay[4];   // global (plan API)
+  std::vector<uint32_t> final_anchor;     // packed block-local (bx | by << 16) + lattice (a|b<<16)
+  std::vector<uint32_t> final_lat_anchor;
+  std::vector<int32_t> final_ax, final_ay;
+  std::vector<PeerPlan> peers;  // row-major neighbour order
+  std::vector<int64_t> delta_seg;  // (offset << 20) | len — owned interior line cells
+};
+
+struct GlobalPlan {
+  mfp_config cfg;
+  int R;
+  std::vector<RankPlan> ranks;
+};
+
+// Validates cfg and builds the plan for one rank (or every rank when rank < 0).
+mfp_status build_plan(const mfp_config* cfg, int rank, GlobalPlan* out, std::string* err);
+mfp_status validate_config(const mfp_config* cfg, std::string* err);
+
+// ---- device-side parameter blocks ----------------------------------------
+struct DevNet {
+  // fp32 tables (SIMT path + embed)
+  const float* conv1_w;  // [8][5]
+  const float* conv1_b;  // [8]
+  const float* conv2_w;  // [8][5]
+  const float* conv2_b;  // [1]
+  const float* W1T;      // [128 k][128 d]   (W1 transposed)
+  const float* b1;       // [d]
+  const float* QTc;      // [d][64]  centre queries Q = X W2^T (b1 folded into z)
+  const float* QTf;      // [d][961] interior queries
+  const float* WhT;      // [n_hidden][k][n] fp32 (transposed for SIMT)
+  const float* bh;       // [n_hidden][d]
+  const float* wo;       // [d]
+  const float* bo;       // [1]
+  int n_hidden;
+  int gelu_tanh;
+  int f16;               // tensor-core operands fp16 (1) or bf16 (0)
+  // bf16 tables (tcgen05 path): weights pre-swizzled into the SW128 K-major image
+  const uint16_t* Wh_sw;  // [n_hidden][32 KB image]
+  const float* Qc;        // [64][d] row-major centre queries (tc path)
+  const float* Qf;        // [961][d] row-major interior queries
+  // exact subsolver
+  const float* HcT;      // [128 k][64]  (61 used)
+  const float* HfT;      // [128 k][961]
+};
+
+// Where chain outputs go.
+struct Sink {
+  int mode;  // 0: lattice centre lines, 1: field block (final phase), 2: dense out
+  int q;
+  float* lat;
+  int64_t offV;
+  int strideH, strideV;
+  const uint32_t* anchors;    // mode 0: lattice (a|b<<16); mode 1: block-local (bx|by<<16)
+  float* field;
+  int ld;
+  float* out;
+};
+
+// ---- kernel launchers (kernels_*.cu) --------------------------------------
+void launch_init_lattice(float* lat, const LatticeGeom& L, int nx, int ny, const float* g,
+                         cudaStream_t s);
+// gather + embed: z[s][d] from lattice anchors (gb == nullptr) or from gb rows.
+void launch_gather_embed(const float* lat, const LatticeGeom& L, const uint32_t* anchors,
+                         const float* gb, int64_t B, const DevNet& net, float* z,
+                         cudaStream_t s);
+// exact subsolver phase (gather + H_c + scatter) for lattice anchors
+void launch_exact_phase(float* lat, const LatticeGeom& L, const uint32_t* anchors, int64_t B,
+                        const float* HcT, cudaStream_t s);
+// exact subsolver for the final phase / batches: gb rows or lattice anchors -> sink
+void launch_exact_general(const float* lat, const LatticeGeom& L, const uint32_t* lat_anchors,
+                          const float* gb, int64_t B, int q, const float* HT, const Sink& sink,
+                          cudaStream_t s);
+void launch_chain_fp32(const float* z, int64_t B, int q, const DevNet& net, const Sink& sink,
+                       cudaStream_t s);
+bool chain_tc_available();
+void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const Sink& sink,
+                     int num_sms, cudaStream_t s);
+void launch_delta(const float* lat, const float* snap, const int64_t* segs, int nseg,
+                  unsigned int* out /* [0]=max bits, [1]=nonfinite flag */, cudaStream_t s);
+void launch_pack(const float* lat, const int32_t* idx, int64_t n, float* buf, cudaStream_t s);
+void launch_unpack(float* lat, const int32_t* idx, int64_t n, const float* buf, cudaStream_t s);
+void launch_final_lines(const float* lat, const LatticeGeom& L, int X0, int Y0, int bw, int bh,
+                        float* field, int ld, cudaStream_t s);
+// one-time preparation (kernels_prep.cu)
+struct PrepArgs {
+  const float* P;          // raw params, MFCK order
+  int n_hidden;
+  int f16;                 // tensor-core operand images in fp16 (1) or bf16 (0)
+  int64_t oW1, oW2, oWh0;  // offsets; Wh_l at oWh0 + l*(d*d + d), bh_l right after
+  float* W1T; float* WhT; float* bh;
+  float* QTc; float* QTf; float* Qc; float* Qf;
+  uint16_t* Wsw;           // [n_hidden][128*128] 16-bit SW128 K-major images
+};
+void launch_prep(const PrepArgs& a, cudaStream_t s);
+void launch_harmonic(int q, float* HT, cudaStream_t s);
+
+}  // namespace mfp
