@@ -45,7 +45,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--iters", type=int, default=64, help="MFP iterations per step (T)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    p.add_argument("--precision", default="bf16", choices=["bf16", "fp16", "fp32"])
     p.add_argument("--no-converge", action="store_true")
     return p.parse_args()
 
@@ -113,7 +113,7 @@ def cpu_oracle_rate(target_s: float = 12.0):
     from mfp_inputs import boundary_points
     bp = boundary_points(NX, NY)
     U[bp[:, 1], bp[:, 0]] = gp_boundary(NX, NY, 0)
-    anc = oracle.anchors(NX, NY, 0)
+    anc = np.concatenate([oracle.anchors(NX, NY, c) for c in range(4)])
     n = 16
     t0 = time.perf_counter()
     oracle.predict_from_field(cfg, U, anc[:n], 0, w)
@@ -189,9 +189,10 @@ def main():
         return float(t.item())
 
     grid = GRIDS[world]
-    prec = mfp.BF16 if args.precision == "bf16" else mfp.FP32
+    prec = {"bf16": mfp.BF16, "fp16": mfp.FP16, "fp32": mfp.FP32}[args.precision]
+    tensor = prec != mfp.FP32
     cfg = mfp.make_config(NX, NY, grid, precision=prec, subsolver=mfp.SDNET, check_every=16)
-    net = mfp.make_net(gelu=1 if prec == mfp.BF16 else 0)
+    net = mfp.make_net(gelu=1 if tensor else 0)
     w = random_weights(0)
     stream = torch.cuda.Stream(device=dev)
     m = mfp.Mfp(cfg, net, w, rank=rank, nccl_comm=comm, stream=stream)
@@ -250,17 +251,20 @@ def main():
     flop_per_launch = prof.chain_rows / max(prof.chain_launches, 1) * HIDDEN_FLOP_PER_ROW
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    peak = peaks.get("bf16_tflops_sustained", 1400.0) if prec == mfp.BF16 else 75.0
+    # fp16 and bf16 dense tensor rates are equal (guide: 2.25 PF each), so the
+    # measured bf16 cuBLAS peak is the denominator for both; fp32 SIMT peak is
+    # derived: 148 SMs x 128 lanes x 2 FLOP x 1.965 GHz = 74.4 TFLOP/s.
+    peak = peaks.get("bf16_tflops_sustained", 1400.0) if tensor else 74.4
     achieved = flop_per_launch / (chain_ms / 1000.0) / 1e12
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tfile):
         traffic = json.load(open(tfile)).get("chain_tc_dram_bytes_per_launch")
-    roofline = {"bound": "tensor" if prec == mfp.BF16 else "alu", "achieved": achieved, "peak": peak,
+    roofline = {"bound": "tensor" if tensor else "alu", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                "kernel": "k_chain_tc (hidden GEMM chain a4 + epilogues a3/a5/a6)",
+                "kernel": "k_chain_tc (hidden GEMM chain a4 + epilogues a3/a5/a6)" if tensor else "k_chain_fp32",
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"
-                if prec == mfp.BF16 else "derived fp32 SIMT peak (DESIGN.md §7)",
+                if tensor else "derived fp32 SIMT peak (DESIGN.md §7)",
                 "chain_ms_per_launch": chain_ms, "chain_share_of_iteration":
                     prof.chain_ms_total / (prof.ms_per_iter * prof.iterations)}
 
@@ -284,7 +288,7 @@ def main():
     if rank == 0 and world == 1:
         rate, n, dt, thr = cpu_oracle_rate()
         cpu = {"value": rate, "unit": "predictions/s", "cores": thr, "kind": "oracle",
-               "sample": f"{n} C5 phase-0 SDNet predictions (fp64 oracle, {dt:.1f} s)"}
+               "sample": f"{n} C5 subdomain SDNet predictions from the initial lattice (fp64 oracle, {dt:.1f} s)"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "predictions/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -292,7 +296,7 @@ def main():
                 "config": {"workload": "C5: 4097x4097 points, m=32 (65,025 predictions/iteration), "
                                        f"{T} MFP iterations + final phase per step",
                            "nx": NX, "ny": NY, "m": 32, "iters_per_step": T, "grid": list(grid),
-                           "subsolver": "sdnet d=128 L_h=3 (W-rand)", "gelu": "tanh" if prec == mfp.BF16 else "erf",
+                           "subsolver": "sdnet d=128 L_h=3 (W-rand)", "gelu": "tanh" if tensor else "erf",
                            "l2": "flushed between steps (512 MB write, outside the events)",
                            "parallelism": f"domain {grid[0]}x{grid[1]}"},
                 "points_iter_per_s": (NX + 1) * (NY + 1) * T * args.steps / (ms / 1000.0),

@@ -160,7 +160,7 @@ void carve(mfp_ctx* c, void* base, size_t* total) {
   dn.QTf = cv.take<float>((size_t)kD * kQF);
   dn.Qc = cv.take<float>((size_t)64 * kD);
   dn.Qf = cv.take<float>((size_t)kQF * kD);
-  dn.Wh_sw = cv.take<uint16_t>((size_t)nh * kD * kD);
+  dn.Wh_sw = cv.take<uint16_t>((size_t)nh * kWImg);
   dn.HcT = cv.take<float>((size_t)kNB * 64);
   dn.HfT = cv.take<float>((size_t)kNB * kQF);
   c->gstage = cv.take<float>((size_t)2 * (c->cfg.nx + c->cfg.ny));
@@ -545,7 +545,7 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
   }
   if (cfg->subsolver == MFP_SDNET) {
     CK(cudaMemcpyAsync(c->params, params, n_params * sizeof(float), cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync((void*)c->dn.Wh_sw, 0, (size_t)net->n_hidden * kD * kD * 2, s));
+    CK(cudaMemsetAsync((void*)c->dn.Wh_sw, 0, (size_t)net->n_hidden * kWImg * 2, s));
     PrepArgs a;
     a.P = c->params; a.n_hidden = net->n_hidden; a.f16 = cfg->precision == MFP_FP16 ? 1 : 0;
     a.oW1 = 89; a.oW2 = 89 + kD * kNB; a.oWh0 = a.oW2 + 2 * kD + kD;

@@ -53,14 +53,31 @@ __global__ void k_prep(PrepArgs a) {
     const float* Wl = a.P + a.oWh0 + (int64_t)l * (d * d + d);
     const float w = Wl[(int64_t)n * d + k];
     a.WhT[i] = w;                                    // [l][k][n]
-    uint8_t* img = reinterpret_cast<uint8_t*>(a.Wsw + (int64_t)l * d * d);
-    // B operand row n = output feature, K-major
-    if (a.f16) *reinterpret_cast<__half*>(img + sw128_offset(n, k)) = __float2half_rn(w);
-    else *reinterpret_cast<__nv_bfloat16*>(img + sw128_offset(n, k)) = __float2bfloat16_rn(w);
+    uint8_t* img = reinterpret_cast<uint8_t*>(a.Wsw + (int64_t)l * kWImg);
+    // B operand row n = output feature, K-major; scaled by 1/2 (exact) because
+    // the tensor-core epilogue feeds h' = 2 GELU(x) into the next layer
+    if (a.f16) *reinterpret_cast<__half*>(img + sw128_offset(n, k)) = __float2half_rn(0.5f * w);
+    else *reinterpret_cast<__nv_bfloat16*>(img + sw128_offset(n, k)) = __float2bfloat16_rn(0.5f * w);
   }
   for (int64_t i = tid; i < (int64_t)a.n_hidden * d; i += nth) {
     int l = (int)(i / d), c = (int)(i % d);
-    a.bh[i] = a.P[a.oWh0 + (int64_t)l * (d * d + d) + (int64_t)d * d + c];
+    const float b = a.P[a.oWh0 + (int64_t)l * (d * d + d) + (int64_t)d * d + c];
+    a.bh[i] = b;
+    // bias block of the tensor-core image: row n = c, K columns 0/1 = b_hi, b_lo
+    // (SWIZZLE_NONE K-major: 8-row x 16-byte core matrices, LBO 128 B, SBO 256 B);
+    // the A operand carries a constant 1 in those two columns, so the MMA adds
+    // b_hi + b_lo (accurate to ~2^-17 relative) to the fp32 accumulator.
+    uint8_t* blk = reinterpret_cast<uint8_t*>(a.Wsw + (int64_t)l * kWImg + kWImgW);
+    const uint32_t off = (uint32_t)((c >> 3) * 256 + (c & 7) * 16);
+    if (a.f16) {
+      const __half hi = __float2half_rn(b);
+      *reinterpret_cast<__half*>(blk + off) = hi;
+      *reinterpret_cast<__half*>(blk + off + 2) = __float2half_rn(b - __half2float(hi));
+    } else {
+      const __nv_bfloat16 hi = __float2bfloat16_rn(b);
+      *reinterpret_cast<__nv_bfloat16*>(blk + off) = hi;
+      *reinterpret_cast<__nv_bfloat16*>(blk + off + 2) = __float2bfloat16_rn(b - __bfloat162float(hi));
+    }
   }
   // Q = X W2^T (b1 is folded into z): centre (64 padded) and interior (961)
   for (int64_t i = tid; i < (int64_t)64 * d; i += nth) {

@@ -12,88 +12,152 @@
 namespace mfp {
 
 // ------------------------------------------------------------ N2+N3: embed
-// One warp per subdomain.  Shared memory: W1^T (64 KB) + conv weights +
-// per-warp scratch.  z = W1 e + b1 is the boundary half of the split layer; the
-// query half Q = X W2^T is a per-query constant table built at init.
+// A block embeds 64 subdomains per round.  Phase A (per warp, 8 subdomains):
+// gather the 128 perimeter values (G1 order), conv1 (1 -> 8, k = 5, circular)
+// + GELU and conv2 (8 -> 1) + GELU with each lane owning 4 consecutive
+// positions (3 LDS.128 windows per channel), e written k-major into smem.
+// Phase B (whole block): z = e W1^T + b1 as a register-tiled 64 x 128 x 128
+// SIMT GEMM — W1^T (64 KB, smem-resident) is read once per 64 subdomains.
+// z is the boundary half of the split layer (Eq. 5); the query half
+// Q = X W2^T is a per-query constant table built at init.
 constexpr int kEmbWarps = 8;
-constexpr int kEmbSmem = (kNB * kD + 96 + kEmbWarps * (kNB + kC1 * kNB + kNB)) * 4;
+constexpr int kEmbSub = 64;                  // subdomains per block round
+constexpr int kEmbPerWarp = kEmbSub / kEmbWarps;
+constexpr int kEs = kEmbSub + 4;             // padded row of e^T (bank spread)
+constexpr int kEmbSmem = (kNB * kD + kNB * kEs + 96 + kD + kEmbWarps * (kNB + kC1 * kNB)) * 4;
 
-__global__ void __launch_bounds__(kEmbWarps * 32, 2)
+template <int GELU>
+__device__ __forceinline__ float emb_act(float x) {
+  if constexpr (GELU == 1) return gelu_tanh(x);
+  else return gelu_erf(x);
+}
+
+template <int GELU>
+__global__ void __launch_bounds__(kEmbWarps * 32, 1)
 k_gather_embed(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ anchors,
                const float* __restrict__ gb, int64_t B, DevNet net, float* __restrict__ z) {
   extern __shared__ float smem[];
-  float* sW1T = smem;                        // [128][128]
-  float* sCw = sW1T + kNB * kD;              // c1w[40] c1b[8] c2w[40] c2b[1]
-  float* sWarp = sCw + 96;
+  float* sW1T = smem;                        // [128 k][128 d]
+  float* sE = sW1T + kNB * kD;               // e^T [128 k][68]
+  float* sCw = sE + kNB * kEs;               // c1w[40] c1b[8] c2w[40] c2b[1]
+  float* sB1 = sCw + 96;                     // b1 (the raw parameter block is not 16 B aligned)
+  float* sWarp = sB1 + kD;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   {
     const float4* src = reinterpret_cast<const float4*>(net.W1T);
     float4* dst = reinterpret_cast<float4*>(sW1T);
     for (int i = threadIdx.x; i < kNB * kD / 4; i += blockDim.x) dst[i] = __ldg(src + i);
+    if (threadIdx.x < kD) sB1[threadIdx.x] = __ldg(net.b1 + threadIdx.x);
     if (threadIdx.x < 40) sCw[threadIdx.x] = __ldg(net.conv1_w + threadIdx.x);
     if (threadIdx.x < 8) sCw[40 + threadIdx.x] = __ldg(net.conv1_b + threadIdx.x);
     if (threadIdx.x < 40) sCw[48 + threadIdx.x] = __ldg(net.conv2_w + threadIdx.x);
     if (threadIdx.x == 0) sCw[88] = __ldg(net.conv2_b);
   }
   __syncthreads();
-  float* g = sWarp + warp * (kNB + kC1 * kNB + kNB);
+  float* g = sWarp + warp * (kNB + kC1 * kNB);
   float* c1 = g + kNB;
-  float* e = c1 + kC1 * kNB;
-  const int64_t nwarps = (int64_t)gridDim.x * kEmbWarps;
-  for (int64_t s = (int64_t)blockIdx.x * kEmbWarps + warp; s < B; s += nwarps) {
-    // gather ĝ in G1 order: 4 edges x 32 contiguous values (coalesced)
-    if (gb) {
+  const int i0 = 4 * lane;                   // this lane's 4 consecutive perimeter positions
+  const int im = (i0 - 4) & (kNB - 1), ip = (i0 + 4) & (kNB - 1);
+  const int edge = lane >> 3, t0 = 4 * (lane & 7);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  for (int64_t base = (int64_t)blockIdx.x * kEmbSub; base < B; base += (int64_t)gridDim.x * kEmbSub) {
+    // ---- phase A: gather + conv stack, 8 subdomains per warp
+    for (int j = 0; j < kEmbPerWarp; j++) {
+      const int col = warp * kEmbPerWarp + j;
+      int64_t s = base + col;
+      if (s > B - 1) s = B - 1;
+      float4 gv;
+      if (gb) {
+        gv = __ldg(reinterpret_cast<const float4*>(gb + s * kNB + i0));
+      } else {
+        int a, b;
+        unpack_anchor(__ldg(anchors + s), a, b);
+        const int lx = kH * a, ly = kH * b;
+        if (edge == 0) gv = *reinterpret_cast<const float4*>(lat + (int64_t)b * L.strideH + lx + t0);
+        else if (edge == 1) gv = *reinterpret_cast<const float4*>(lat + L.offV + (int64_t)(a + 2) * L.strideV + ly + t0);
+        else if (edge == 2) {
+          const float* r = lat + (int64_t)(b + 2) * L.strideH + lx + kM - t0;
+          gv = make_float4(r[0], r[-1], r[-2], r[-3]);
+        } else {
+          const float* r = lat + L.offV + (int64_t)a * L.strideV + ly + kM - t0;
+          gv = make_float4(r[0], r[-1], r[-2], r[-3]);
+        }
+      }
+      *reinterpret_cast<float4*>(g + i0) = gv;
+      __syncwarp();
+      // conv1 on positions i0..i0+3 from the window g[i0-2 .. i0+5]
+      {
+        const float4 wm = *reinterpret_cast<const float4*>(g + im);
+        const float4 wp = *reinterpret_cast<const float4*>(g + ip);
+        const float win[8] = {wm.z, wm.w, gv.x, gv.y, gv.z, gv.w, wp.x, wp.y};
 #pragma unroll
-      for (int e4 = 0; e4 < 4; e4++) g[e4 * 32 + lane] = __ldg(gb + s * kNB + e4 * 32 + lane);
-    } else {
-      int a, b;
-      unpack_anchor(__ldg(anchors + s), a, b);
+        for (int o = 0; o < kC1; o++) {
+          float acc[4];
 #pragma unroll
-      for (int e4 = 0; e4 < 4; e4++)
-        g[e4 * 32 + lane] = lat[perim_cell(a, b, e4 * 32 + lane, L.strideH, L.strideV, L.offV)];
+          for (int p = 0; p < 4; p++) {
+            float v = sCw[40 + o];
+#pragma unroll
+            for (int t = 0; t < kK; t++) v = fmaf(sCw[o * kK + t], win[p + t], v);
+            acc[p] = emb_act<GELU>(v);
+          }
+          *reinterpret_cast<float4*>(c1 + o * kNB + i0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        }
+      }
+      __syncwarp();
+      // conv2 (8 -> 1) + GELU -> e^T[:, col]
+      {
+        float acc[4] = {sCw[88], sCw[88], sCw[88], sCw[88]};
+#pragma unroll
+        for (int o = 0; o < kC1; o++) {
+          const float* row = c1 + o * kNB;
+          const float4 wm = *reinterpret_cast<const float4*>(row + im);
+          const float4 w0 = *reinterpret_cast<const float4*>(row + i0);
+          const float4 wp = *reinterpret_cast<const float4*>(row + ip);
+          const float win[8] = {wm.z, wm.w, w0.x, w0.y, w0.z, w0.w, wp.x, wp.y};
+#pragma unroll
+          for (int p = 0; p < 4; p++)
+#pragma unroll
+            for (int t = 0; t < kK; t++) acc[p] = fmaf(sCw[48 + o * kK + t], win[p + t], acc[p]);
+        }
+#pragma unroll
+        for (int p = 0; p < 4; p++) sE[(i0 + p) * kEs + col] = emb_act<GELU>(acc[p]);
+      }
+      __syncwarp();
     }
-    __syncwarp();
-    // conv1: 1 -> 8 channels, k = 5, circular padding 2, GELU
+    __syncthreads();
+    // ---- phase B: z[64 x 128] = e[64 x 128] W1^T, thread = 4 subdomains x 8 outputs
+    {
+      float acc[4][8];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int i = lane + 32 * u;
-      float gv[kK];
+      for (int i = 0; i < 4; i++)
 #pragma unroll
-      for (int t = 0; t < kK; t++) gv[t] = g[(i + t - 2) & (kNB - 1)];
+        for (int jj = 0; jj < 8; jj++) acc[i][jj] = 0.f;
+#pragma unroll 4
+      for (int k = 0; k < kNB; k++) {
+        const float4 a = *reinterpret_cast<const float4*>(sE + k * kEs + ty * 4);
+        const float4 w0 = *reinterpret_cast<const float4*>(sW1T + k * kD + tx * 4);
+        const float4 w1 = *reinterpret_cast<const float4*>(sW1T + k * kD + 64 + tx * 4);
+        const float av[4] = {a.x, a.y, a.z, a.w};
+        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-      for (int o = 0; o < kC1; o++) {
-        float acc = sCw[40 + o];
+        for (int i = 0; i < 4; i++)
 #pragma unroll
-        for (int t = 0; t < kK; t++) acc = fmaf(sCw[o * kK + t], gv[t], acc);
-        c1[o * kNB + i] = gelu_erf(acc);
+          for (int jj = 0; jj < 8; jj++) acc[i][jj] = fmaf(av[i], wv[jj], acc[i][jj]);
+      }
+      const float4 b0 = *reinterpret_cast<const float4*>(sB1 + tx * 4);
+      const float4 b1 = *reinterpret_cast<const float4*>(sB1 + 64 + tx * 4);
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const int64_t s = base + ty * 4 + i;
+        if (s >= B) continue;
+        float* zr = z + s * kD;
+        *reinterpret_cast<float4*>(zr + tx * 4) =
+            make_float4(acc[i][0] + b0.x, acc[i][1] + b0.y, acc[i][2] + b0.z, acc[i][3] + b0.w);
+        *reinterpret_cast<float4*>(zr + 64 + tx * 4) =
+            make_float4(acc[i][4] + b1.x, acc[i][5] + b1.y, acc[i][6] + b1.z, acc[i][7] + b1.w);
       }
     }
-    __syncwarp();
-    // conv2: 8 -> 1 channel, GELU -> e (ch_last * 4m = 128)
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int i = lane + 32 * u;
-      float acc = sCw[88];
-#pragma unroll
-      for (int o = 0; o < kC1; o++)
-#pragma unroll
-        for (int t = 0; t < kK; t++) acc = fmaf(sCw[48 + o * kK + t], c1[o * kNB + ((i + t - 2) & (kNB - 1))], acc);
-      e[i] = gelu_erf(acc);
-    }
-    __syncwarp();
-    // z = W1 e + b1
-    float acc[4];
-#pragma unroll
-    for (int u = 0; u < 4; u++) acc[u] = 0.f;
-#pragma unroll 4
-    for (int k = 0; k < kNB; k++) {
-      const float ek = e[k];
-#pragma unroll
-      for (int u = 0; u < 4; u++) acc[u] = fmaf(sW1T[k * kD + lane + 32 * u], ek, acc[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; u++) z[s * kD + lane + 32 * u] = acc[u] + __ldg(net.b1 + lane + 32 * u);
-    __syncwarp();
+    __syncthreads();
   }
 }
 
@@ -102,12 +166,16 @@ void launch_gather_embed(const float* lat, const LatticeGeom& L, const uint32_t*
   if (B <= 0) return;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gather_embed, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmbSmem);
+    cudaFuncSetAttribute(k_gather_embed<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmbSmem);
+    cudaFuncSetAttribute(k_gather_embed<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmbSmem);
     attr = true;
   }
-  int64_t blocks = (B + kEmbWarps - 1) / kEmbWarps;
-  if (blocks > 148 * 2) blocks = 148 * 2;
-  k_gather_embed<<<(int)blocks, kEmbWarps * 32, kEmbSmem, s>>>(lat, L, anchors, gb, B, net, z);
+  int64_t blocks = (B + kEmbSub - 1) / kEmbSub;
+  if (blocks > 148) blocks = 148;
+  if (net.gelu_tanh)
+    k_gather_embed<1><<<(int)blocks, kEmbWarps * 32, kEmbSmem, s>>>(lat, L, anchors, gb, B, net, z);
+  else
+    k_gather_embed<0><<<(int)blocks, kEmbWarps * 32, kEmbSmem, s>>>(lat, L, anchors, gb, B, net, z);
 }
 
 // ------------------------------------------------------ N4-fp32: SIMT chain

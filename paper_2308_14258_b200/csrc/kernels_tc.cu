@@ -1,22 +1,28 @@
-// kernels_tc.cu — bf16 SDNet MLP chain on the 5th-generation tensor cores (N4).
+// kernels_tc.cu — SDNet MLP chain on the 5th-generation tensor cores (N4),
+// bf16 or fp16 operands, fp32 accumulation in TMEM.
 //
 // The hidden GEMM chain h <- GELU(h W_l^T + b_l) is the path's one
 // dense contraction: rows = (subdomain, query) pairs packed densely
 // (row = s*q + p), K = N = d = 128.  Design:
 //   * persistent CTAs (one per SM), 128-row tiles (UMMA M = 128, N = 128,
-//     K = 16 x 8 per layer), fp32 accumulators in TMEM;
+//     K = 16 x 8 per layer), fp32 accumulators in TMEM (2 x 128 columns);
 //   * the n_hidden weight matrices stay resident in shared memory for the
-//     whole kernel as bf16 SWIZZLE_128B K-major images (B operand);
-//   * two epilogue warpgroups ping-pong on two tiles (TMEM slots 0/1, smem A
-//     buffers 0/1): while the tensor core runs layer l of one tile, the other
-//     warpgroup's epilogue (tcgen05.ld -> +bias -> GELU -> bf16 -> st.shared
-//     into the swizzled A operand of layer l+1) runs on the other;
-//   * one elected thread issues tcgen05.mma and tcgen05.commit -> mbarrier;
-//   * the layer-1 input is Eq. 5's broadcasted sum GELU(z[s] + Q[p]) built
-//     directly into the A buffer (Q = X W2^T resident in smem for the 61
-//     centre-line queries); the last epilogue does the head dot y = wo.h + bo
-//     and the scatter onto the lattice (fused N5).
+//     whole kernel as 16-bit SWIZZLE_128B K-major images (B operand), pre-
+//     scaled by 1/2 (exact) because the epilogue produces h' = 2 GELU(x);
+//   * warp 0 issues tcgen05.mma from one lane and commits to an mbarrier;
+//     warp 1 owns the TMEM allocation; warps 2..17 form four epilogue
+//     warpgroups: two per tile slot (ping-pong over 2 slots), each owning 64
+//     of the 128 accumulator columns of its slot's tile;
+//   * epilogue of a layer feeding another MMA: tcgen05.ld -> +bias (fp32) ->
+//     round to 16 bit -> packed GELU (HFMA2 + MUFU tanh on x2 lanes) ->
+//     st.shared into the swizzled A operand -> fence.proxy.async -> arrive;
+//   * the layer-1 input is Eq. 5's broadcasted sum GELU(z[s] + Q[p]) (z for the
+//     <= 4 subdomains of a tile staged in smem, Q = X W2^T resident in smem for
+//     the 61 centre-line queries); the last layer's epilogue stays fp32 (GELU +
+//     head dot y = wo.h + bo; the head cancels strongly) and the
+//     two column halves combine through smem before the fused scatter (N5).
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "device_common.cuh"
 
@@ -24,10 +30,14 @@ namespace mfp {
 namespace tc {
 
 constexpr int kRows = 128;
-constexpr int kThreads = 384;          // warp 0: MMA issue, warp 1: TMEM alloc, warps 4-11: epilogue
-constexpr int kTile = kRows * kD * 2;  // 32 KB bf16 operand image
-constexpr int kQStride = 132;          // padded fp32 row of the smem Q table (bank spread)
+constexpr int kEpiWarps = 16;
+constexpr int kThreads = 32 * (2 + kEpiWarps);  // 576
+constexpr int kTile = kRows * kD * 2;           // 32 KB 16-bit operand image
+constexpr int kQStride = 132;                   // padded fp32 row of the smem Q table
 constexpr int kTmemCols = 256;
+constexpr int kZRows = 4;                       // subdomains one 128-row tile can touch (q >= 61)
+constexpr float kG0 = 0.7978845608028654f;      // sqrt(2/pi)
+constexpr float kG1 = 0.7978845608028654f * 0.044715f;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -43,20 +53,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 // Shared-memory matrix descriptor, K-major, SWIZZLE_128B: start address >> 4,
 // LBO = 1 (unused for swizzled K-major), SBO = 1024 B (8 rows x 128 B),
@@ -70,9 +77,9 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor, kind::f16: D fp32 (bits 4-5 = 1), A/B bf16 (bits
-// 7-9, 10-12 = 1), both K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28.
-// A/B format 1 = bf16, 0 = fp16.
+// Instruction descriptor, kind::f16: D fp32 (bits 4-5 = 1), A/B format at
+// bits 7-9 / 10-12 (1 = bf16, 0 = fp16), both K-major, N >> 3 at bits 17-22,
+// M >> 4 at bits 24-28.
 template <int F16>
 constexpr uint32_t idesc() {
   return (1u << 4) | ((F16 ? 0u : 1u) << 7) | ((F16 ? 0u : 1u) << 10) | ((uint32_t)(kD >> 3) << 17) |
@@ -107,13 +114,41 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// Round two fp32 values to the operand type (lo -> bits 0-15).
+// Round two fp32 values to the operand type (lo -> bits 0-15).  fp16: F2FP
+// (cvt.rn).  bf16: round-half-away-from-zero on the magnitude via an integer
+// add of half a bf16 ulp and a byte permute — ALU-pipe work instead of an
+// F2FP on the quarter-rate XU pipe, which MUFU.TANH already saturates
+// (differs from round-to-nearest-even only on exact ties; finite inputs).
 template <int F16>
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   uint32_t r;
-  if constexpr (F16) asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  else asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  if constexpr (F16) {
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  } else {
+    const uint32_t a = __float_as_uint(lo) + 0x8000u, b = __float_as_uint(hi) + 0x8000u;
+    r = __byte_perm(a, b, 0x7632);
+  }
   return r;
+}
+
+// h' = x (1 + tanh(x (G0 + G1 x^2))) = 2 GELU_tanh(x) on two packed 16-bit lanes.
+template <int F16>
+__device__ __forceinline__ uint32_t gelu2x2(uint32_t x, uint32_t c0, uint32_t c1) {
+  uint32_t x2, t, u, th, h;
+  if constexpr (F16) {
+    asm("mul.rn.f16x2 %0, %1, %1;" : "=r"(x2) : "r"(x));
+    asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(t) : "r"(x2), "r"(c1), "r"(c0));
+    asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(u) : "r"(x), "r"(t));
+    asm("tanh.approx.f16x2 %0, %1;" : "=r"(th) : "r"(u));
+    asm("fma.rn.f16x2 %0, %1, %2, %1;" : "=r"(h) : "r"(x), "r"(th));
+  } else {
+    asm("mul.rn.bf16x2 %0, %1, %1;" : "=r"(x2) : "r"(x));
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(t) : "r"(x2), "r"(c1), "r"(c0));
+    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(u) : "r"(x), "r"(t));
+    asm("tanh.approx.bf16x2 %0, %1;" : "=r"(th) : "r"(u));
+    asm("fma.rn.bf16x2 %0, %1, %2, %1;" : "=r"(h) : "r"(x), "r"(th));
+  }
+  return h;
 }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -121,54 +156,121 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
                : "memory");
 }
 
-// Byte offset of (row, k) in a 128 x 128 bf16 SW128 K-major image (two 16 KB
+// Byte offset of (row, k) in a 128 x 128 16-bit SW128 K-major image (two 16 KB
 // K-halves; 16-byte chunk index XOR row mod 8).  Same formula as kernels_prep.
 __device__ __forceinline__ uint32_t sw128_off(int r, int k) {
   const int kb = k >> 6, chunk = (k & 63) >> 3;
   return (uint32_t)(kb * 16384 + r * 128 + ((chunk ^ (r & 7)) << 4));
 }
 
+// Activation of the fp32 last layer, up to the factor the head weights carry:
+// tanh form returns x (1 + tanh(x (G0 + G1 x^2))) = 2 GELU(x) (smem wo holds
+// wo / 2), erf form returns GELU(x) (smem wo holds wo).
 template <int GELU>
-__device__ __forceinline__ float act(float x) {
-  if constexpr (GELU == 1) return gelu_tanh(x);
-  else return gelu_erf(x);
+__device__ __forceinline__ float act_head(float x) {
+  if constexpr (GELU == 1) {
+    const float u = x * fmaf(kG1, x * x, kG0);
+    return fmaf(x, tanh_approx(u), x);
+  } else {
+    return gelu_erf(x);
+  }
+}
+// Activation of a layer feeding an MMA, 8 fp32 pre-activations -> 4 packed words of h' = 2 GELU.
+template <int GELU, int F16>
+__device__ __forceinline__ void act8(const float (&v)[8], uint32_t (&w)[4], uint32_t c0, uint32_t c1) {
+  if constexpr (GELU == 1) {
+#pragma unroll
+    for (int e = 0; e < 4; e++) w[e] = gelu2x2<F16>(pack2<F16>(v[2 * e], v[2 * e + 1]), c0, c1);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; e++) w[e] = pack2<F16>(2.f * gelu_erf(v[2 * e]), 2.f * gelu_erf(v[2 * e + 1]));
+  }
+}
+
+constexpr int kWTile = kWImg * 2;   // 36 KB per hidden layer: weights (SW128) + bias block
+constexpr int kOnes = kRows * 16 * 2;  // 4 KB constant A block: columns 0/1 = 1
+
+// SWIZZLE_NONE K-major descriptor for the K = 16 bias step: 8-row x 16-byte
+// core matrices, LBO = 128 B (next 8 K elements), SBO = 256 B (next 8 rows).
+__device__ __forceinline__ uint64_t nosw_desc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(128 >> 4) << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+
+struct Smem {
+  uint8_t* W;      // [nh][36 KB]
+  uint8_t* A;      // [2][32 KB]
+  uint8_t* ones;   // 4 KB
+  float* Q;        // [64][132]
+  float* zbuf;     // [2][4][128]
+  float* ypart;    // [2][128]
+  float* wo;       // [128]
+  uint64_t* bars;  // a_full[2], d_full[2]
+  uint32_t* tmem_slot;
+};
+
+// `raw` is the 1024-byte aligned dynamic shared window (SWIZZLE_128B operand
+// images need 1024-byte aligned atoms); plain pointer offsets keep the shared
+// address space visible to the compiler (LDS/STS, not generic LD/ST).
+__device__ __forceinline__ Smem carve(uint8_t* raw, int nh) {
+  Smem s;
+  uint8_t* base = raw;
+  s.W = base;
+  s.A = base + nh * kWTile;
+  s.ones = s.A + 2 * kTile;
+  s.Q = (float*)(s.ones + kOnes);
+  s.zbuf = s.Q + 64 * kQStride;
+  s.ypart = s.zbuf + 2 * kZRows * kD;
+  s.wo = s.ypart + 2 * kRows;
+  s.bars = (uint64_t*)(s.wo + kD);
+  s.tmem_slot = (uint32_t*)(s.bars + 4);
+  return s;
+}
+
+size_t smem_bytes(int n_hidden) {
+  return (size_t)n_hidden * kWTile + 2 * kTile + kOnes +
+         4 * ((size_t)64 * kQStride + 2 * kZRows * kD + 2 * kRows + kD) + 64;
 }
 
 template <int GELU, int F16>
 __global__ void __launch_bounds__(kThreads, 1)
 k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, const float* __restrict__ Qg,
            DevNet net, Sink sink) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int nh = net.n_hidden;
-  uint8_t* sW = base;
-  uint8_t* sA = base + nh * kTile;
-  float* sQ = (float*)(sA + 2 * kTile);
-  float* sBh = sQ + 64 * kQStride;
-  float* sWo = sBh + kMaxHidden * kD;
-  uint64_t* bars = (uint64_t*)(sWo + kD);  // a_full[2], d_full[2]
-  uint32_t* tmem_slot = (uint32_t*)(bars + 4);
+  const Smem S = carve(smem_raw, nh);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // ---- prologue: resident weights / tables
+  // ---- prologue: resident weight images / tables, barriers, TMEM
   {
     const uint4* src = reinterpret_cast<const uint4*>(net.Wh_sw);
-    uint4* dst = reinterpret_cast<uint4*>(sW);
-    for (int i = threadIdx.x; i < nh * kTile / 16; i += kThreads) dst[i] = __ldg(src + i);
+    uint4* dst = reinterpret_cast<uint4*>(S.W);
+    for (int i = threadIdx.x; i < nh * kWTile / 16; i += kThreads) dst[i] = __ldg(src + i);
     if (q == kQC)
-      for (int i = threadIdx.x; i < 64 * kD; i += kThreads) sQ[(i >> 7) * kQStride + (i & 127)] = __ldg(net.Qc + i);
-    for (int i = threadIdx.x; i < nh * kD; i += kThreads) sBh[i] = __ldg(net.bh + i);
-    for (int i = threadIdx.x; i < kD; i += kThreads) sWo[i] = __ldg(net.wo + i);
+      for (int i = threadIdx.x; i < 64 * kD; i += kThreads) S.Q[(i >> 7) * kQStride + (i & 127)] = __ldg(net.Qc + i);
+    for (int i = threadIdx.x; i < kD; i += kThreads) S.wo[i] = (GELU == 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
+    // constant A block of the bias step: row r, K columns 0/1 = 1.0, others 0
+    if (threadIdx.x < kRows) {
+      const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
+      const int r = threadIdx.x;
+      uint4* p0 = reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + (r & 7) * 16);
+      *p0 = make_uint4(one | (one << 16), 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + 128 + (r & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
+    }
   }
+  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();  // SW128 atoms need 1024 B alignment
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 128);
-    mbar_init(&bars[1], 128);
-    mbar_init(&bars[2], 1);
-    mbar_init(&bars[3], 1);
+    mbar_init(&S.bars[0], 256);
+    mbar_init(&S.bars[1], 256);
+    mbar_init(&S.bars[2], 1);
+    mbar_init(&S.bars[3], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
                  "r"(kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -177,11 +279,11 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, const float* 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const float bo = __ldg(net.bo);
+  const uint32_t tmem = *S.tmem_slot;
 
   const int64_t ntiles = (total_rows + kRows - 1) / kRows;
   const int64_t nloc = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t nsub = total_rows / q;
 
   if (warp == 0) {
     // ---- MMA issuer: round-robin over (tile pair, layer, slot)
@@ -191,63 +293,82 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, const float* 
         for (int l = 0; l < nh; l++) {
           for (int s = 0; s < 2; s++) {
             if (j0 + s >= nloc) continue;
-            mbar_wait(&bars[s], pa[s]);
+            mbar_wait(&S.bars[s], pa[s]);
             pa[s] ^= 1u;
             tc_fence_after();
-            const uint32_t a0 = smem_u32(sA + s * kTile), b0 = smem_u32(sW + l * kTile);
+            const uint32_t a0 = smem_u32(S.A + s * kTile), b0 = smem_u32(S.W + l * kWTile);
+            const uint32_t d = tmem + (uint32_t)(s * kD);
 #pragma unroll
             for (int k = 0; k < kD / 16; k++) {
               const uint32_t off = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
-              mma_f16<F16>(tmem + (uint32_t)(s * kD), sw128_desc(a0 + off), sw128_desc(b0 + off), k > 0 ? 1u : 0u);
+              mma_f16<F16>(d, sw128_desc(a0 + off), sw128_desc(b0 + off), k > 0 ? 1u : 0u);
             }
-            mma_commit(&bars[2 + s]);
+            // bias step: D += [1 1 0..] [b_hi b_lo 0..]^T
+            mma_f16<F16>(d, nosw_desc(smem_u32(S.ones)), nosw_desc(b0 + (uint32_t)(kWImgW * 2)), 1u);
+            mma_commit(&S.bars[2 + s]);
           }
         }
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
-    // ---- epilogue warpgroups: slot wg = 0 / 1, thread <-> tile row <-> TMEM lane
-    const int wg = (warp - 4) >> 2;
-    const int quad = (warp - 4) & 3;
-    const int row = quad * 32 + lane;
-    uint8_t* A = sA + wg * kTile;
+  } else if (warp >= 2) {
+    // ---- epilogue: 4 warpgroups = 2 slots x 2 column halves
+    const int ew = warp - 2;
+    const int wg = ew >> 2, slot = wg >> 1, half = wg & 1;
+    const int quad = warp & 3;                       // TMEM lane quadrant of this warp
+    const int row = quad * 32 + lane;                // tile row == TMEM lane
+    const int tid_s = half * 128 + row;              // 0..255 within the slot
+    const int c_lo = half * 64;
+    uint8_t* A = S.A + slot * kTile;
     const uint32_t a_base = smem_u32(A);
-    const uint32_t t_row = tmem + (uint32_t)(wg * kD) + ((uint32_t)(quad * 32) << 16);
+    const uint32_t t_row = tmem + (uint32_t)(slot * kD + c_lo) + ((uint32_t)(quad * 32) << 16);
+    float* zb = S.zbuf + slot * kZRows * kD;
+    const uint32_t c0 = pack2<F16>(kG0, kG0), c1 = pack2<F16>(kG1, kG1);
     uint32_t pd = 0u;
-    for (int64_t j = wg; j < nloc; j += 2) {
+    for (int64_t j = slot; j < nloc; j += 2) {
       const int64_t tile = blockIdx.x + j * (int64_t)gridDim.x;
-      const int64_t grow = tile * kRows + row;
+      const int64_t row0 = tile * kRows;
+      const int64_t s_first = row0 / q;
+      // stage z of the <= 4 subdomains this tile touches (coalesced, 2 floats per thread)
+      {
+        const int idx = 2 * tid_s, r = idx >> 7, c = idx & 127;
+        int64_t sidx = s_first + r;
+        if (sidx > nsub - 1) sidx = nsub - 1;
+        *reinterpret_cast<float2*>(zb + idx) = __ldg(reinterpret_cast<const float2*>(z + sidx * kD + c));
+      }
+      named_sync(1 + slot, 256);
+      const int64_t grow = row0 + row;
       const bool valid = grow < total_rows;
       const int64_t gr = valid ? grow : total_rows - 1;
       const int64_t sidx = gr / q;
       const int p = (int)(gr - sidx * q);
-      // layer-1 input (Eq. 5): GELU(z[s] + Q[p]) -> bf16 A operand
+      // layer-1 input (Eq. 5): h' = 2 GELU(z[s] + Q[p]) -> A operand
       {
-        const float4* zr = reinterpret_cast<const float4*>(z + sidx * kD);
-        const float4* qr = reinterpret_cast<const float4*>(q == kQC ? sQ + p * kQStride : Qg + (int64_t)p * kD);
+        const float* zr = zb + (int)(sidx - s_first) * kD + c_lo;
+        const float* qr = q == kQC ? S.Q + p * kQStride + c_lo : Qg + (int64_t)p * kD + c_lo;
 #pragma unroll 2
-        for (int cc = 0; cc < kD / 8; cc++) {
-          const float4 z0 = __ldg(zr + 2 * cc), z1 = __ldg(zr + 2 * cc + 1);
-          const float4 q0 = qr[2 * cc], q1 = qr[2 * cc + 1];
-          const uint32_t w0 = pack2<F16>(act<GELU>(z0.x + q0.x), act<GELU>(z0.y + q0.y));
-          const uint32_t w1 = pack2<F16>(act<GELU>(z0.z + q0.z), act<GELU>(z0.w + q0.w));
-          const uint32_t w2 = pack2<F16>(act<GELU>(z1.x + q1.x), act<GELU>(z1.y + q1.y));
-          const uint32_t w3 = pack2<F16>(act<GELU>(z1.z + q1.z), act<GELU>(z1.w + q1.w));
-          st_shared_v4(a_base + sw128_off(row, cc * 8), w0, w1, w2, w3);
+        for (int cc = 0; cc < 8; cc++) {
+          const float4 z0 = *reinterpret_cast<const float4*>(zr + cc * 8);
+          const float4 z1 = *reinterpret_cast<const float4*>(zr + cc * 8 + 4);
+          const float4 q0 = *reinterpret_cast<const float4*>(qr + cc * 8);
+          const float4 q1 = *reinterpret_cast<const float4*>(qr + cc * 8 + 4);
+          const float v[8] = {z0.x + q0.x, z0.y + q0.y, z0.z + q0.z, z0.w + q0.w,
+                              z1.x + q1.x, z1.y + q1.y, z1.z + q1.z, z1.w + q1.w};
+          uint32_t w[4];
+          act8<GELU, F16>(v, w, c0, c1);
+          st_shared_v4(a_base + sw128_off(row, c_lo + cc * 8), w[0], w[1], w[2], w[3]);
         }
       }
       fence_proxy_async();
-      mbar_arrive(&bars[wg]);
+      mbar_arrive(&S.bars[slot]);
       float y = 0.f;
       for (int l = 0; l < nh; l++) {
-        mbar_wait(&bars[2 + wg], pd);
+        mbar_wait(&S.bars[2 + slot], pd);
         pd ^= 1u;
         tc_fence_after();
-        const float* bl = sBh + l * kD;
         const bool last = (l == nh - 1);
 #pragma unroll 1
-        for (int ch = 0; ch < kD / 32; ch++) {
+        for (int ch = 0; ch < 2; ch++) {
           uint32_t r[32];
           tmem_ld32(t_row + (uint32_t)(ch * 32), r);
           tmem_wait_ld();
@@ -255,28 +376,30 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, const float* 
 #pragma unroll
             for (int c8 = 0; c8 < 4; c8++) {
               const int c = ch * 32 + c8 * 8;
-              uint32_t w[4];
+              float v[8];
 #pragma unroll
-              for (int e = 0; e < 4; e++) {
-                const float v0 = act<GELU>(__uint_as_float(r[c8 * 8 + 2 * e]) + bl[c + 2 * e]);
-                const float v1 = act<GELU>(__uint_as_float(r[c8 * 8 + 2 * e + 1]) + bl[c + 2 * e + 1]);
-                w[e] = pack2<F16>(v0, v1);
-              }
-              st_shared_v4(a_base + sw128_off(row, c), w[0], w[1], w[2], w[3]);
+              for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[c8 * 8 + e]);  // bias already in D
+              uint32_t w[4];
+              act8<GELU, F16>(v, w, c0, c1);
+              st_shared_v4(a_base + sw128_off(row, c_lo + c), w[0], w[1], w[2], w[3]);
             }
           } else {
+            const float* wo = S.wo + c_lo + ch * 32;
 #pragma unroll
-            for (int e = 0; e < 32; e++)
-              y = fmaf(sWo[ch * 32 + e], act<GELU>(__uint_as_float(r[e]) + bl[ch * 32 + e]), y);
+            for (int e = 0; e < 32; e++) y = fmaf(wo[e], act_head<GELU>(__uint_as_float(r[e])), y);
           }
         }
         tc_fence_before();
         if (!last) {
           fence_proxy_async();
-          mbar_arrive(&bars[wg]);
+          mbar_arrive(&S.bars[slot]);
         }
       }
-      if (valid) sink_store(sink, sidx, p, y + bo);
+      // head: combine the two column halves, fused scatter (N5)
+      float* yp = S.ypart + slot * kRows;
+      if (half == 1) yp[row] = y;
+      named_sync(3 + slot, 256);
+      if (half == 0 && valid) sink_store(sink, sidx, p, y + yp[row] + __ldg(net.bo));
     }
   }
   tc_fence_before();
@@ -285,11 +408,6 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, const float* 
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
   }
-}
-
-size_t smem_bytes(int n_hidden) {
-  return 1024 + (size_t)n_hidden * kTile + 2 * kTile + (size_t)64 * kQStride * 4 + (size_t)kMaxHidden * kD * 4 +
-         (size_t)kD * 4 + 64;
 }
 
 }  // namespace tc

@@ -21,6 +21,12 @@ constexpr int kD = 128;            // SDNet width (G7)
 constexpr int kC1 = 8;             // conv channels 1 -> 8 -> 1, k = 5 (G7)
 constexpr int kK = 5;
 constexpr int kMaxHidden = 3;
+// 16-bit tensor-core image of one hidden layer: the 128 x 128 weight block
+// (SWIZZLE_128B K-major, 32 KB) followed by a 128 x 16 bias block (SWIZZLE_NONE
+// K-major, 4 KB) whose columns 0/1 hold the bias split b = b_hi + b_lo.
+constexpr int kWImgW = kD * kD;             // elements
+constexpr int kWImgB = kD * 16;
+constexpr int kWImg = kWImgW + kWImgB;      // 18432 elements = 36 KB
 
 // Local lattice of one rank: horizontal lines y = RY0 + 16 i
 // (x-contiguous, RX0..RX1) then vertical lines x = RX0 + 16 j (y-contiguous,
