@@ -148,6 +148,7 @@ void carve(mfp_ctx* c, void* base, size_t* total) {
   const int64_t oW1 = 89, oW2 = oW1 + kD * kNB, ob1 = oW2 + 2 * kD, oWh0 = ob1 + kD;
   const int64_t owo = oWh0 + (int64_t)nh * (kD * kD + kD);
   dn.b1 = P ? P + ob1 : nullptr;
+  dn.W2 = P ? P + oW2 : nullptr;
   dn.wo = P ? P + owo : nullptr;
   dn.bo = P ? P + owo + kD : nullptr;
   dn.n_hidden = nh;

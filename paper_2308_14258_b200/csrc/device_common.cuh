@@ -64,6 +64,22 @@ __device__ __forceinline__ int64_t centre_cell(int a, int b, int p, int strideH,
   return (int64_t)(b + 1) * strideH + lx + k;
 }
 
+// Local normalised query coordinates (x/m, y/m): centre lines (G3, q = 61) or
+// the interior grid (q = 961, i fastest).
+__device__ __forceinline__ void query_xy(int q, int p, float* x, float* y) {
+  if (q == kQC) {
+    if (p < kM - 1) { *x = 0.5f; *y = (float)(p + 1) / kM; }
+    else {
+      const int j = p - (kM - 1);
+      const int k = j + 1 + (j >= kH - 1 ? 1 : 0);
+      *x = (float)k / kM; *y = 0.5f;
+    }
+  } else {
+    *x = (float)(p % (kM - 1) + 1) / kM;
+    *y = (float)(p / (kM - 1) + 1) / kM;
+  }
+}
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -11,21 +11,6 @@
 
 namespace mfp {
 
-// Query coordinates: centre lines (G3) and interior grid.
-__device__ __forceinline__ void query_xy(int q, int p, float* x, float* y) {
-  if (q == kQC) {
-    if (p < kM - 1) { *x = 0.5f; *y = (float)(p + 1) / kM; }
-    else {
-      int j = p - (kM - 1);
-      int k = j + 1 + (j >= kH - 1 ? 1 : 0);
-      *x = (float)k / kM; *y = 0.5f;
-    }
-  } else {
-    *x = (float)(p % (kM - 1) + 1) / kM;
-    *y = (float)(p / (kM - 1) + 1) / kM;
-  }
-}
-
 // Byte offset of element (row r, k) in a 128 x 128 bf16 K-major tile stored as
 // two SW128 atoms-columns (k < 64, k >= 64) of 16 KB each: 128 B rows, the
 // 16-byte chunk index XOR-ed with (r mod 8) — the layout tcgen05 smem

@@ -5,22 +5,27 @@
 // dense contraction: rows = (subdomain, query) pairs packed densely
 // (row = s*q + p), K = N = d = 128.  Design:
 //   * persistent CTAs (one per SM), 128-row tiles (UMMA M = 128, N = 128,
-//     K = 16 x 8 per layer), fp32 accumulators in TMEM (2 x 128 columns);
+//     K = 16 x 8 per layer + one K = 16 bias step), fp32 accumulators in TMEM
+//     (3 slots x 128 columns);
 //   * the n_hidden weight matrices stay resident in shared memory for the
 //     whole kernel as 16-bit SWIZZLE_128B K-major images (B operand), pre-
-//     scaled by 1/2 (exact) because the epilogue produces h' = 2 GELU(x);
+//     scaled by 1/2 (exact) because the epilogue produces h' = 2 GELU(x); each
+//     image carries a bias block (b = b_hi + b_lo in two K columns) that a
+//     constant ones-column A block adds on the tensor core;
 //   * warp 0 issues tcgen05.mma from one lane and commits to an mbarrier;
-//     warp 1 owns the TMEM allocation; warps 2..17 form four epilogue
-//     warpgroups: two per tile slot (ping-pong over 2 slots), each owning 64
-//     of the 128 accumulator columns of its slot's tile;
-//   * epilogue of a layer feeding another MMA: tcgen05.ld -> +bias (fp32) ->
-//     round to 16 bit -> packed GELU (HFMA2 + MUFU tanh on x2 lanes) ->
-//     st.shared into the swizzled A operand -> fence.proxy.async -> arrive;
-//   * the layer-1 input is Eq. 5's broadcasted sum GELU(z[s] + Q[p]) (z for the
-//     <= 4 subdomains of a tile staged in smem, Q = X W2^T resident in smem for
-//     the 61 centre-line queries); the last layer's epilogue stays fp32 (GELU +
-//     head dot y = wo.h + bo; the head cancels strongly) and the
-//     two column halves combine through smem before the fused scatter (N5).
+//     warp 1 owns the TMEM allocation; warps 2..13 form three epilogue
+//     warpgroups, one per tile slot, so up to three tiles are in flight and
+//     the GELU pipes (MUFU tanh is the binding unit) stay fed
+//     while other tiles sit in the tensor core;
+//   * epilogue of a layer feeding another MMA: tcgen05.ld -> round to 16 bit
+//     -> packed GELU (HFMA2 + MUFU tanh) -> st.shared into the swizzled A
+//     operand -> fence.proxy.async -> mbarrier arrive;
+//   * the layer-1 input is Eq. 5's broadcasted sum GELU(z[s] + W2 x_p): z of
+//     the <= 4 subdomains of a tile staged in smem (prefetched into registers
+//     one tile ahead), W2 x_p recomputed with two FMAs per element (no Q table
+//     in smem); the last layer's epilogue stays fp32 (GELU + head dot
+//     y = wo.h + bo; the head cancels strongly) followed by the
+//     fused scatter onto the lattice (N5).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -30,13 +35,14 @@ namespace mfp {
 namespace tc {
 
 constexpr int kRows = 128;
-constexpr int kEpiWarps = 16;
-constexpr int kThreads = 32 * (2 + kEpiWarps);  // 576
-constexpr int kTile = kRows * kD * 2;           // 32 KB 16-bit operand image
-constexpr int kQStride = 132;                   // padded fp32 row of the smem Q table
-constexpr int kTmemCols = 256;
-constexpr int kZRows = 4;                       // subdomains one 128-row tile can touch (q >= 61)
-constexpr float kG0 = 0.7978845608028654f;      // sqrt(2/pi)
+constexpr int kSlots = 3;
+constexpr int kThreads = 32 * (2 + 4 * kSlots);  // 448
+constexpr int kTile = kRows * kD * 2;            // 32 KB 16-bit operand image
+constexpr int kWTile = kWImg * 2;                // 36 KB per hidden layer: weights (SW128) + bias block
+constexpr int kOnes = kRows * 16 * 2;            // 4 KB constant A block: K columns 0/1 = 1
+constexpr int kTmemCols = 512;
+constexpr int kZRows = 4;                        // subdomains one 128-row tile can touch (q >= 61)
+constexpr float kG0 = 0.7978845608028654f;       // sqrt(2/pi)
 constexpr float kG1 = 0.7978845608028654f * 0.044715f;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -58,6 +64,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -74,6 +91,15 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   d |= (uint64_t)(1024 >> 4) << 32;
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;
+  return d;
+}
+// SWIZZLE_NONE K-major descriptor for the K = 16 bias step: 8-row x 16-byte
+// core matrices, LBO = 128 B (next 8 K elements), SBO = 256 B (next 8 rows).
+__device__ __forceinline__ uint64_t nosw_desc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(128 >> 4) << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
   return d;
 }
 
@@ -187,28 +213,14 @@ __device__ __forceinline__ void act8(const float (&v)[8], uint32_t (&w)[4], uint
   }
 }
 
-constexpr int kWTile = kWImg * 2;   // 36 KB per hidden layer: weights (SW128) + bias block
-constexpr int kOnes = kRows * 16 * 2;  // 4 KB constant A block: columns 0/1 = 1
-
-// SWIZZLE_NONE K-major descriptor for the K = 16 bias step: 8-row x 16-byte
-// core matrices, LBO = 128 B (next 8 K elements), SBO = 256 B (next 8 rows).
-__device__ __forceinline__ uint64_t nosw_desc(uint32_t saddr) {
-  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)(128 >> 4) << 16;
-  d |= (uint64_t)(256 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  return d;
-}
-
 struct Smem {
   uint8_t* W;      // [nh][36 KB]
-  uint8_t* A;      // [2][32 KB]
+  uint8_t* A;      // [3][32 KB]
   uint8_t* ones;   // 4 KB
-  float* Q;        // [64][132]
-  float* zbuf;     // [2][4][128]
-  float* ypart;    // [2][128]
+  float* zbuf;     // [3][4][128]
+  float* w2;       // [2][128]: W2[:,0], W2[:,1]
   float* wo;       // [128]
-  uint64_t* bars;  // a_full[2], d_full[2]
+  uint64_t* bars;  // a_full[3], d_full[3]
   uint32_t* tmem_slot;
 };
 
@@ -217,28 +229,25 @@ struct Smem {
 // address space visible to the compiler (LDS/STS, not generic LD/ST).
 __device__ __forceinline__ Smem carve(uint8_t* raw, int nh) {
   Smem s;
-  uint8_t* base = raw;
-  s.W = base;
-  s.A = base + nh * kWTile;
-  s.ones = s.A + 2 * kTile;
-  s.Q = (float*)(s.ones + kOnes);
-  s.zbuf = s.Q + 64 * kQStride;
-  s.ypart = s.zbuf + 2 * kZRows * kD;
-  s.wo = s.ypart + 2 * kRows;
+  s.W = raw;
+  s.A = raw + nh * kWTile;
+  s.ones = s.A + kSlots * kTile;
+  s.zbuf = (float*)(s.ones + kOnes);
+  s.w2 = s.zbuf + kSlots * kZRows * kD;
+  s.wo = s.w2 + 2 * kD;
   s.bars = (uint64_t*)(s.wo + kD);
-  s.tmem_slot = (uint32_t*)(s.bars + 4);
+  s.tmem_slot = (uint32_t*)(s.bars + 2 * kSlots);
   return s;
 }
 
 size_t smem_bytes(int n_hidden) {
-  return (size_t)n_hidden * kWTile + 2 * kTile + kOnes +
-         4 * ((size_t)64 * kQStride + 2 * kZRows * kD + 2 * kRows + kD) + 64;
+  return (size_t)n_hidden * kWTile + kSlots * kTile + kOnes + 4 * ((size_t)kSlots * kZRows * kD + 3 * kD) +
+         16 * kSlots + 16;
 }
 
 template <int GELU, int F16>
 __global__ void __launch_bounds__(kThreads, 1)
-k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, const float* __restrict__ Qg,
-           DevNet net, Sink sink) {
+k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, Sink sink) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int nh = net.n_hidden;
   const Smem S = carve(smem_raw, nh);
@@ -249,24 +258,25 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, const float* 
     const uint4* src = reinterpret_cast<const uint4*>(net.Wh_sw);
     uint4* dst = reinterpret_cast<uint4*>(S.W);
     for (int i = threadIdx.x; i < nh * kWTile / 16; i += kThreads) dst[i] = __ldg(src + i);
-    if (q == kQC)
-      for (int i = threadIdx.x; i < 64 * kD; i += kThreads) S.Q[(i >> 7) * kQStride + (i & 127)] = __ldg(net.Qc + i);
-    for (int i = threadIdx.x; i < kD; i += kThreads) S.wo[i] = (GELU == 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
+    for (int i = threadIdx.x; i < kD; i += kThreads) {
+      S.wo[i] = (GELU == 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
+      S.w2[i] = __ldg(net.W2 + 2 * i);
+      S.w2[kD + i] = __ldg(net.W2 + 2 * i + 1);
+    }
     // constant A block of the bias step: row r, K columns 0/1 = 1.0, others 0
     if (threadIdx.x < kRows) {
       const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
       const int r = threadIdx.x;
-      uint4* p0 = reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + (r & 7) * 16);
-      *p0 = make_uint4(one | (one << 16), 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + (r & 7) * 16) = make_uint4(one | (one << 16), 0u, 0u, 0u);
       *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + 128 + (r & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
     }
   }
   if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();  // SW128 atoms need 1024 B alignment
   if (threadIdx.x == 0) {
-    mbar_init(&S.bars[0], 256);
-    mbar_init(&S.bars[1], 256);
-    mbar_init(&S.bars[2], 1);
-    mbar_init(&S.bars[3], 1);
+    for (int s = 0; s < kSlots; s++) {
+      mbar_init(&S.bars[s], 128);           // a_full[s]: the slot's 128 epilogue threads
+      mbar_init(&S.bars[kSlots + s], 1);    // d_full[s]: tcgen05.commit
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -275,7 +285,7 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, const float* 
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  fence_proxy_async();  // generic-proxy writes of W visible to the tensor core
+  fence_proxy_async();  // generic-proxy writes of W / ones visible to the tensor core
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -286,105 +296,127 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, const float* 
   const int64_t nsub = total_rows / q;
 
   if (warp == 0) {
-    // ---- MMA issuer: round-robin over (tile pair, layer, slot)
+    // ---- MMA issuer: serve whichever slot has its A operand ready (no
+    // head-of-line blocking behind a slow slot); per slot the (tile, layer)
+    // sequence is in order.
     if (lane == 0) {
-      uint32_t pa[2] = {0u, 0u};
-      for (int64_t j0 = 0; j0 < nloc; j0 += 2) {
-        for (int l = 0; l < nh; l++) {
-          for (int s = 0; s < 2; s++) {
-            if (j0 + s >= nloc) continue;
-            mbar_wait(&S.bars[s], pa[s]);
-            pa[s] ^= 1u;
-            tc_fence_after();
-            const uint32_t a0 = smem_u32(S.A + s * kTile), b0 = smem_u32(S.W + l * kWTile);
-            const uint32_t d = tmem + (uint32_t)(s * kD);
+      uint32_t pa[kSlots] = {0u, 0u, 0u};
+      int64_t jn[kSlots];
+      int ln[kSlots] = {0, 0, 0};
+      int active = 0;
 #pragma unroll
-            for (int k = 0; k < kD / 16; k++) {
-              const uint32_t off = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
-              mma_f16<F16>(d, sw128_desc(a0 + off), sw128_desc(b0 + off), k > 0 ? 1u : 0u);
-            }
-            // bias step: D += [1 1 0..] [b_hi b_lo 0..]^T
-            mma_f16<F16>(d, nosw_desc(smem_u32(S.ones)), nosw_desc(b0 + (uint32_t)(kWImgW * 2)), 1u);
-            mma_commit(&S.bars[2 + s]);
+      for (int s = 0; s < kSlots; s++) {
+        jn[s] = s;
+        active += (s < nloc) ? 1 : 0;
+      }
+      const uint32_t ones_desc_addr = smem_u32(S.ones);
+      while (active > 0) {
+#pragma unroll
+        for (int s = 0; s < kSlots; s++) {
+          if (jn[s] >= nloc || !mbar_test(&S.bars[s], pa[s])) continue;
+          pa[s] ^= 1u;
+          tc_fence_after();
+          const int l = ln[s];
+          const uint32_t a0 = smem_u32(S.A + s * kTile), b0 = smem_u32(S.W + l * kWTile);
+          const uint32_t d = tmem + (uint32_t)(s * kD);
+#pragma unroll
+          for (int k = 0; k < kD / 16; k++) {
+            const uint32_t off = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
+            mma_f16<F16>(d, sw128_desc(a0 + off), sw128_desc(b0 + off), k > 0 ? 1u : 0u);
+          }
+          // bias step: D += [1 1 0..] [b_hi b_lo 0..]^T
+          mma_f16<F16>(d, nosw_desc(ones_desc_addr), nosw_desc(b0 + (uint32_t)(kWImgW * 2)), 1u);
+          mma_commit(&S.bars[kSlots + s]);
+          if (++ln[s] == nh) {
+            ln[s] = 0;
+            jn[s] += kSlots;
+            if (jn[s] >= nloc) active--;
           }
         }
       }
     }
     __syncwarp();
   } else if (warp >= 2) {
-    // ---- epilogue: 4 warpgroups = 2 slots x 2 column halves
-    const int ew = warp - 2;
-    const int wg = ew >> 2, slot = wg >> 1, half = wg & 1;
+    // ---- epilogue: warpgroup `slot` owns every third local tile
+    const int slot = (warp - 2) >> 2;
     const int quad = warp & 3;                       // TMEM lane quadrant of this warp
     const int row = quad * 32 + lane;                // tile row == TMEM lane
-    const int tid_s = half * 128 + row;              // 0..255 within the slot
-    const int c_lo = half * 64;
-    uint8_t* A = S.A + slot * kTile;
-    const uint32_t a_base = smem_u32(A);
-    const uint32_t t_row = tmem + (uint32_t)(slot * kD + c_lo) + ((uint32_t)(quad * 32) << 16);
+    const int tid_s = (warp - 2 - 4 * slot) * 32 + lane;  // 0..127 within the slot
+    const uint32_t a_base = smem_u32(S.A + slot * kTile);
+    const uint32_t t_row = tmem + (uint32_t)(slot * kD) + ((uint32_t)(quad * 32) << 16);
     float* zb = S.zbuf + slot * kZRows * kD;
     const uint32_t c0 = pack2<F16>(kG0, kG0), c1 = pack2<F16>(kG1, kG1);
+    const float bo = __ldg(net.bo);
+    // z staging: thread tid_s moves 4 consecutive floats of the tile's <= 4 subdomains
+    const int zi = 4 * tid_s, zr_ = zi >> 7, zc = zi & 127;
+    auto z_fetch = [&](int64_t j) -> float4 {
+      const int64_t t = blockIdx.x + j * (int64_t)gridDim.x;
+      int64_t sidx = (t * kRows) / q + zr_;
+      if (sidx > nsub - 1) sidx = nsub - 1;
+      return __ldg(reinterpret_cast<const float4*>(z + sidx * kD + zc));
+    };
+    if (slot < nloc) *reinterpret_cast<float4*>(zb + zi) = z_fetch(slot);
     uint32_t pd = 0u;
-    for (int64_t j = slot; j < nloc; j += 2) {
+    for (int64_t j = slot; j < nloc; j += kSlots) {
       const int64_t tile = blockIdx.x + j * (int64_t)gridDim.x;
       const int64_t row0 = tile * kRows;
       const int64_t s_first = row0 / q;
-      // stage z of the <= 4 subdomains this tile touches (coalesced, 2 floats per thread)
-      {
-        const int idx = 2 * tid_s, r = idx >> 7, c = idx & 127;
-        int64_t sidx = s_first + r;
-        if (sidx > nsub - 1) sidx = nsub - 1;
-        *reinterpret_cast<float2*>(zb + idx) = __ldg(reinterpret_cast<const float2*>(z + sidx * kD + c));
-      }
-      named_sync(1 + slot, 256);
+      named_sync(1 + slot, 128);                     // zbuf of this tile visible
+      const bool have_next = j + kSlots < nloc;
+      float4 znext = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (have_next) znext = z_fetch(j + kSlots);    // prefetch, consumed after the last layer
       const int64_t grow = row0 + row;
       const bool valid = grow < total_rows;
       const int64_t gr = valid ? grow : total_rows - 1;
       const int64_t sidx = gr / q;
       const int p = (int)(gr - sidx * q);
-      // layer-1 input (Eq. 5): h' = 2 GELU(z[s] + Q[p]) -> A operand
+      float qx, qy;
+      query_xy(q, p, &qx, &qy);
+      // layer-1 input (Eq. 5): h' = 2 GELU(z[s] + W2 x_p) -> A operand
       {
-        const float* zr = zb + (int)(sidx - s_first) * kD + c_lo;
-        const float* qr = q == kQC ? S.Q + p * kQStride + c_lo : Qg + (int64_t)p * kD + c_lo;
+        const float* zr = zb + (int)(sidx - s_first) * kD;
 #pragma unroll 2
-        for (int cc = 0; cc < 8; cc++) {
+        for (int cc = 0; cc < kD / 8; cc++) {
           const float4 z0 = *reinterpret_cast<const float4*>(zr + cc * 8);
           const float4 z1 = *reinterpret_cast<const float4*>(zr + cc * 8 + 4);
-          const float4 q0 = *reinterpret_cast<const float4*>(qr + cc * 8);
-          const float4 q1 = *reinterpret_cast<const float4*>(qr + cc * 8 + 4);
-          const float v[8] = {z0.x + q0.x, z0.y + q0.y, z0.z + q0.z, z0.w + q0.w,
-                              z1.x + q1.x, z1.y + q1.y, z1.z + q1.z, z1.w + q1.w};
+          const float4 a0 = *reinterpret_cast<const float4*>(S.w2 + cc * 8);
+          const float4 a1 = *reinterpret_cast<const float4*>(S.w2 + cc * 8 + 4);
+          const float4 b0 = *reinterpret_cast<const float4*>(S.w2 + kD + cc * 8);
+          const float4 b1 = *reinterpret_cast<const float4*>(S.w2 + kD + cc * 8 + 4);
+          const float v[8] = {z0.x + fmaf(a0.x, qx, b0.x * qy), z0.y + fmaf(a0.y, qx, b0.y * qy),
+                              z0.z + fmaf(a0.z, qx, b0.z * qy), z0.w + fmaf(a0.w, qx, b0.w * qy),
+                              z1.x + fmaf(a1.x, qx, b1.x * qy), z1.y + fmaf(a1.y, qx, b1.y * qy),
+                              z1.z + fmaf(a1.z, qx, b1.z * qy), z1.w + fmaf(a1.w, qx, b1.w * qy)};
           uint32_t w[4];
           act8<GELU, F16>(v, w, c0, c1);
-          st_shared_v4(a_base + sw128_off(row, c_lo + cc * 8), w[0], w[1], w[2], w[3]);
+          st_shared_v4(a_base + sw128_off(row, cc * 8), w[0], w[1], w[2], w[3]);
         }
       }
       fence_proxy_async();
       mbar_arrive(&S.bars[slot]);
       float y = 0.f;
       for (int l = 0; l < nh; l++) {
-        mbar_wait(&S.bars[2 + slot], pd);
+        mbar_wait(&S.bars[kSlots + slot], pd);
         pd ^= 1u;
         tc_fence_after();
         const bool last = (l == nh - 1);
 #pragma unroll 1
-        for (int ch = 0; ch < 2; ch++) {
+        for (int ch = 0; ch < kD / 32; ch++) {
           uint32_t r[32];
           tmem_ld32(t_row + (uint32_t)(ch * 32), r);
           tmem_wait_ld();
           if (!last) {
 #pragma unroll
             for (int c8 = 0; c8 < 4; c8++) {
-              const int c = ch * 32 + c8 * 8;
               float v[8];
 #pragma unroll
               for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[c8 * 8 + e]);  // bias already in D
               uint32_t w[4];
               act8<GELU, F16>(v, w, c0, c1);
-              st_shared_v4(a_base + sw128_off(row, c_lo + c), w[0], w[1], w[2], w[3]);
+              st_shared_v4(a_base + sw128_off(row, ch * 32 + c8 * 8), w[0], w[1], w[2], w[3]);
             }
           } else {
-            const float* wo = S.wo + c_lo + ch * 32;
+            const float* wo = S.wo + ch * 32;
 #pragma unroll
             for (int e = 0; e < 32; e++) y = fmaf(wo[e], act_head<GELU>(__uint_as_float(r[e])), y);
           }
@@ -395,11 +427,10 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, const float* 
           mbar_arrive(&S.bars[slot]);
         }
       }
-      // head: combine the two column halves, fused scatter (N5)
-      float* yp = S.ypart + slot * kRows;
-      if (half == 1) yp[row] = y;
-      named_sync(3 + slot, 256);
-      if (half == 0 && valid) sink_store(sink, sidx, p, y + yp[row] + __ldg(net.bo));
+      // every thread of the slot finished reading zbuf (the layer MMAs needed
+      // all 128 arrivals), so the prefetched z of the next tile can land
+      if (have_next) *reinterpret_cast<float4*>(zb + zi) = znext;
+      if (valid) sink_store(sink, sidx, p, y + bo);   // fused scatter (N5)
     }
   }
   tc_fence_before();
@@ -430,13 +461,12 @@ void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const 
   const int64_t rows = B * q;
   const int64_t tiles = (rows + tc::kRows - 1) / tc::kRows;
   const int grid = (int)(tiles < num_sms ? tiles : num_sms);
-  const float* Qg = q == kQC ? net.Qc : net.Qf;
   if (net.f16) {
-    if (net.gelu_tanh) tc::k_chain_tc<1, 1><<<grid, tc::kThreads, sm, s>>>(z, rows, q, Qg, net, sink);
-    else tc::k_chain_tc<0, 1><<<grid, tc::kThreads, sm, s>>>(z, rows, q, Qg, net, sink);
+    if (net.gelu_tanh) tc::k_chain_tc<1, 1><<<grid, tc::kThreads, sm, s>>>(z, rows, q, net, sink);
+    else tc::k_chain_tc<0, 1><<<grid, tc::kThreads, sm, s>>>(z, rows, q, net, sink);
   } else {
-    if (net.gelu_tanh) tc::k_chain_tc<1, 0><<<grid, tc::kThreads, sm, s>>>(z, rows, q, Qg, net, sink);
-    else tc::k_chain_tc<0, 0><<<grid, tc::kThreads, sm, s>>>(z, rows, q, Qg, net, sink);
+    if (net.gelu_tanh) tc::k_chain_tc<1, 0><<<grid, tc::kThreads, sm, s>>>(z, rows, q, net, sink);
+    else tc::k_chain_tc<0, 0><<<grid, tc::kThreads, sm, s>>>(z, rows, q, net, sink);
   }
 }
 

@@ -78,6 +78,7 @@ struct DevNet {
   const float* conv2_b;  // [1]
   const float* W1T;      // [128 k][128 d]   (W1 transposed)
   const float* b1;       // [d]
+  const float* W2;       // [d][2] (query half of the split layer, Eq. 5)
   const float* QTc;      // [d][64]  centre queries Q = X W2^T (b1 folded into z)
   const float* QTf;      // [d][961] interior queries
   const float* WhT;      // [n_hidden][k][n] fp32 (transposed for SIMT)
