@@ -61,28 +61,34 @@ k_gather_embed(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __r
   const int edge = lane >> 3, t0 = 4 * (lane & 7);
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   for (int64_t base = (int64_t)blockIdx.x * kEmbSub; base < B; base += (int64_t)gridDim.x * kEmbSub) {
-    // ---- phase A: gather + conv stack, 8 subdomains per warp
+    // ---- phase A: gather + conv stack, 8 subdomains per warp.  All 8
+    // perimeter gathers are issued up front (one exposed L2 latency per round).
+    float4 gpre[kEmbPerWarp];
+#pragma unroll
     for (int j = 0; j < kEmbPerWarp; j++) {
-      const int col = warp * kEmbPerWarp + j;
-      int64_t s = base + col;
+      int64_t s = base + warp * kEmbPerWarp + j;
       if (s > B - 1) s = B - 1;
-      float4 gv;
       if (gb) {
-        gv = __ldg(reinterpret_cast<const float4*>(gb + s * kNB + i0));
+        gpre[j] = __ldg(reinterpret_cast<const float4*>(gb + s * kNB + i0));
       } else {
         int a, b;
         unpack_anchor(__ldg(anchors + s), a, b);
         const int lx = kH * a, ly = kH * b;
-        if (edge == 0) gv = *reinterpret_cast<const float4*>(lat + (int64_t)b * L.strideH + lx + t0);
-        else if (edge == 1) gv = *reinterpret_cast<const float4*>(lat + L.offV + (int64_t)(a + 2) * L.strideV + ly + t0);
+        if (edge == 0) gpre[j] = *reinterpret_cast<const float4*>(lat + (int64_t)b * L.strideH + lx + t0);
+        else if (edge == 1) gpre[j] = *reinterpret_cast<const float4*>(lat + L.offV + (int64_t)(a + 2) * L.strideV + ly + t0);
         else if (edge == 2) {
           const float* r = lat + (int64_t)(b + 2) * L.strideH + lx + kM - t0;
-          gv = make_float4(r[0], r[-1], r[-2], r[-3]);
+          gpre[j] = make_float4(r[0], r[-1], r[-2], r[-3]);
         } else {
           const float* r = lat + L.offV + (int64_t)a * L.strideV + ly + kM - t0;
-          gv = make_float4(r[0], r[-1], r[-2], r[-3]);
+          gpre[j] = make_float4(r[0], r[-1], r[-2], r[-3]);
         }
       }
+    }
+#pragma unroll
+    for (int j = 0; j < kEmbPerWarp; j++) {
+      const int col = warp * kEmbPerWarp + j;
+      const float4 gv = gpre[j];
       *reinterpret_cast<float4*>(g + i0) = gv;
       __syncwarp();
       // conv1 on positions i0..i0+3 from the window g[i0-2 .. i0+5]

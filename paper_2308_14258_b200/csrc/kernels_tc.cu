@@ -296,41 +296,30 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, S
   const int64_t nsub = total_rows / q;
 
   if (warp == 0) {
-    // ---- MMA issuer: serve whichever slot has its A operand ready (no
-    // head-of-line blocking behind a slow slot); per slot the (tile, layer)
-    // sequence is in order.
+    // ---- MMA issuer: round-robin over (tile group, layer, slot).  (Serving
+    // slots out of order with mbarrier.test_wait polling measured slower: the
+    // poll loop steals issue slots from the epilogue warps on its SMSP.)
     if (lane == 0) {
       uint32_t pa[kSlots] = {0u, 0u, 0u};
-      int64_t jn[kSlots];
-      int ln[kSlots] = {0, 0, 0};
-      int active = 0;
-#pragma unroll
-      for (int s = 0; s < kSlots; s++) {
-        jn[s] = s;
-        active += (s < nloc) ? 1 : 0;
-      }
       const uint32_t ones_desc_addr = smem_u32(S.ones);
-      while (active > 0) {
+      for (int64_t j0 = 0; j0 < nloc; j0 += kSlots) {
+        for (int l = 0; l < nh; l++) {
 #pragma unroll
-        for (int s = 0; s < kSlots; s++) {
-          if (jn[s] >= nloc || !mbar_test(&S.bars[s], pa[s])) continue;
-          pa[s] ^= 1u;
-          tc_fence_after();
-          const int l = ln[s];
-          const uint32_t a0 = smem_u32(S.A + s * kTile), b0 = smem_u32(S.W + l * kWTile);
-          const uint32_t d = tmem + (uint32_t)(s * kD);
+          for (int s = 0; s < kSlots; s++) {
+            if (j0 + s >= nloc) continue;
+            mbar_wait(&S.bars[s], pa[s]);
+            pa[s] ^= 1u;
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(S.A + s * kTile), b0 = smem_u32(S.W + l * kWTile);
+            const uint32_t d = tmem + (uint32_t)(s * kD);
 #pragma unroll
-          for (int k = 0; k < kD / 16; k++) {
-            const uint32_t off = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
-            mma_f16<F16>(d, sw128_desc(a0 + off), sw128_desc(b0 + off), k > 0 ? 1u : 0u);
-          }
-          // bias step: D += [1 1 0..] [b_hi b_lo 0..]^T
-          mma_f16<F16>(d, nosw_desc(ones_desc_addr), nosw_desc(b0 + (uint32_t)(kWImgW * 2)), 1u);
-          mma_commit(&S.bars[kSlots + s]);
-          if (++ln[s] == nh) {
-            ln[s] = 0;
-            jn[s] += kSlots;
-            if (jn[s] >= nloc) active--;
+            for (int k = 0; k < kD / 16; k++) {
+              const uint32_t off = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
+              mma_f16<F16>(d, sw128_desc(a0 + off), sw128_desc(b0 + off), k > 0 ? 1u : 0u);
+            }
+            // bias step: D += [1 1 0..] [b_hi b_lo 0..]^T
+            mma_f16<F16>(d, nosw_desc(ones_desc_addr), nosw_desc(b0 + (uint32_t)(kWImgW * 2)), 1u);
+            mma_commit(&S.bars[kSlots + s]);
           }
         }
       }
@@ -400,25 +389,30 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, S
         pd ^= 1u;
         tc_fence_after();
         const bool last = (l == nh - 1);
+        // two 32-column TMEM loads in flight per wait
 #pragma unroll 1
-        for (int ch = 0; ch < kD / 32; ch++) {
-          uint32_t r[32];
-          tmem_ld32(t_row + (uint32_t)(ch * 32), r);
+        for (int ch = 0; ch < kD / 32; ch += 2) {
+          uint32_t r[2][32];
+          tmem_ld32(t_row + (uint32_t)(ch * 32), r[0]);
+          tmem_ld32(t_row + (uint32_t)(ch * 32 + 32), r[1]);
           tmem_wait_ld();
-          if (!last) {
 #pragma unroll
-            for (int c8 = 0; c8 < 4; c8++) {
-              float v[8];
+          for (int h = 0; h < 2; h++) {
+            if (!last) {
 #pragma unroll
-              for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[c8 * 8 + e]);  // bias already in D
-              uint32_t w[4];
-              act8<GELU, F16>(v, w, c0, c1);
-              st_shared_v4(a_base + sw128_off(row, ch * 32 + c8 * 8), w[0], w[1], w[2], w[3]);
+              for (int c8 = 0; c8 < 4; c8++) {
+                float v[8];
+#pragma unroll
+                for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[h][c8 * 8 + e]);  // bias already in D
+                uint32_t w[4];
+                act8<GELU, F16>(v, w, c0, c1);
+                st_shared_v4(a_base + sw128_off(row, (ch + h) * 32 + c8 * 8), w[0], w[1], w[2], w[3]);
+              }
+            } else {
+              const float* wo = S.wo + (ch + h) * 32;
+#pragma unroll
+              for (int e = 0; e < 32; e++) y = fmaf(wo[e], act_head<GELU>(__uint_as_float(r[h][e])), y);
             }
-          } else {
-            const float* wo = S.wo + ch * 32;
-#pragma unroll
-            for (int e = 0; e < 32; e++) y = fmaf(wo[e], act_head<GELU>(__uint_as_float(r[e])), y);
           }
         }
         tc_fence_before();
