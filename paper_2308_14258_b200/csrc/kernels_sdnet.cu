@@ -15,16 +15,29 @@ namespace mfp {
 // A block embeds 64 subdomains per round.  Phase A (per warp, 8 subdomains):
 // gather the 128 perimeter values (G1 order), conv1 (1 -> 8, k = 5, circular)
 // + GELU and conv2 (8 -> 1) + GELU with each lane owning 4 consecutive
-// positions (3 LDS.128 windows per channel), e written k-major into smem.
+// positions; the circular neighbours come from the adjacent lanes by warp
+// shuffles (no per-warp smem), e written k-major into smem.
 // Phase B (whole block): z = e W1^T + b1 as a register-tiled 64 x 128 x 128
 // SIMT GEMM — W1^T (64 KB, smem-resident) is read once per 64 subdomains.
+// ~99 KB of smem per block: two blocks per SM.
 // z is the boundary half of the split layer (Eq. 5); the query half
 // Q = X W2^T is a per-query constant table built at init.
 constexpr int kEmbWarps = 8;
 constexpr int kEmbSub = 64;                  // subdomains per block round
 constexpr int kEmbPerWarp = kEmbSub / kEmbWarps;
 constexpr int kEs = kEmbSub + 4;             // padded row of e^T (bank spread)
-constexpr int kEmbSmem = (kNB * kD + kNB * kEs + 96 + kD + kEmbWarps * (kNB + kC1 * kNB)) * 4;
+constexpr int kEmbSmem = (kNB * kD + kNB * kEs + 96 + kD) * 4;
+
+// Window [i0-2, i0+5] of a circular length-128 signal held 4-per-lane (lane l
+// owns positions 4l..4l+3): two values from each neighbouring lane.
+__device__ __forceinline__ void circ_window(const float (&v)[4], int lane, float (&w)[8]) {
+  const int left = (lane + 31) & 31, right = (lane + 1) & 31;
+  w[0] = __shfl_sync(0xffffffffu, v[2], left);
+  w[1] = __shfl_sync(0xffffffffu, v[3], left);
+  w[2] = v[0]; w[3] = v[1]; w[4] = v[2]; w[5] = v[3];
+  w[6] = __shfl_sync(0xffffffffu, v[0], right);
+  w[7] = __shfl_sync(0xffffffffu, v[1], right);
+}
 
 template <int GELU>
 __device__ __forceinline__ float emb_act(float x) {
@@ -33,7 +46,7 @@ __device__ __forceinline__ float emb_act(float x) {
 }
 
 template <int GELU>
-__global__ void __launch_bounds__(kEmbWarps * 32, 1)
+__global__ void __launch_bounds__(kEmbWarps * 32, 2)
 k_gather_embed(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ anchors,
                const float* __restrict__ gb, int64_t B, DevNet net, float* __restrict__ z) {
   extern __shared__ float smem[];
@@ -41,7 +54,6 @@ k_gather_embed(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __r
   float* sE = sW1T + kNB * kD;               // e^T [128 k][68]
   float* sCw = sE + kNB * kEs;               // c1w[40] c1b[8] c2w[40] c2b[1]
   float* sB1 = sCw + 96;                     // b1 (the raw parameter block is not 16 B aligned)
-  float* sWarp = sB1 + kD;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   {
     const float4* src = reinterpret_cast<const float4*>(net.W1T);
@@ -54,10 +66,7 @@ k_gather_embed(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __r
     if (threadIdx.x == 0) sCw[88] = __ldg(net.conv2_b);
   }
   __syncthreads();
-  float* g = sWarp + warp * (kNB + kC1 * kNB);
-  float* c1 = g + kNB;
   const int i0 = 4 * lane;                   // this lane's 4 consecutive perimeter positions
-  const int im = (i0 - 4) & (kNB - 1), ip = (i0 + 4) & (kNB - 1);
   const int edge = lane >> 3, t0 = 4 * (lane & 7);
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   for (int64_t base = (int64_t)blockIdx.x * kEmbSub; base < B; base += (int64_t)gridDim.x * kEmbSub) {
@@ -88,47 +97,31 @@ k_gather_embed(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __r
 #pragma unroll
     for (int j = 0; j < kEmbPerWarp; j++) {
       const int col = warp * kEmbPerWarp + j;
-      const float4 gv = gpre[j];
-      *reinterpret_cast<float4*>(g + i0) = gv;
-      __syncwarp();
-      // conv1 on positions i0..i0+3 from the window g[i0-2 .. i0+5]
-      {
-        const float4 wm = *reinterpret_cast<const float4*>(g + im);
-        const float4 wp = *reinterpret_cast<const float4*>(g + ip);
-        const float win[8] = {wm.z, wm.w, gv.x, gv.y, gv.z, gv.w, wp.x, wp.y};
+      const float gv4[4] = {gpre[j].x, gpre[j].y, gpre[j].z, gpre[j].w};
+      float win[8];
+      circ_window(gv4, lane, win);
+      // conv1 (1 -> 8) + GELU on positions i0..i0+3, then conv2 (8 -> 1)
+      // accumulated channel by channel from each channel's shuffled window
+      float acc2[4] = {sCw[88], sCw[88], sCw[88], sCw[88]};
 #pragma unroll
-        for (int o = 0; o < kC1; o++) {
-          float acc[4];
+      for (int o = 0; o < kC1; o++) {
+        float c1v[4];
 #pragma unroll
-          for (int p = 0; p < 4; p++) {
-            float v = sCw[40 + o];
+        for (int p = 0; p < 4; p++) {
+          float v = sCw[40 + o];
 #pragma unroll
-            for (int t = 0; t < kK; t++) v = fmaf(sCw[o * kK + t], win[p + t], v);
-            acc[p] = emb_act<GELU>(v);
-          }
-          *reinterpret_cast<float4*>(c1 + o * kNB + i0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+          for (int t = 0; t < kK; t++) v = fmaf(sCw[o * kK + t], win[p + t], v);
+          c1v[p] = emb_act<GELU>(v);
         }
+        float w2[8];
+        circ_window(c1v, lane, w2);
+#pragma unroll
+        for (int p = 0; p < 4; p++)
+#pragma unroll
+          for (int t = 0; t < kK; t++) acc2[p] = fmaf(sCw[48 + o * kK + t], w2[p + t], acc2[p]);
       }
-      __syncwarp();
-      // conv2 (8 -> 1) + GELU -> e^T[:, col]
-      {
-        float acc[4] = {sCw[88], sCw[88], sCw[88], sCw[88]};
 #pragma unroll
-        for (int o = 0; o < kC1; o++) {
-          const float* row = c1 + o * kNB;
-          const float4 wm = *reinterpret_cast<const float4*>(row + im);
-          const float4 w0 = *reinterpret_cast<const float4*>(row + i0);
-          const float4 wp = *reinterpret_cast<const float4*>(row + ip);
-          const float win[8] = {wm.z, wm.w, w0.x, w0.y, w0.z, w0.w, wp.x, wp.y};
-#pragma unroll
-          for (int p = 0; p < 4; p++)
-#pragma unroll
-            for (int t = 0; t < kK; t++) acc[p] = fmaf(sCw[48 + o * kK + t], win[p + t], acc[p]);
-        }
-#pragma unroll
-        for (int p = 0; p < 4; p++) sE[(i0 + p) * kEs + col] = emb_act<GELU>(acc[p]);
-      }
-      __syncwarp();
+      for (int p = 0; p < 4; p++) sE[(i0 + p) * kEs + col] = emb_act<GELU>(acc2[p]);
     }
     __syncthreads();
     // ---- phase B: z[64 x 128] = e[64 x 128] W1^T, thread = 4 subdomains x 8 outputs
@@ -177,7 +170,7 @@ void launch_gather_embed(const float* lat, const LatticeGeom& L, const uint32_t*
     attr = true;
   }
   int64_t blocks = (B + kEmbSub - 1) / kEmbSub;
-  if (blocks > 148) blocks = 148;
+  if (blocks > 2 * 148) blocks = 2 * 148;   // two resident blocks per SM
   if (net.gelu_tanh)
     k_gather_embed<1><<<(int)blocks, kEmbWarps * 32, kEmbSmem, s>>>(lat, L, anchors, gb, B, net, z);
   else
