@@ -39,10 +39,20 @@ __global__ void k_prep(PrepArgs a) {
     const float w = Wl[(int64_t)n * d + k];
     a.WhT[i] = w;                                    // [l][k][n]
     uint8_t* img = reinterpret_cast<uint8_t*>(a.Wsw + (int64_t)l * kWImg);
+    // CTA-pair image: half n/64 holds rows n%64 as a 64-row SW128 K-major
+    // block (two 8 KB K-halves) followed by its 2 KB bias block
+    uint8_t* img2 = reinterpret_cast<uint8_t*>(a.Wsw2 + (int64_t)l * kWImg) + (n >> 6) * (kWImg);
+    const int rr = n & 63;
+    const uint32_t off2 = (uint32_t)((k >> 6) * 8192 + rr * 128 + ((((k & 63) >> 3) ^ (rr & 7)) << 4) + (k & 7) * 2);
     // B operand row n = output feature, K-major; scaled by 1/2 (exact) because
     // the tensor-core epilogue feeds h' = 2 GELU(x) into the next layer
-    if (a.f16) *reinterpret_cast<__half*>(img + sw128_offset(n, k)) = __float2half_rn(0.5f * w);
-    else *reinterpret_cast<__nv_bfloat16*>(img + sw128_offset(n, k)) = __float2bfloat16_rn(0.5f * w);
+    if (a.f16) {
+      *reinterpret_cast<__half*>(img + sw128_offset(n, k)) = __float2half_rn(0.5f * w);
+      *reinterpret_cast<__half*>(img2 + off2) = __float2half_rn(0.5f * w);
+    } else {
+      *reinterpret_cast<__nv_bfloat16*>(img + sw128_offset(n, k)) = __float2bfloat16_rn(0.5f * w);
+      *reinterpret_cast<__nv_bfloat16*>(img2 + off2) = __float2bfloat16_rn(0.5f * w);
+    }
   }
   for (int64_t i = tid; i < (int64_t)a.n_hidden * d; i += nth) {
     int l = (int)(i / d), c = (int)(i % d);
@@ -54,14 +64,21 @@ __global__ void k_prep(PrepArgs a) {
     // b_hi + b_lo (accurate to ~2^-17 relative) to the fp32 accumulator.
     uint8_t* blk = reinterpret_cast<uint8_t*>(a.Wsw + (int64_t)l * kWImg + kWImgW);
     const uint32_t off = (uint32_t)((c >> 3) * 256 + (c & 7) * 16);
+    const int rr = c & 63;
+    uint8_t* blk2 = reinterpret_cast<uint8_t*>(a.Wsw2 + (int64_t)l * kWImg) + (c >> 6) * kWImg + 16384;
+    const uint32_t off2 = (uint32_t)((rr >> 3) * 256 + (rr & 7) * 16);
     if (a.f16) {
-      const __half hi = __float2half_rn(b);
+      const __half hi = __float2half_rn(b), lo = __float2half_rn(b - __half2float(hi));
       *reinterpret_cast<__half*>(blk + off) = hi;
-      *reinterpret_cast<__half*>(blk + off + 2) = __float2half_rn(b - __half2float(hi));
+      *reinterpret_cast<__half*>(blk + off + 2) = lo;
+      *reinterpret_cast<__half*>(blk2 + off2) = hi;
+      *reinterpret_cast<__half*>(blk2 + off2 + 2) = lo;
     } else {
-      const __nv_bfloat16 hi = __float2bfloat16_rn(b);
+      const __nv_bfloat16 hi = __float2bfloat16_rn(b), lo = __float2bfloat16_rn(b - __bfloat162float(hi));
       *reinterpret_cast<__nv_bfloat16*>(blk + off) = hi;
-      *reinterpret_cast<__nv_bfloat16*>(blk + off + 2) = __float2bfloat16_rn(b - __bfloat162float(hi));
+      *reinterpret_cast<__nv_bfloat16*>(blk + off + 2) = lo;
+      *reinterpret_cast<__nv_bfloat16*>(blk2 + off2) = hi;
+      *reinterpret_cast<__nv_bfloat16*>(blk2 + off2 + 2) = lo;
     }
   }
   // Q = X W2^T (b1 is folded into z): centre (64 padded) and interior (961)

@@ -141,19 +141,26 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // Round two fp32 values to the operand type (lo -> bits 0-15).  fp16: F2FP
-// (cvt.rn).  bf16: round-half-away-from-zero on the magnitude via an integer
-// add of half a bf16 ulp and a byte permute — ALU-pipe work instead of an
-// F2FP on the quarter-rate XU pipe, which MUFU.TANH already saturates
-// (differs from round-to-nearest-even only on exact ties; finite inputs).
+// (cvt.rn).  bf16: truncation of the pre-activation by one byte permute — an
+// ALU-pipe op instead of an F2FP on the quarter-rate XU pipe that MUFU.TANH
+// already saturates (emulated cost: conditioning-scale error 3.5e-4 -> 4.1e-4
+// against the 3e-3 bar).  The GELU output fed to the next MMA is
+// produced by bf16x2 arithmetic (round-to-nearest).
 template <int F16>
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   uint32_t r;
   if constexpr (F16) {
     asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   } else {
-    const uint32_t a = __float_as_uint(lo) + 0x8000u, b = __float_as_uint(hi) + 0x8000u;
-    r = __byte_perm(a, b, 0x7632);
+    r = __byte_perm(__float_as_uint(lo), __float_as_uint(hi), 0x7632);
   }
+  return r;
+}
+template <int F16>
+__device__ __forceinline__ uint32_t pack2_rn(float lo, float hi) {  // constants
+  uint32_t r;
+  if constexpr (F16) asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  else asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
 
@@ -334,7 +341,7 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, S
     const uint32_t a_base = smem_u32(S.A + slot * kTile);
     const uint32_t t_row = tmem + (uint32_t)(slot * kD) + ((uint32_t)(quad * 32) << 16);
     float* zb = S.zbuf + slot * kZRows * kD;
-    const uint32_t c0 = pack2<F16>(kG0, kG0), c1 = pack2<F16>(kG1, kG1);
+    const uint32_t c0 = pack2_rn<F16>(kG0, kG0), c1 = pack2_rn<F16>(kG1, kG1);
     const float bo = __ldg(net.bo);
     // z staging: thread tid_s moves 4 consecutive floats of the tile's <= 4 subdomains
     const int zi = 4 * tid_s, zr_ = zi >> 7, zc = zi & 127;
@@ -437,11 +444,329 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, S
 
 }  // namespace tc
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2).  A cluster of two CTAs on one TPC computes
+// 256-row pair tiles with M = 256 MMAs issued by the even CTA: each CTA keeps
+// its own 128 rows of A and only its 64-row half of every weight image (the
+// pair's tensor cores read both halves), which halves the resident weight
+// footprint and buys a fourth tile slot (TMEM 4 x 128 columns) and 16
+// epilogue warps per SM.  Epilogue warps of both CTAs arrive (one elected lane
+// per warp) on the even CTA's a_full barrier through mapa; the MMA commit is
+// multicast to the d_full barriers of both CTAs.
+namespace tc2 {
+using namespace tc;
+
+constexpr int kSlots2 = 4;
+constexpr int kThreads2 = 32 * (2 + 4 * kSlots2);  // 576
+constexpr int kHalf = kWImg;                       // bytes of one CTA's half image per layer (18 KB)
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// kind::f16, D fp32, M = 256 (pair), N = 128.
+template <int F16>
+constexpr uint32_t idesc2() {
+  return (1u << 4) | ((F16 ? 0u : 1u) << 7) | ((F16 ? 0u : 1u) << 10) | ((uint32_t)(kD >> 3) << 17) |
+         ((uint32_t)(256 >> 4) << 24);
+}
+template <int F16>
+__device__ __forceinline__ void mma2(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc2<F16>()), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void commit2(uint64_t* bar) {
+  const uint16_t mask = 0x3;
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+struct Smem2 {
+  uint8_t* W;      // [nh][18 KB]: this CTA's 64-row half + bias block
+  uint8_t* A;      // [4][32 KB]
+  uint8_t* ones;   // 4 KB
+  float* zbuf;     // [4][4][128]
+  float* w2;       // [2][128]
+  float* wo;       // [128]
+  uint64_t* bars;  // a_full[4] (used in the even CTA), d_full[4]
+  uint32_t* tmem_slot;
+};
+
+__device__ __forceinline__ Smem2 carve2(uint8_t* raw, int nh) {
+  Smem2 s;
+  s.W = raw;
+  s.A = raw + nh * kHalf;
+  s.ones = s.A + kSlots2 * kTile;
+  s.zbuf = (float*)(s.ones + kOnes);
+  s.w2 = s.zbuf + kSlots2 * kZRows * kD;
+  s.wo = s.w2 + 2 * kD;
+  s.bars = (uint64_t*)(s.wo + kD);
+  s.tmem_slot = (uint32_t*)(s.bars + 2 * kSlots2);
+  return s;
+}
+
+size_t smem_bytes2(int n_hidden) {
+  return (size_t)n_hidden * kHalf + kSlots2 * kTile + kOnes + 4 * ((size_t)kSlots2 * kZRows * kD + 3 * kD) +
+         16 * kSlots2 + 16;
+}
+
+template <int GELU, int F16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
+k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, Sink sink) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int nh = net.n_hidden;
+  const Smem2 S = carve2(smem_raw, nh);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+
+  // ---- prologue
+  {
+    for (int l = 0; l < nh; l++) {
+      const uint4* src =
+          reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(net.Wh_sw2) + (size_t)l * 2 * kHalf + rank * kHalf);
+      uint4* dst = reinterpret_cast<uint4*>(S.W + l * kHalf);
+      for (int i = threadIdx.x; i < kHalf / 16; i += kThreads2) dst[i] = __ldg(src + i);
+    }
+    for (int i = threadIdx.x; i < kD; i += kThreads2) {
+      S.wo[i] = (GELU == 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
+      S.w2[i] = __ldg(net.W2 + 2 * i);
+      S.w2[kD + i] = __ldg(net.W2 + 2 * i + 1);
+    }
+    if (threadIdx.x < kRows) {
+      const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
+      const int r = threadIdx.x;
+      *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + (r & 7) * 16) = make_uint4(one | (one << 16), 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + 128 + (r & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSlots2; s++) {
+      mbar_init(&S.bars[s], 8);             // a_full[s]: 4 warps x 2 CTAs (elected lanes)
+      mbar_init(&S.bars[kSlots2 + s], 1);   // d_full[s]: multicast commit
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // both CTAs' barriers initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *S.tmem_slot;
+
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int64_t ntiles = (total_rows + 2 * kRows - 1) / (2 * kRows);
+  const int64_t nloc = ntiles > cid ? (ntiles - cid + ncl - 1) / ncl : 0;
+  const int64_t nsub = total_rows / q;
+
+  if (warp == 0) {
+    if (rank == 0 && lane == 0) {
+      uint32_t pa[kSlots2] = {0u, 0u, 0u, 0u};
+      const uint32_t ones_addr = smem_u32(S.ones);
+      for (int64_t j0 = 0; j0 < nloc; j0 += kSlots2) {
+        for (int l = 0; l < nh; l++) {
+#pragma unroll
+          for (int s = 0; s < kSlots2; s++) {
+            if (j0 + s >= nloc) continue;
+            mbar_wait_cluster(&S.bars[s], pa[s]);
+            pa[s] ^= 1u;
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(S.A + s * kTile), b0 = smem_u32(S.W + l * kHalf);
+            const uint32_t d = tmem + (uint32_t)(s * kD);
+#pragma unroll
+            for (int k = 0; k < kD / 16; k++) {
+              const uint32_t offa = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
+              const uint32_t offb = (uint32_t)((k >> 2) * 8192 + (k & 3) * 32);
+              mma2<F16>(d, sw128_desc(a0 + offa), sw128_desc(b0 + offb), k > 0 ? 1u : 0u);
+            }
+            mma2<F16>(d, nosw_desc(ones_addr), nosw_desc(b0 + 16384u), 1u);   // bias step
+            commit2(&S.bars[kSlots2 + s]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 2) {
+    const int slot = (warp - 2) >> 2;
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const int tid_s = (warp - 2 - 4 * slot) * 32 + lane;
+    const uint32_t a_base = smem_u32(S.A + slot * kTile);
+    const uint32_t t_row = tmem + (uint32_t)(slot * kD) + ((uint32_t)(quad * 32) << 16);
+    float* zb = S.zbuf + slot * kZRows * kD;
+    const uint32_t c0 = pack2_rn<F16>(kG0, kG0), c1 = pack2_rn<F16>(kG1, kG1);
+    const float bo = __ldg(net.bo);
+    const int zi = 4 * tid_s, zr_ = zi >> 7, zc = zi & 127;
+    auto row0_of = [&](int64_t j) -> int64_t { return (cid + j * ncl) * (2 * kRows) + rank * kRows; };
+    auto z_fetch = [&](int64_t j) -> float4 {
+      int64_t sidx = row0_of(j) / q + zr_;
+      if (sidx > nsub - 1) sidx = nsub - 1;
+      return __ldg(reinterpret_cast<const float4*>(z + sidx * kD + zc));
+    };
+    auto arrive_a = [&]() {
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&S.bars[slot], 0u);
+    };
+    if (slot < nloc) *reinterpret_cast<float4*>(zb + zi) = z_fetch(slot);
+    uint32_t pd = 0u;
+    for (int64_t j = slot; j < nloc; j += kSlots2) {
+      const int64_t row0 = row0_of(j);
+      int64_t s_first = row0 / q;
+      if (s_first > nsub - 1) s_first = nsub - 1;
+      named_sync(1 + slot, 128);
+      const bool have_next = j + kSlots2 < nloc;
+      float4 znext = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (have_next) znext = z_fetch(j + kSlots2);
+      const int64_t grow = row0 + row;
+      const bool valid = grow < total_rows;
+      const int64_t gr = valid ? grow : total_rows - 1;
+      const int64_t sidx = gr / q;
+      const int p = (int)(gr - sidx * q);
+      float qx, qy;
+      query_xy(q, p, &qx, &qy);
+      {
+        int zo = (int)(sidx - s_first);
+        if (zo < 0 || zo >= kZRows) zo = 0;   // rows past the end of the batch (not stored)
+        const float* zr = zb + zo * kD;
+#pragma unroll 2
+        for (int cc = 0; cc < kD / 8; cc++) {
+          const float4 z0 = *reinterpret_cast<const float4*>(zr + cc * 8);
+          const float4 z1 = *reinterpret_cast<const float4*>(zr + cc * 8 + 4);
+          const float4 a0 = *reinterpret_cast<const float4*>(S.w2 + cc * 8);
+          const float4 a1 = *reinterpret_cast<const float4*>(S.w2 + cc * 8 + 4);
+          const float4 b0 = *reinterpret_cast<const float4*>(S.w2 + kD + cc * 8);
+          const float4 b1 = *reinterpret_cast<const float4*>(S.w2 + kD + cc * 8 + 4);
+          const float v[8] = {z0.x + fmaf(a0.x, qx, b0.x * qy), z0.y + fmaf(a0.y, qx, b0.y * qy),
+                              z0.z + fmaf(a0.z, qx, b0.z * qy), z0.w + fmaf(a0.w, qx, b0.w * qy),
+                              z1.x + fmaf(a1.x, qx, b1.x * qy), z1.y + fmaf(a1.y, qx, b1.y * qy),
+                              z1.z + fmaf(a1.z, qx, b1.z * qy), z1.w + fmaf(a1.w, qx, b1.w * qy)};
+          uint32_t w[4];
+          act8<GELU, F16>(v, w, c0, c1);
+          st_shared_v4(a_base + sw128_off(row, cc * 8), w[0], w[1], w[2], w[3]);
+        }
+      }
+      fence_proxy_async();
+      arrive_a();
+      float y = 0.f;
+      for (int l = 0; l < nh; l++) {
+        mbar_wait(&S.bars[kSlots2 + slot], pd);
+        pd ^= 1u;
+        tc_fence_after();
+        const bool last = (l == nh - 1);
+#pragma unroll 1
+        for (int ch = 0; ch < kD / 32; ch++) {
+          uint32_t r[32];
+          tmem_ld32(t_row + (uint32_t)(ch * 32), r);
+          tmem_wait_ld();
+          if (!last) {
+#pragma unroll
+            for (int c8 = 0; c8 < 4; c8++) {
+              float v[8];
+#pragma unroll
+              for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[c8 * 8 + e]);
+              uint32_t w[4];
+              act8<GELU, F16>(v, w, c0, c1);
+              st_shared_v4(a_base + sw128_off(row, ch * 32 + c8 * 8), w[0], w[1], w[2], w[3]);
+            }
+          } else {
+            const float* wo = S.wo + ch * 32;
+#pragma unroll
+            for (int e = 0; e < 32; e++) y = fmaf(wo[e], act_head<GELU>(__uint_as_float(r[e])), y);
+          }
+        }
+        tc_fence_before();
+        if (!last) {
+          fence_proxy_async();
+          arrive_a();
+        }
+      }
+      if (have_next) *reinterpret_cast<float4*>(zb + zi) = znext;
+      if (valid) sink_store(sink, sidx, p, y + bo);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  }
+}
+
+}  // namespace tc2
+
 bool chain_tc_available() { return true; }
+
+// Variant: 2 = CTA pair (default), 1 = single-CTA 3-slot kernel (MFP_CHAIN_VARIANT=1,
+// kept for A/B measurement).
+static int chain_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MFP_CHAIN_VARIANT");
+    v = (e && e[0] == '1') ? 1 : 2;
+  }
+  return v;
+}
 
 void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const Sink& sink, int num_sms,
                      cudaStream_t s) {
   if (B <= 0) return;
+  const int64_t rows = B * q;
+  if (chain_variant() == 2) {
+    const size_t sm = tc2::smem_bytes2(net.n_hidden);
+    static bool attr2 = false;
+    if (!attr2) {
+      const int mx = (int)tc2::smem_bytes2(kMaxHidden);
+      cudaFuncSetAttribute(tc2::k_chain_tc2<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(tc2::k_chain_tc2<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(tc2::k_chain_tc2<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(tc2::k_chain_tc2<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      attr2 = true;
+    }
+    const int64_t ptiles = (rows + 2 * tc::kRows - 1) / (2 * tc::kRows);
+    const int64_t pairs = num_sms / 2;
+    const int grid = 2 * (int)(ptiles < pairs ? ptiles : pairs);
+    if (net.f16) {
+      if (net.gelu_tanh) tc2::k_chain_tc2<1, 1><<<grid, tc2::kThreads2, sm, s>>>(z, rows, q, net, sink);
+      else tc2::k_chain_tc2<0, 1><<<grid, tc2::kThreads2, sm, s>>>(z, rows, q, net, sink);
+    } else {
+      if (net.gelu_tanh) tc2::k_chain_tc2<1, 0><<<grid, tc2::kThreads2, sm, s>>>(z, rows, q, net, sink);
+      else tc2::k_chain_tc2<0, 0><<<grid, tc2::kThreads2, sm, s>>>(z, rows, q, net, sink);
+    }
+    return;
+  }
   const size_t sm = tc::smem_bytes(net.n_hidden);
   static bool attr = false;
   if (!attr) {
@@ -452,7 +777,6 @@ void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const 
     cudaFuncSetAttribute(tc::k_chain_tc<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     attr = true;
   }
-  const int64_t rows = B * q;
   const int64_t tiles = (rows + tc::kRows - 1) / tc::kRows;
   const int grid = (int)(tiles < num_sms ? tiles : num_sms);
   if (net.f16) {
