@@ -157,6 +157,8 @@ typedef struct {
   int64_t lattice_cells;       /* horizontal + vertical line cells held locally      */
   int32_t n_hlines, n_vlines;  /* local line counts (y = RY0 + 16 i, x = RX0 + 16 j)  */
   int32_t hline_len, vline_len;/* RX1-RX0+1, RY1-RY0+1                               */
+  int64_t phase0_interior;     /* phase-0 subdomains touching no halo cell: they run  */
+                               /* while the previous exchange is in flight           */
 } mfp_plan_info;
 
 /* ---- sizing / lifetime ------------------------------------------------------ */

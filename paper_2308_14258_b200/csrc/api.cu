@@ -64,6 +64,9 @@ struct mfp_ctx {
   int R = 1;
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;         // halo exchange (overlaps interior phase 0)
+  cudaEvent_t ev_packed = nullptr, ev_unpacked = nullptr;
+  bool pending = false;                // an exchange is in flight on `side`
   std::vector<RankState> ranks;
   DevNet dn{};
   float* params = nullptr;
@@ -238,42 +241,57 @@ void chain(mfp_ctx* c, const float* z, int64_t B, int q, const Sink& sk) {
   c->launches++;
 }
 
-void run_phase(mfp_ctx* c, RankState& rs, int ph) {
-  const int64_t B = (int64_t)rs.plan.phase_anchor[ph].size();
-  if (B == 0) return;
+// One phase (or the anchor sub-range [b0, b1) of it) of one rank.
+void run_phase(mfp_ctx* c, RankState& rs, int ph, int64_t b0 = 0, int64_t b1 = -1) {
+  if (b1 < 0) b1 = (int64_t)rs.plan.phase_anchor[ph].size();
+  const int64_t B = b1 - b0;
+  if (B <= 0) return;
+  const uint32_t* anchors = rs.anchors[ph] + b0;
   if (c->cfg.subsolver == MFP_EXACT_LAPLACE) {
     SpanGuard g(c, kKindExact, B);
-    launch_exact_phase(rs.lat, rs.plan.lat, rs.anchors[ph], B, c->dn.HcT, c->stream);
+    launch_exact_phase(rs.lat, rs.plan.lat, anchors, B, c->dn.HcT, c->stream);
     c->launches++;
   } else {
     {
       SpanGuard g(c, kKindGather, B);
-      launch_gather_embed(rs.lat, rs.plan.lat, rs.anchors[ph], nullptr, B, c->dn, rs.z, c->stream);
+      launch_gather_embed(rs.lat, rs.plan.lat, anchors, nullptr, B, c->dn, rs.z, c->stream);
       c->launches++;
     }
-    chain(c, rs.z, B, kQC, lattice_sink(rs, ph));
+    Sink sk = lattice_sink(rs, ph);
+    sk.anchors = anchors;
+    chain(c, rs.z, B, kQC, sk);
   }
 }
 
-// communicate_new_boundaries: pack -> exchange -> unpack, once per iteration
-mfp_status exchange(mfp_ctx* c) {
+// communicate_new_boundaries, once per iteration, split in two
+// halves so the exchange overlaps the next iteration's interior phase-0
+// subdomains (north_star): exchange_begin packs on the main stream (a snapshot
+// of the owned cells), then the transport — grouped ncclSend/ncclRecv, or
+// device copies for MFP_ALL_RANKS — and the unpack run on the side stream;
+// exchange_wait makes the main stream wait for the unpack.
+mfp_status exchange_begin(mfp_ctx* c) {
   if (c->R == 1) return MFP_OK;
-  SpanGuard g(c, kKindHalo, 0);
   for (auto& rs : c->ranks) {
     launch_pack(rs.lat, rs.send_idx, rs.nsend, rs.sendbuf, c->stream);
     c->launches++;
+  }
+  CK(cudaEventRecord(c->ev_packed, c->stream));
+  CK(cudaStreamWaitEvent(c->side, c->ev_packed, 0));
+  cudaEvent_t h0 = nullptr;
+  if (c->profiling) {  // transport + unpack span, timed on the side stream
+    h0 = ev(c);
+    cudaEventRecord(h0, c->side);
   }
   if (c->rank == MFP_ALL_RANKS) {
     for (auto& dst : c->ranks)
       for (size_t i = 0; i < dst.plan.peers.size(); i++) {
         const RankState& src = c->ranks[dst.plan.peers[i].rank];
-        // find dst in src's peer list
-        size_t j = 0;
+        size_t j = 0;  // dst's index in src's peer list
         while (j < src.plan.peers.size() && src.plan.peers[j].rank != dst.plan.rank) j++;
         const int64_t n = (int64_t)dst.plan.peers[i].recv_idx.size();
         if (n == 0) continue;
         CK(cudaMemcpyAsync(dst.recvbuf + dst.recv_off[i], src.sendbuf + src.send_off[j],
-                           n * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+                           n * sizeof(float), cudaMemcpyDeviceToDevice, c->side));
       }
   } else {
     RankState& rs = c->ranks[0];
@@ -281,17 +299,47 @@ mfp_status exchange(mfp_ctx* c) {
     for (size_t i = 0; i < rs.plan.peers.size(); i++) {
       const auto& pp = rs.plan.peers[i];
       if (!pp.send_idx.empty())
-        NK(ncclSend(rs.sendbuf + rs.send_off[i], pp.send_idx.size(), ncclFloat32, pp.rank, c->comm, c->stream));
+        NK(ncclSend(rs.sendbuf + rs.send_off[i], pp.send_idx.size(), ncclFloat32, pp.rank, c->comm, c->side));
       if (!pp.recv_idx.empty())
-        NK(ncclRecv(rs.recvbuf + rs.recv_off[i], pp.recv_idx.size(), ncclFloat32, pp.rank, c->comm, c->stream));
+        NK(ncclRecv(rs.recvbuf + rs.recv_off[i], pp.recv_idx.size(), ncclFloat32, pp.rank, c->comm, c->side));
     }
     NK(ncclGroupEnd());
   }
   for (auto& rs : c->ranks) {
-    launch_unpack(rs.lat, rs.recv_idx, rs.nrecv, rs.recvbuf, c->stream);
+    launch_unpack(rs.lat, rs.recv_idx, rs.nrecv, rs.recvbuf, c->side);
     c->launches++;
   }
+  CK(cudaEventRecord(c->ev_unpacked, c->side));
+  if (c->profiling) {
+    cudaEvent_t h1 = ev(c);
+    cudaEventRecord(h1, c->side);
+    c->spans.push_back({h0, h1, kKindHalo, 0});
+  }
+  c->pending = true;
   return MFP_OK;
+}
+
+mfp_status exchange_wait(mfp_ctx* c) {
+  if (!c->pending) return MFP_OK;
+  CK(cudaStreamWaitEvent(c->stream, c->ev_unpacked, 0));
+  c->pending = false;
+  return MFP_OK;
+}
+
+// One iteration: phase 0 (interior subdomains first while a pending exchange
+// is in flight, then the halo-touching ones), phases 1-3, then the exchange.
+mfp_status iterate(mfp_ctx* c) {
+  mfp_status st;
+  if (c->pending) {
+    for (auto& rs : c->ranks) run_phase(c, rs, 0, 0, rs.plan.n0_interior);
+    if ((st = exchange_wait(c))) return st;
+    for (auto& rs : c->ranks) run_phase(c, rs, 0, rs.plan.n0_interior, -1);
+  } else {
+    for (auto& rs : c->ranks) run_phase(c, rs, 0);
+  }
+  for (int ph = 1; ph < 4; ph++)
+    for (auto& rs : c->ranks) run_phase(c, rs, ph);
+  return exchange_begin(c);
 }
 
 // delta_k (reading G5) -> host, max over ranks; returns nonfinite flag
@@ -394,14 +442,17 @@ mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, floa
   float delta = -1.f;
   for (it = 1; it <= t; it++) {
     const bool check = (tol > 0.f && it % ce == 0) || it == t;
+    // snapshot for delta (only owned cells are compared; halo cells being
+    // unpacked concurrently on the side stream are never read back)
     if (check)
       for (auto& rs : c->ranks)
         CK(cudaMemcpyAsync(rs.snap, rs.lat, rs.plan.lat.cells * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
-    for (int ph = 0; ph < 4; ph++)
-      for (auto& rs : c->ranks) run_phase(c, rs, ph);
-    mfp_status st = exchange(c);
+    mfp_status st = iterate(c);
     if (st) return st;
     if (check) {
+      // complete the exchange first: NCCL ops on one communicator must not be
+      // reordered across streams (allreduce on `stream`, send/recv on `side`)
+      if ((st = exchange_wait(c))) return st;
       bool bad = false;
       st = reduce_delta(c, &delta, &bad);
       if (st) return st;
@@ -410,6 +461,10 @@ mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, floa
     }
   }
   if (it > t) it = t;
+  {
+    mfp_status st = exchange_wait(c);
+    if (st) return st;
+  }
   CK(cudaEventRecord(e1, c->stream));
   if (do_final) {
     mfp_status st = final_phase(c, u_dev);
@@ -523,6 +578,9 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
     return fail(c, MFP_ERR_WORKSPACE, "workspace too small or not 256-byte aligned");
   carve(c, workspace, &need);
   CK(cudaMallocHost(&c->hdelta, 4 * sizeof(unsigned int)));
+  CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_packed, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_unpacked, cudaEventDisableTiming));
   cudaStream_t s = c->stream;
   // upload plan tables
   for (auto& rs : c->ranks) {
@@ -570,6 +628,12 @@ void mfp_destroy(mfp_ctx* c) {
   if (!c) return;
   for (auto e : c->evpool) cudaEventDestroy(e);
   if (c->hdelta) cudaFreeHost(c->hdelta);
+  if (c->side) {
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+  }
+  if (c->ev_packed) cudaEventDestroy(c->ev_packed);
+  if (c->ev_unpacked) cudaEventDestroy(c->ev_unpacked);
   delete c;
 }
 
@@ -686,9 +750,11 @@ mfp_status mfp_profile_iterations(mfp_ctx* c, int32_t iters, mfp_profile* o) {
   cudaEvent_t a = ev(c), b = ev(c);
   CK(cudaEventRecord(a, c->stream));
   for (int it = 0; it < iters; it++) {
-    for (int ph = 0; ph < 4; ph++)
-      for (auto& rs : c->ranks) run_phase(c, rs, ph);
-    mfp_status st = exchange(c);
+    mfp_status st = iterate(c);
+    if (st) { c->profiling = false; return st; }
+  }
+  {
+    mfp_status st = exchange_wait(c);
     if (st) { c->profiling = false; return st; }
   }
   CK(cudaEventRecord(b, c->stream));

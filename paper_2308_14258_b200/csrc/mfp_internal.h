@@ -51,6 +51,10 @@ struct RankPlan {
   int bw, bh;                   // owned block extent in points
   LatticeGeom lat;
   std::vector<uint32_t> phase_anchor[4];  // packed (a | b << 16), local line indices
+  // phase_anchor[0] is ordered interior-first: its first n0_interior subdomains
+  // neither read nor write a halo (received) cell, so they may run while the
+  // previous iteration's exchange is still in flight on the side stream.
+  int64_t n0_interior = 0;
   std::vector<int32_t> phase_ax[4], phase_ay[4];   // global (plan API)
   std::vector<uint32_t> final_anchor;     // packed block-local (bx | by << 16) + lattice (a|b<<16)
   std::vector<uint32_t> final_lat_anchor;

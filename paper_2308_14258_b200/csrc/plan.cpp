@@ -163,6 +163,34 @@ static void build_rank(const mfp_config* c, int r, RankPlan* p) {
       }
       if (!pp.send_idx.empty() || !pp.recv_idx.empty()) p->peers.push_back(std::move(pp));
     }
+  // Overlap split of phase 0 (north_star: halo exchange overlapped with interior
+  // subdomain batches): interior = no perimeter cell and no centre-line cell is
+  // a received halo cell.  Within a class every order is equivalent.
+  {
+    std::vector<uint8_t> halo((size_t)L.cells, 0);
+    for (auto& pp : p->peers)
+      for (int32_t c : pp.recv_idx) halo[(size_t)c] = 1;
+    std::vector<uint32_t> inner, outer;
+    for (uint32_t pk : p->phase_anchor[0]) {
+      const int a = (int)(pk & 0xffffu), b = (int)(pk >> 16);
+      const int lx = kH * a, ly = kH * b;
+      bool touches = false;
+      for (int t = 0; t < kM && !touches; t++) {
+        // perimeter (G1): bottom, right, top, left edges
+        touches |= halo[(size_t)b * L.strideH + lx + t] || halo[(size_t)(b + 2) * L.strideH + lx + kM - t] ||
+                   halo[(size_t)(L.offV + (int64_t)(a + 2) * L.strideV + ly + t)] ||
+                   halo[(size_t)(L.offV + (int64_t)a * L.strideV + ly + kM - t)];
+        // centre lines (G3)
+        if (t >= 1)
+          touches |= halo[(size_t)(L.offV + (int64_t)(a + 1) * L.strideV + ly + t)] ||
+                     halo[(size_t)(b + 1) * L.strideH + lx + t];
+      }
+      (touches ? outer : inner).push_back(pk);
+    }
+    p->n0_interior = (int64_t)inner.size();
+    p->phase_anchor[0] = inner;
+    p->phase_anchor[0].insert(p->phase_anchor[0].end(), outer.begin(), outer.end());
+  }
 }
 
 mfp_status build_plan(const mfp_config* cfg, int rank, GlobalPlan* out, std::string* err) {
@@ -209,6 +237,7 @@ extern "C" mfp_status mfp_plan_query(const mfp_config* cfg, int32_t rank, mfp_pl
   o->lattice_cells = (int64_t)p.lat.nH * p.lat.lenH + (int64_t)p.lat.nV * p.lat.lenV;
   o->n_hlines = p.lat.nH; o->n_vlines = p.lat.nV;
   o->hline_len = p.lat.lenH; o->vline_len = p.lat.lenV;
+  o->phase0_interior = p.n0_interior;
   return MFP_OK;
 }
 

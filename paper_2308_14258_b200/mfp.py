@@ -76,7 +76,8 @@ class mfp_plan_info(ctypes.Structure):
                 ("n_peers", ctypes.c_int32), ("peers", ctypes.c_int32 * 8),
                 ("send_count", ctypes.c_int64 * 8), ("recv_count", ctypes.c_int64 * 8),
                 ("lattice_cells", ctypes.c_int64), ("n_hlines", ctypes.c_int32), ("n_vlines", ctypes.c_int32),
-                ("hline_len", ctypes.c_int32), ("vline_len", ctypes.c_int32)]
+                ("hline_len", ctypes.c_int32), ("vline_len", ctypes.c_int32),
+                ("phase0_interior", ctypes.c_int64)]
 
 
 _P = ctypes.POINTER

@@ -154,6 +154,28 @@ def test_halo_lists(grid, kx, ky):
                     assert (0, x, y) in covered
 
 
+@pytest.mark.parametrize("grid,kx,ky", GRIDS)
+def test_phase0_overlap_split(grid, kx, ky):
+    """North_star overlap: the phase-0 subdomains run before the previous
+    exchange completes are exactly those that neither read (perimeter) nor
+    write (centre lines) a received halo cell."""
+    nx, ny = kx * M, ky * M
+    cfg = mfp.make_config(nx, ny, grid)
+    for r in range(grid[0] * grid[1]):
+        info = mfp.mfp_plan_query(cfg, r)
+        halo = set()
+        for i in range(info.n_peers):
+            for kind, x, y in mfp.mfp_plan_halo(cfg, r, i, 1):
+                halo.add((int(x), int(y)))
+        n = 0
+        for ax, ay in mfp.mfp_plan_anchors(cfg, r, 0):
+            cells = {tuple(p) for p in oracle.perimeter(ax, ay)} | {tuple(p) for p in oracle.writeset(ax, ay)[0]}
+            n += not (cells & halo)
+        assert info.phase0_interior == n
+        if grid == (1, 1):
+            assert n == info.phase_count[0]
+
+
 def test_message_counts_stencil():
     """interior rank of a 3x3 grid talks to 8 neighbours, corner to 3."""
     cfg = mfp.make_config(6 * M, 6 * M, (3, 3))
