@@ -67,6 +67,9 @@ struct mfp_ctx {
   cudaStream_t side = nullptr;         // halo exchange (overlaps interior phase 0)
   cudaEvent_t ev_packed = nullptr, ev_unpacked = nullptr;
   bool pending = false;                // an exchange is in flight on `side`
+  bool use_graphs = false;             // replay blocks of c iterations as CUDA graphs
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // [0] plain block, [1] block ending in a check
+  int glaunches[2] = {0, 0};
   std::vector<RankState> ranks;
   DevNet dn{};
   float* params = nullptr;
@@ -343,7 +346,8 @@ mfp_status iterate(mfp_ctx* c) {
 }
 
 // delta_k (reading G5) -> host, max over ranks; returns nonfinite flag
-mfp_status reduce_delta(mfp_ctx* c, float* delta, bool* nonfinite) {
+// Enqueue the delta reduction (no host sync: capturable into a graph).
+mfp_status enqueue_delta(mfp_ctx* c) {
   CK(cudaMemsetAsync(c->delta, 0, 2 * sizeof(unsigned int), c->stream));
   {
     SpanGuard g(c, kKindDelta, 0);
@@ -354,12 +358,58 @@ mfp_status reduce_delta(mfp_ctx* c, float* delta, bool* nonfinite) {
   }
   if (c->comm) NK(ncclAllReduce(c->delta, c->delta, 2, ncclUint32, ncclMax, c->comm, c->stream));
   CK(cudaMemcpyAsync(c->hdelta, c->delta, 2 * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
+  return MFP_OK;
+}
+
+// Host side of the check: wait for the pinned copy and decode it.
+mfp_status read_delta(mfp_ctx* c, float* delta, bool* nonfinite) {
   CK(cudaStreamSynchronize(c->stream));
   uint32_t bits = c->hdelta[0];
   float d;
   memcpy(&d, &bits, 4);
   *delta = d;
   *nonfinite = c->hdelta[1] != 0;
+  return MFP_OK;
+}
+
+mfp_status reduce_delta(mfp_ctx* c, float* delta, bool* nonfinite) {
+  mfp_status st = enqueue_delta(c);
+  if (st) return st;
+  return read_delta(c, delta, nonfinite);
+}
+
+// Capture (once) and replay a block of c iterations as a CUDA graph.  kind 1
+// ends with the snapshot-delta-allreduce of a check iteration (the pinned D2H
+// copy of delta is a graph node; the host reads it after the launch).
+mfp_status run_block(mfp_ctx* c, int kind) {
+  const int ce = c->cfg.check_every;
+  if (!c->gexec[kind]) {
+    const int l0 = c->launches;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    mfp_status st = MFP_OK;
+    for (int i = 0; i < ce && st == MFP_OK; i++) {
+      if (kind == 1 && i == ce - 1)
+        for (auto& rs : c->ranks)
+          cudaMemcpyAsync(rs.snap, rs.lat, rs.plan.lat.cells * sizeof(float), cudaMemcpyDeviceToDevice, c->stream);
+      st = iterate(c);
+    }
+    if (st == MFP_OK) st = exchange_wait(c);
+    if (st == MFP_OK && kind == 1) st = enqueue_delta(c);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (st != MFP_OK) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    if (e != cudaSuccess) return fail(c, MFP_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    const cudaError_t ei = cudaGraphInstantiate(&c->gexec[kind], g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) return fail(c, MFP_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
+    c->glaunches[kind] = c->launches - l0;
+    c->launches = l0;
+  }
+  CK(cudaGraphLaunch(c->gexec[kind], c->stream));
+  c->launches += c->glaunches[kind];
   return MFP_OK;
 }
 
@@ -437,10 +487,28 @@ mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, floa
     }
   }
   const int ce = c->cfg.check_every;
-  int it = 0;
+  int it = 0;  // iterations completed
   bool converged = false;
   float delta = -1.f;
-  for (it = 1; it <= t; it++) {
+  while (it < t) {
+    // A whole block of c iterations (starting on a block boundary, no exchange
+    // in flight) replays one captured CUDA graph: c x (4 phases + exchange),
+    // plus the snapshot / delta / allreduce of the check iteration.
+    if (c->use_graphs && it % ce == 0 && t - it >= ce && !c->pending) {
+      const int end = it + ce;
+      const bool check = (tol > 0.f) || end == t;
+      mfp_status st = run_block(c, check ? 1 : 0);
+      if (st) return st;
+      it = end;
+      if (check) {
+        bool bad = false;
+        if ((st = read_delta(c, &delta, &bad))) return st;
+        if (bad) return fail(c, MFP_ERR_NONFINITE, "non-finite prediction (S:345)");
+        if (tol > 0.f && delta <= tol) { converged = true; break; }
+      }
+      continue;
+    }
+    it++;
     const bool check = (tol > 0.f && it % ce == 0) || it == t;
     // snapshot for delta (only owned cells are compared; halo cells being
     // unpacked concurrently on the side stream are never read back)
@@ -460,7 +528,6 @@ mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, floa
       if (tol > 0.f && it % ce == 0 && delta <= tol) { converged = true; break; }
     }
   }
-  if (it > t) it = t;
   {
     mfp_status st = exchange_wait(c);
     if (st) return st;
@@ -579,6 +646,10 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
   carve(c, workspace, &need);
   CK(cudaMallocHost(&c->hdelta, 4 * sizeof(unsigned int)));
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  // graphs need a capturable (non-legacy) stream; MFP_NO_GRAPHS=1 disables them
+  c->use_graphs = c->stream != nullptr && !(getenv("MFP_NO_GRAPHS") && getenv("MFP_NO_GRAPHS")[0] == '1');
+  sdnet_kernel_attributes();
+  tc_kernel_attributes();
   CK(cudaEventCreateWithFlags(&c->ev_packed, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_unpacked, cudaEventDisableTiming));
   cudaStream_t s = c->stream;
@@ -632,6 +703,8 @@ void mfp_destroy(mfp_ctx* c) {
     cudaStreamSynchronize(c->side);
     cudaStreamDestroy(c->side);
   }
+  for (auto& g : c->gexec)
+    if (g) cudaGraphExecDestroy(g);
   if (c->ev_packed) cudaEventDestroy(c->ev_packed);
   if (c->ev_unpacked) cudaEventDestroy(c->ev_unpacked);
   delete c;

@@ -163,12 +163,6 @@ k_gather_embed(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __r
 void launch_gather_embed(const float* lat, const LatticeGeom& L, const uint32_t* anchors,
                          const float* gb, int64_t B, const DevNet& net, float* z, cudaStream_t s) {
   if (B <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gather_embed<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmbSmem);
-    cudaFuncSetAttribute(k_gather_embed<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmbSmem);
-    attr = true;
-  }
   int64_t blocks = (B + kEmbSub - 1) / kEmbSub;
   if (blocks > 2 * 148) blocks = 2 * 148;   // two resident blocks per SM
   if (net.gelu_tanh)
@@ -273,17 +267,19 @@ void launch_chain_fp32(const float* z, int64_t B, int q, const DevNet& net, cons
                        cudaStream_t s) {
   if (B <= 0) return;
   const size_t sm = simt_smem(net.n_hidden);
-  static size_t attr = 0;
-  if (attr < sm) {
-    cudaFuncSetAttribute(k_chain_fp32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = sm;
-  }
   const int64_t rows = B * q;
   int64_t tiles = (rows + kSimtRows - 1) / kSimtRows;
   int blocks = (int)(tiles < 148 ? tiles : 148);
   const float* QT = q == kQC ? net.QTc : net.QTf;
   const int qpad = q == kQC ? 64 : kQF;
   k_chain_fp32<<<blocks, 256, sm, s>>>(z, rows, q, qpad, QT, net, sink);
+}
+
+// Opt-in shared-memory sizes, set once from mfp_init (never inside a graph capture).
+void sdnet_kernel_attributes() {
+  cudaFuncSetAttribute(k_gather_embed<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmbSmem);
+  cudaFuncSetAttribute(k_gather_embed<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmbSmem);
+  cudaFuncSetAttribute(k_chain_fp32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)simt_smem(kMaxHidden));
 }
 
 }  // namespace mfp

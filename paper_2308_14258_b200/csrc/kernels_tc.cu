@@ -740,21 +740,26 @@ static int chain_variant() {
   return v;
 }
 
+// Opt-in shared-memory sizes, set once from mfp_init (never inside a graph capture).
+void tc_kernel_attributes() {
+  const int mx2 = (int)tc2::smem_bytes2(kMaxHidden);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  const int mx = (int)tc::smem_bytes(kMaxHidden);
+  cudaFuncSetAttribute(tc::k_chain_tc<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(tc::k_chain_tc<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(tc::k_chain_tc<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(tc::k_chain_tc<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+}
+
 void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const Sink& sink, int num_sms,
                      cudaStream_t s) {
   if (B <= 0) return;
   const int64_t rows = B * q;
   if (chain_variant() == 2) {
     const size_t sm = tc2::smem_bytes2(net.n_hidden);
-    static bool attr2 = false;
-    if (!attr2) {
-      const int mx = (int)tc2::smem_bytes2(kMaxHidden);
-      cudaFuncSetAttribute(tc2::k_chain_tc2<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      cudaFuncSetAttribute(tc2::k_chain_tc2<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      cudaFuncSetAttribute(tc2::k_chain_tc2<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      cudaFuncSetAttribute(tc2::k_chain_tc2<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      attr2 = true;
-    }
     const int64_t ptiles = (rows + 2 * tc::kRows - 1) / (2 * tc::kRows);
     const int64_t pairs = num_sms / 2;
     const int grid = 2 * (int)(ptiles < pairs ? ptiles : pairs);
@@ -768,15 +773,6 @@ void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const 
     return;
   }
   const size_t sm = tc::smem_bytes(net.n_hidden);
-  static bool attr = false;
-  if (!attr) {
-    const int mx = (int)tc::smem_bytes(kMaxHidden);
-    cudaFuncSetAttribute(tc::k_chain_tc<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(tc::k_chain_tc<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(tc::k_chain_tc<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(tc::k_chain_tc<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    attr = true;
-  }
   const int64_t tiles = (rows + tc::kRows - 1) / tc::kRows;
   const int grid = (int)(tiles < num_sms ? tiles : num_sms);
   if (net.f16) {

@@ -152,6 +152,8 @@ struct PrepArgs {
   uint16_t* Wsw2;          // [n_hidden][kWImg] CTA-pair half images
 };
 void launch_prep(const PrepArgs& a, cudaStream_t s);
+void sdnet_kernel_attributes();
+void tc_kernel_attributes();
 void launch_harmonic(int q, float* HT, cudaStream_t s);
 
 }  // namespace mfp

@@ -279,8 +279,18 @@ class Mfp:
         self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device="cuda")
         off = (-self.workspace.data_ptr()) % 256
         self.ws = self.workspace[off: off + nbytes]
-        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        # a dedicated (capturable) stream by default: the library replays blocks
+        # of iterations as CUDA graphs, which the legacy default stream forbids
+        self.stream = stream if stream is not None else torch.cuda.Stream()
         self.ctx = mfp_init(cfg, self.net, params, rank, nccl_comm, self.ws, self.stream.cuda_stream)
+
+    def _enter(self):
+        import torch
+        self.stream.wait_stream(torch.cuda.current_stream())
+
+    def _leave(self):
+        import torch
+        torch.cuda.current_stream().wait_stream(self.stream)
 
     @property
     def ranks(self):
@@ -294,7 +304,10 @@ class Mfp:
         return u, rep
 
     def solve_device(self, g_dev, max_iters, tol, u_dev):
-        return mfp_solve_device(self.ctx, g_dev, max_iters, tol, u_dev)
+        self._enter()
+        rep = mfp_solve_device(self.ctx, g_dev, max_iters, tol, u_dev)
+        self._leave()
+        return rep
 
     def sdnet_batch(self, gb_dev, query_set=QUERY_CENTRE, out=None):
         import torch
@@ -303,7 +316,9 @@ class Mfp:
         B = gb_dev.shape[0]
         if out is None:
             out = torch.empty((B, q), dtype=torch.float32, device=gb_dev.device)
+        self._enter()
         mfp_sdnet_batch(self.ctx, gb_dev, B, query_set, out, self.stream.cuda_stream)
+        self._leave()
         return out
 
     def lines(self, rank: int | None = None) -> Lattice:

@@ -88,6 +88,32 @@ def test_exact_distributed_parity(lib, grid, kx, ky, t):
         assert crossings_consistent(m.lines(r))
 
 
+def test_exact_distributed_large(lib):
+    """C3 (2049^2) on the 2x4 grid the 8-GPU bench uses: exchange overlap,
+    D1 compute sets and final assembly at size, vs the oracle's emulation."""
+    nx = ny = 2048
+    grid = (2, 4)
+    g = gp_boundary(nx, ny, 1)
+    m, _ = make(lib, nx, ny, grid)
+    u, rep = m.solve(g, 3, 0.0)
+    ref = oracle.mfp_run(oracle.MfpConfig(nx, ny, Py=2, Px=4, subsolver="exact"), g.astype(np.float64), 3)
+    assert rel_err(gpu_lines(lib, m, nx, ny, grid), ref.lines, line_mask(nx, ny)) <= FP32_TOL
+    assert rel_err(u, ref.u) <= FP32_TOL
+
+
+@pytest.mark.parametrize("precision", [1, 2])
+def test_sdnet_tensorcore_distributed_2x4(lib, precision):
+    nx = ny = 1024
+    grid = (2, 4)
+    g = gp_boundary(nx, ny, 2)
+    m, w = make(lib, nx, ny, grid, subsolver="sdnet", precision=precision, gelu=1)
+    u, rep = m.solve(g, 3, 0.0)
+    ref = oracle.mfp_run(oracle.MfpConfig(nx, ny, Py=2, Px=4), g.astype(np.float64), 3,
+                         params=w.astype(np.float64))
+    assert rel_err(gpu_lines(lib, m, nx, ny, grid), ref.lines, line_mask(nx, ny)) <= BF16_TOL
+    assert rel_err(u, ref.u) <= BF16_TOL
+
+
 def test_exact_converges_to_discrete_solution(lib):
     """C2 to convergence against the scipy DST-I global discrete solution."""
     from tests._refsolve import dst_laplace
