@@ -169,6 +169,7 @@ void carve(mfp_ctx* c, void* base, size_t* total) {
   dn.Qf = cv.take<float>((size_t)kQF * kD);
   dn.Wh_sw = cv.take<uint16_t>((size_t)nh * kWImg);
   dn.Wh_sw2 = cv.take<uint16_t>((size_t)nh * kWImg);
+  dn.W1img = cv.take<uint16_t>((size_t)2 * kD * kNB);
   dn.HcT = cv.take<float>((size_t)kNB * 64);
   dn.HfT = cv.take<float>((size_t)kNB * kQF);
   c->gstage = cv.take<float>((size_t)2 * (c->cfg.nx + c->cfg.ny));
@@ -237,6 +238,14 @@ struct SpanGuard {
   }
 };
 
+// N2 + N3: gather + embedding z = W1 e + b1; the tensor-core precisions use the
+// tcgen05 split-bf16 embed (kernels_embed_tc.cu), fp32 the SIMT one.
+void embed(mfp_ctx* c, const float* lat, const LatticeGeom& L, const uint32_t* anchors, const float* gb,
+           int64_t B, float* z) {
+  if (c->cfg.precision != MFP_FP32 && embed_tc_enabled()) launch_embed_tc(lat, L, anchors, gb, B, c->dn, z, c->stream);
+  else launch_gather_embed(lat, L, anchors, gb, B, c->dn, z, c->stream);
+}
+
 void chain(mfp_ctx* c, const float* z, int64_t B, int q, const Sink& sk) {
   SpanGuard g(c, kKindChain, B * q);
   if (c->cfg.precision != MFP_FP32) launch_chain_tc(z, B, q, c->dn, sk, c->num_sms, c->stream);
@@ -257,7 +266,7 @@ void run_phase(mfp_ctx* c, RankState& rs, int ph, int64_t b0 = 0, int64_t b1 = -
   } else {
     {
       SpanGuard g(c, kKindGather, B);
-      launch_gather_embed(rs.lat, rs.plan.lat, anchors, nullptr, B, c->dn, rs.z, c->stream);
+      embed(c, rs.lat, rs.plan.lat, anchors, nullptr, B, rs.z);
       c->launches++;
     }
     Sink sk = lattice_sink(rs, ph);
@@ -434,7 +443,7 @@ mfp_status final_phase(mfp_ctx* c, float* u) {
     } else {
       for (int64_t s0 = 0; s0 < B; s0 += rs.zcap) {
         const int64_t nb = std::min(rs.zcap, B - s0);
-        launch_gather_embed(rs.lat, p.lat, rs.final_lat_anchor + s0, nullptr, nb, c->dn, rs.z, c->stream);
+        embed(c, rs.lat, p.lat, rs.final_lat_anchor + s0, nullptr, nb, rs.z);
         Sink sk2 = sk;
         sk2.anchors = rs.final_anchor + s0;
         c->launches++;
@@ -650,6 +659,7 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
   c->use_graphs = c->stream != nullptr && !(getenv("MFP_NO_GRAPHS") && getenv("MFP_NO_GRAPHS")[0] == '1');
   sdnet_kernel_attributes();
   tc_kernel_attributes();
+  embed_tc_kernel_attributes();
   CK(cudaEventCreateWithFlags(&c->ev_packed, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_unpacked, cudaEventDisableTiming));
   cudaStream_t s = c->stream;
@@ -685,6 +695,7 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
     a.QTc = (float*)c->dn.QTc; a.QTf = (float*)c->dn.QTf; a.Qc = (float*)c->dn.Qc; a.Qf = (float*)c->dn.Qf;
     a.Wsw = (uint16_t*)c->dn.Wh_sw;
     a.Wsw2 = (uint16_t*)c->dn.Wh_sw2;
+    a.W1img = (uint16_t*)c->dn.W1img;
     launch_prep(a, s);
   } else {
     launch_harmonic(kQC, (float*)c->dn.HcT, s);
@@ -764,7 +775,7 @@ mfp_status mfp_sdnet_batch(mfp_ctx* c, const float* gb, int64_t B, int32_t query
     } else {
       {
         SpanGuard g(c, kKindGather, nb);
-        launch_gather_embed(nullptr, rs.plan.lat, nullptr, gb + s0 * kNB, nb, c->dn, rs.z, c->stream);
+        embed(c, nullptr, rs.plan.lat, nullptr, gb + s0 * kNB, nb, rs.z);
       }
       chain(c, rs.z, nb, q, sk);
     }

@@ -80,6 +80,66 @@ __device__ __forceinline__ void query_xy(int q, int p, float* x, float* y) {
   }
 }
 
+// ---- boundary embedding helpers (reading G7) -----------------------
+// Window [i0-2, i0+5] of a circular length-128 signal held 4-per-lane (lane l
+// owns positions 4l..4l+3): two values from each neighbouring lane.
+__device__ __forceinline__ void circ_window(const float (&v)[4], int lane, float (&w)[8]) {
+  const int left = (lane + 31) & 31, right = (lane + 1) & 31;
+  w[0] = __shfl_sync(0xffffffffu, v[2], left);
+  w[1] = __shfl_sync(0xffffffffu, v[3], left);
+  w[2] = v[0]; w[3] = v[1]; w[4] = v[2]; w[5] = v[3];
+  w[6] = __shfl_sync(0xffffffffu, v[0], right);
+  w[7] = __shfl_sync(0xffffffffu, v[1], right);
+}
+
+template <int GELU>
+__device__ __forceinline__ float emb_act(float x) {
+  if constexpr (GELU == 1) return gelu_tanh(x);
+  else return gelu_erf(x);
+}
+
+// conv1 (1 -> 8, k = 5, circular) + GELU, conv2 (8 -> 1) + GELU on the 4
+// positions this lane owns; cw = {c1w[40], c1b[8], c2w[40], c2b[1]} (smem).
+template <int GELU>
+__device__ __forceinline__ void conv_stack(const float (&g4)[4], int lane, const float* cw, float (&e)[4]) {
+  float win[8];
+  circ_window(g4, lane, win);
+  float acc2[4] = {cw[88], cw[88], cw[88], cw[88]};
+#pragma unroll
+  for (int o = 0; o < kC1; o++) {
+    float c1v[4];
+#pragma unroll
+    for (int p = 0; p < 4; p++) {
+      float v = cw[40 + o];
+#pragma unroll
+      for (int t = 0; t < kK; t++) v = fmaf(cw[o * kK + t], win[p + t], v);
+      c1v[p] = emb_act<GELU>(v);
+    }
+    float w2[8];
+    circ_window(c1v, lane, w2);
+#pragma unroll
+    for (int p = 0; p < 4; p++)
+#pragma unroll
+      for (int t = 0; t < kK; t++) acc2[p] = fmaf(cw[48 + o * kK + t], w2[p + t], acc2[p]);
+  }
+#pragma unroll
+  for (int p = 0; p < 4; p++) e[p] = emb_act<GELU>(acc2[p]);
+}
+
+// Gather the 4 perimeter values (G1 order) lane `lane` owns: positions 4l..4l+3
+// of edge l/8 — one float4 for the two forward edges, 4 scalars for the
+// reversed ones (top R->L, left T->B).
+__device__ __forceinline__ float4 gather4(const float* lat, const LatticeGeom& L, uint32_t packed, int lane) {
+  int a, b;
+  unpack_anchor(packed, a, b);
+  const int lx = kH * a, ly = kH * b, edge = lane >> 3, t0 = 4 * (lane & 7);
+  if (edge == 0) return *reinterpret_cast<const float4*>(lat + (int64_t)b * L.strideH + lx + t0);
+  if (edge == 1) return *reinterpret_cast<const float4*>(lat + L.offV + (int64_t)(a + 2) * L.strideV + ly + t0);
+  const float* r = edge == 2 ? lat + (int64_t)(b + 2) * L.strideH + lx + kM - t0
+                             : lat + L.offV + (int64_t)a * L.strideV + ly + kM - t0;
+  return make_float4(r[0], r[-1], r[-2], r[-3]);
+}
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

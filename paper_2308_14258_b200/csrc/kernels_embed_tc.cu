@@ -1,0 +1,175 @@
+// kernels_embed_tc.cu — boundary gather + embedding (N2 + N3) for the
+// tensor-core paths (precision bf16 / fp16).
+//
+// PAPER.md P:239 (1-D convolutions over g give the boundary embedding) and
+// Eq. 5 P:270 (z = g W1^T is computed once per boundary and broadcast over
+// the queries).  Per round a CTA embeds 128 subdomains:
+//   * 16 warps x 8 subdomains: gather the 128 perimeter values (G1 order;
+//     lane l owns positions 4l..4l+3), conv1 1->8 / conv2 8->1 (k = 5,
+//     circular) + GELU in registers with warp-shuffle windows;
+//   * the embedding e (fp32) is split e = e_hi + e_lo into two bf16 SWIZZLE_128B
+//     A operands; W1 = W1_hi + W1_lo is resident as two bf16 B operands; one
+//     elected thread issues the three products hi.hi + hi.lo + lo.hi
+//     (tcgen05.mma, M = N = 128, 24 x K16) into a TMEM accumulator, so
+//     z = W1 e keeps ~fp32 accuracy (error ~2^-16 of the terms) at tensor-core
+//     speed;
+//   * 16 warps drain TMEM (tcgen05.ld, 32 columns each) and store z + b1.
+// The fp32 path keeps the SIMT embed (kernels_sdnet.cu).
+#include <cuda_bf16.h>
+
+#include "tc_common.cuh"
+
+namespace mfp {
+namespace emb {
+
+using namespace tcx;
+
+constexpr int kRowsE = 128;              // subdomains per round (UMMA M)
+constexpr int kThreadsE = 512;           // 16 warps
+constexpr int kImg = kRowsE * kNB * 2;   // 32 KB bf16 image
+constexpr int kPerWarp = kRowsE / 16;
+
+size_t smem_bytes() { return 4 * (size_t)kImg + 4 * (96 + kD) + 64; }
+
+template <int GELU>
+__global__ void __launch_bounds__(kThreadsE, 1)
+k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ anchors,
+           const float* __restrict__ gb, int64_t B, DevNet net, float* __restrict__ z) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sWhi = smem_raw;
+  uint8_t* sWlo = sWhi + kImg;
+  uint8_t* sAhi = sWlo + kImg;
+  uint8_t* sAlo = sAhi + kImg;
+  float* sCw = reinterpret_cast<float*>(sAlo + kImg);   // c1w[40] c1b[8] c2w[40] c2b[1]
+  float* sB1 = sCw + 96;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sB1 + kD);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(net.W1img);
+    uint4* dst = reinterpret_cast<uint4*>(sWhi);
+    for (int i = threadIdx.x; i < 2 * kImg / 16; i += kThreadsE) dst[i] = __ldg(src + i);
+    if (threadIdx.x < kD) sB1[threadIdx.x] = __ldg(net.b1 + threadIdx.x);
+    if (threadIdx.x < 40) sCw[threadIdx.x] = __ldg(net.conv1_w + threadIdx.x);
+    if (threadIdx.x < 8) sCw[40 + threadIdx.x] = __ldg(net.conv1_b + threadIdx.x);
+    if (threadIdx.x < 40) sCw[48 + threadIdx.x] = __ldg(net.conv2_w + threadIdx.x);
+    if (threadIdx.x == 0) sCw[88] = __ldg(net.conv2_b);
+  }
+  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(128)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int i0 = 4 * lane;
+  const uint32_t a_hi = smem_u32(sAhi), a_lo = smem_u32(sAlo);
+  uint32_t phase = 0u;
+  for (int64_t base = (int64_t)blockIdx.x * kRowsE; base < B; base += (int64_t)gridDim.x * kRowsE) {
+    // ---- gather + conv stack, 8 subdomains per warp (gathers issued up front)
+    float4 gpre[kPerWarp];
+#pragma unroll
+    for (int j = 0; j < kPerWarp; j++) {
+      int64_t s = base + warp * kPerWarp + j;
+      if (s > B - 1) s = B - 1;
+      gpre[j] = gb ? __ldg(reinterpret_cast<const float4*>(gb + s * kNB + i0)) : gather4(lat, L, __ldg(anchors + s), lane);
+    }
+#pragma unroll
+    for (int j = 0; j < kPerWarp; j++) {
+      const int row = warp * kPerWarp + j;
+      const float g4[4] = {gpre[j].x, gpre[j].y, gpre[j].z, gpre[j].w};
+      float e[4];
+      conv_stack<GELU>(g4, lane, sCw, e);
+      // e = e_hi + e_lo, both bf16 (round to nearest)
+      uint32_t h01, h23, l01, l23;
+      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h01) : "f"(e[1]), "f"(e[0]));
+      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h23) : "f"(e[3]), "f"(e[2]));
+      const float r0 = e[0] - __uint_as_float(h01 << 16), r1 = e[1] - __uint_as_float(h01 & 0xffff0000u);
+      const float r2 = e[2] - __uint_as_float(h23 << 16), r3 = e[3] - __uint_as_float(h23 & 0xffff0000u);
+      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l01) : "f"(r1), "f"(r0));
+      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l23) : "f"(r3), "f"(r2));
+      const uint32_t off = sw128_off(row, i0) + (uint32_t)((i0 & 7) * 2);
+      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a_hi + off), "r"(h01), "r"(h23) : "memory");
+      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a_lo + off), "r"(l01), "r"(l23) : "memory");
+    }
+    fence_proxy_async();
+    __syncthreads();
+    // ---- z = e W1^T on the tensor core: hi.hi + hi.lo + lo.hi
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+      const uint32_t w_hi = smem_u32(sWhi), w_lo = smem_u32(sWlo);
+#pragma unroll
+      for (int k = 0; k < kNB / 16; k++) {
+        const uint32_t off = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
+        mma_f16<0>(tmem, sw128_desc(a_hi + off), sw128_desc(w_hi + off), k > 0 ? 1u : 0u);
+        mma_f16<0>(tmem, sw128_desc(a_hi + off), sw128_desc(w_lo + off), 1u);
+        mma_f16<0>(tmem, sw128_desc(a_lo + off), sw128_desc(w_hi + off), 1u);
+      }
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    tc_fence_after();
+    // ---- drain: warp w reads lanes 32 (w % 4).., columns 32 (w / 4)..
+    {
+      const int quad = warp & 3, cb = warp >> 2;
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(cb * 32), r);
+      tmem_wait_ld();
+      const int64_t s = base + quad * 32 + lane;
+      if (s < B) {
+        float4* dst = reinterpret_cast<float4*>(z + s * kD + cb * 32);
+        const float* bb = sB1 + cb * 32;
+#pragma unroll
+        for (int v = 0; v < 8; v++)
+          dst[v] = make_float4(__uint_as_float(r[4 * v]) + bb[4 * v], __uint_as_float(r[4 * v + 1]) + bb[4 * v + 1],
+                               __uint_as_float(r[4 * v + 2]) + bb[4 * v + 2], __uint_as_float(r[4 * v + 3]) + bb[4 * v + 3]);
+      }
+    }
+    tc_fence_before();
+    __syncthreads();   // A operands and the accumulator are reused next round
+  }
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128) : "memory");
+  }
+}
+
+}  // namespace emb
+
+bool embed_tc_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MFP_EMBED_SIMT");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+void embed_tc_kernel_attributes() {
+  cudaFuncSetAttribute(emb::k_embed_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)emb::smem_bytes());
+  cudaFuncSetAttribute(emb::k_embed_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)emb::smem_bytes());
+}
+
+void launch_embed_tc(const float* lat, const LatticeGeom& L, const uint32_t* anchors, const float* gb,
+                     int64_t B, const DevNet& net, float* z, cudaStream_t s) {
+  if (B <= 0) return;
+  int64_t blocks = (B + emb::kRowsE - 1) / emb::kRowsE;
+  if (blocks > 148) blocks = 148;
+  const size_t sm = emb::smem_bytes();
+  if (net.gelu_tanh)
+    emb::k_embed_tc<1><<<(int)blocks, emb::kThreadsE, sm, s>>>(lat, L, anchors, gb, B, net, z);
+  else
+    emb::k_embed_tc<0><<<(int)blocks, emb::kThreadsE, sm, s>>>(lat, L, anchors, gb, B, net, z);
+}
+
+}  // namespace mfp

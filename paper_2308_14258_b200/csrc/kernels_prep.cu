@@ -25,10 +25,16 @@ __global__ void k_prep(PrepArgs a) {
   const int d = kD;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  // W1T[k][c] = W1[c][k]
+  // W1T[k][c] = W1[c][k]; bf16 split images W1 = W1_hi + W1_lo (row c, K k)
   for (int64_t i = tid; i < (int64_t)kNB * d; i += nth) {
     int k = (int)(i / d), c = (int)(i % d);
-    a.W1T[i] = a.P[a.oW1 + (int64_t)c * kNB + k];
+    const float w = a.P[a.oW1 + (int64_t)c * kNB + k];
+    a.W1T[i] = w;
+    const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(w - __bfloat162float(hi));
+    uint8_t* img = reinterpret_cast<uint8_t*>(a.W1img);
+    *reinterpret_cast<__nv_bfloat16*>(img + sw128_offset(c, k)) = hi;
+    *reinterpret_cast<__nv_bfloat16*>(img + kD * kNB * 2 + sw128_offset(c, k)) = lo;
   }
   // hidden layers
   for (int64_t i = tid; i < (int64_t)a.n_hidden * d * d; i += nth) {

@@ -28,23 +28,6 @@ constexpr int kEmbPerWarp = kEmbSub / kEmbWarps;
 constexpr int kEs = kEmbSub + 4;             // padded row of e^T (bank spread)
 constexpr int kEmbSmem = (kNB * kD + kNB * kEs + 96 + kD) * 4;
 
-// Window [i0-2, i0+5] of a circular length-128 signal held 4-per-lane (lane l
-// owns positions 4l..4l+3): two values from each neighbouring lane.
-__device__ __forceinline__ void circ_window(const float (&v)[4], int lane, float (&w)[8]) {
-  const int left = (lane + 31) & 31, right = (lane + 1) & 31;
-  w[0] = __shfl_sync(0xffffffffu, v[2], left);
-  w[1] = __shfl_sync(0xffffffffu, v[3], left);
-  w[2] = v[0]; w[3] = v[1]; w[4] = v[2]; w[5] = v[3];
-  w[6] = __shfl_sync(0xffffffffu, v[0], right);
-  w[7] = __shfl_sync(0xffffffffu, v[1], right);
-}
-
-template <int GELU>
-__device__ __forceinline__ float emb_act(float x) {
-  if constexpr (GELU == 1) return gelu_tanh(x);
-  else return gelu_erf(x);
-}
-
 template <int GELU>
 __global__ void __launch_bounds__(kEmbWarps * 32, 2)
 k_gather_embed(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ anchors,
@@ -67,7 +50,6 @@ k_gather_embed(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __r
   }
   __syncthreads();
   const int i0 = 4 * lane;                   // this lane's 4 consecutive perimeter positions
-  const int edge = lane >> 3, t0 = 4 * (lane & 7);
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   for (int64_t base = (int64_t)blockIdx.x * kEmbSub; base < B; base += (int64_t)gridDim.x * kEmbSub) {
     // ---- phase A: gather + conv stack, 8 subdomains per warp.  All 8
@@ -77,51 +59,16 @@ k_gather_embed(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __r
     for (int j = 0; j < kEmbPerWarp; j++) {
       int64_t s = base + warp * kEmbPerWarp + j;
       if (s > B - 1) s = B - 1;
-      if (gb) {
-        gpre[j] = __ldg(reinterpret_cast<const float4*>(gb + s * kNB + i0));
-      } else {
-        int a, b;
-        unpack_anchor(__ldg(anchors + s), a, b);
-        const int lx = kH * a, ly = kH * b;
-        if (edge == 0) gpre[j] = *reinterpret_cast<const float4*>(lat + (int64_t)b * L.strideH + lx + t0);
-        else if (edge == 1) gpre[j] = *reinterpret_cast<const float4*>(lat + L.offV + (int64_t)(a + 2) * L.strideV + ly + t0);
-        else if (edge == 2) {
-          const float* r = lat + (int64_t)(b + 2) * L.strideH + lx + kM - t0;
-          gpre[j] = make_float4(r[0], r[-1], r[-2], r[-3]);
-        } else {
-          const float* r = lat + L.offV + (int64_t)a * L.strideV + ly + kM - t0;
-          gpre[j] = make_float4(r[0], r[-1], r[-2], r[-3]);
-        }
-      }
+      gpre[j] = gb ? __ldg(reinterpret_cast<const float4*>(gb + s * kNB + i0)) : gather4(lat, L, __ldg(anchors + s), lane);
     }
 #pragma unroll
     for (int j = 0; j < kEmbPerWarp; j++) {
       const int col = warp * kEmbPerWarp + j;
       const float gv4[4] = {gpre[j].x, gpre[j].y, gpre[j].z, gpre[j].w};
-      float win[8];
-      circ_window(gv4, lane, win);
-      // conv1 (1 -> 8) + GELU on positions i0..i0+3, then conv2 (8 -> 1)
-      // accumulated channel by channel from each channel's shuffled window
-      float acc2[4] = {sCw[88], sCw[88], sCw[88], sCw[88]};
+      float e[4];
+      conv_stack<GELU>(gv4, lane, sCw, e);
 #pragma unroll
-      for (int o = 0; o < kC1; o++) {
-        float c1v[4];
-#pragma unroll
-        for (int p = 0; p < 4; p++) {
-          float v = sCw[40 + o];
-#pragma unroll
-          for (int t = 0; t < kK; t++) v = fmaf(sCw[o * kK + t], win[p + t], v);
-          c1v[p] = emb_act<GELU>(v);
-        }
-        float w2[8];
-        circ_window(c1v, lane, w2);
-#pragma unroll
-        for (int p = 0; p < 4; p++)
-#pragma unroll
-          for (int t = 0; t < kK; t++) acc2[p] = fmaf(sCw[48 + o * kK + t], w2[p + t], acc2[p]);
-      }
-#pragma unroll
-      for (int p = 0; p < 4; p++) sE[(i0 + p) * kEs + col] = emb_act<GELU>(acc2[p]);
+      for (int p = 0; p < 4; p++) sE[(i0 + p) * kEs + col] = e[p];
     }
     __syncthreads();
     // ---- phase B: z[64 x 128] = e[64 x 128] W1^T, thread = 4 subdomains x 8 outputs

@@ -95,6 +95,7 @@ struct DevNet {
   // bf16 tables (tcgen05 path): weights pre-swizzled into the SW128 K-major image
   const uint16_t* Wh_sw;  // [n_hidden][36 KB image]   (single-CTA chain)
   const uint16_t* Wh_sw2; // [n_hidden][2][18 KB half] (CTA-pair chain: rows 64h..64h+63)
+  const uint16_t* W1img;  // [2][128*128] bf16 SW128 images of W1 = W1_hi + W1_lo (tensor-core embed)
   const float* Qc;        // [64][d] row-major centre queries (tc path)
   const float* Qf;        // [961][d] row-major interior queries
   // exact subsolver
@@ -150,7 +151,12 @@ struct PrepArgs {
   float* QTc; float* QTf; float* Qc; float* Qf;
   uint16_t* Wsw;           // [n_hidden][kWImg] 16-bit SW128 K-major images
   uint16_t* Wsw2;          // [n_hidden][kWImg] CTA-pair half images
+  uint16_t* W1img;         // [2][128*128] W1 hi / lo bf16 images
 };
+bool embed_tc_enabled();
+void launch_embed_tc(const float* lat, const LatticeGeom& L, const uint32_t* anchors, const float* gb,
+                     int64_t B, const DevNet& net, float* z, cudaStream_t s);
+void embed_tc_kernel_attributes();
 void launch_prep(const PrepArgs& a, cudaStream_t s);
 void sdnet_kernel_attributes();
 void tc_kernel_attributes();

@@ -6,6 +6,8 @@ placement / indexing bit-exact (written-cell sets identical, untouched cells
 bit-identical).  Inputs: seeded GP boundaries and W-rand weights
 (mfp_inputs), identical on both sides.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -206,6 +208,29 @@ def test_sdnet_tensorcore_field_parity(lib, precision, nx, ny, t, grid):
         inner[0, :] = inner[-1, :] = False
         inner[:, 0] = inner[:, -1] = False
         assert rel_err(gpu_lines(lib, m, nx, ny, grid), ref.lines, inner) <= BF16_TOL
+
+
+WFIT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "weights", "sdnet_fit_d128.npy")
+
+
+@pytest.mark.skipif(not os.path.exists(WFIT), reason="fitted weights not generated (tools/fit_sdnet.py)")
+@pytest.mark.parametrize("precision,tol", [(0, FP32_TOL), (1, BF16_TOL), (2, BF16_TOL)])
+def test_fitted_weights_parity(lib, precision, tol):
+    """W-fit (tools/fit_sdnet.py): outputs are O(1) harmonic-extension values, so
+    every precision is held to its bar relative to the output itself."""
+    import torch
+    w = np.load(WFIT)
+    nx = ny = 128
+    cfg = lib.make_config(nx, ny, precision=precision, subsolver=lib.SDNET, check_every=1)
+    m = lib.Mfp(cfg, lib.make_net(gelu=1 if precision else 0), w)
+    gb = random_boundaries(500, seed=13)
+    out = m.sdnet_batch(torch.from_numpy(gb).cuda(), 0).cpu().numpy()
+    ref = oracle.sdnet_forward(w.astype(np.float64), gb.astype(np.float64), oracle.writeset(0, 0)[1])
+    assert rel_err(out, ref) <= tol
+    g = gp_boundary(nx, ny, 1)
+    u, _ = m.solve(g, 10, 0.0)
+    r = oracle.mfp_run(oracle.MfpConfig(nx, ny), g.astype(np.float64), 10, params=w.astype(np.float64))
+    assert rel_err(u, r.u) <= tol
 
 
 # ----------------------------------------------------------------- placement
