@@ -96,7 +96,8 @@ def sample_boundaries(torch, n, device, gen):
     arg = kx[:, :, None] * pp[None, None, :, 0] + ky[:, :, None] * pp[None, None, :, 1] + ph[:, :, None]
     out[2 * k:] = (amp[:, :, None] * torch.sin(arg)).sum(1)
     # (c) copies of (a)/(b) with whole edges zeroed (interior lines still at the initial 0)
-    src = out[torch.randint(0, n, (k,), device=device, generator=gen)]
+    pick = torch.randint(0, n - k, (k,), device=device, generator=gen)
+    src = out[torch.where(pick < k, pick, pick + k)]      # rows of (a) or (b) only
     mask = (torch.rand(k, 4, device=device, generator=gen) < 0.35).float()
     mask = mask.repeat_interleave(M, dim=1)
     out[k:2 * k] = src * (1 - mask)
@@ -124,6 +125,8 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "weights", "sdnet_fit_d128.npy"))
     ap.add_argument("--wide", action="store_true")
     ap.add_argument("--normalized-loss", action="store_true")
+    ap.add_argument("--init", default=None, help="start from these flat weights (MFCK order)")
+    ap.add_argument("--eval", action="store_true", help="only evaluate --init")
     args = ap.parse_args()
     global WIDE
     WIDE = args.wide
@@ -157,6 +160,19 @@ def main():
                 h = F.gelu(lin(h))
             return s.head(h)[..., 0]
 
+        def load_flat(s, v):
+            v = torch.as_tensor(v, dtype=torch.float32)
+            o = 0
+            parts = [s.c0.weight, s.c0.bias, s.c1.weight, s.c1.bias, s.W1.weight, s.W2.weight, s.W1.bias]
+            for lin in s.hid:
+                parts += [lin.weight, lin.bias]
+            parts += [s.head.weight, s.head.bias]
+            with torch.no_grad():
+                for p in parts:
+                    p.copy_(v[o:o + p.numel()].reshape(p.shape))
+                    o += p.numel()
+            assert o == v.numel()
+
         def flat(s):
             parts = [s.c0.weight, s.c0.bias, s.c1.weight, s.c1.bias, s.W1.weight, s.W2.weight, s.W1.bias]
             for lin in s.hid:
@@ -165,12 +181,16 @@ def main():
             return torch.cat([p.detach().reshape(-1).float().cpu() for p in parts]).numpy()
 
     net = SDNet().to(dev)
+    if args.init:
+        net.load_flat(np.load(args.init))
+    if args.eval:
+        args.steps = 0
     opt = torch.optim.AdamW(net.parameters(), lr=args.lr, weight_decay=0.0)
-    sched = torch.optim.lr_scheduler.OneCycleLR(opt, max_lr=args.lr, total_steps=args.steps,
-                                                pct_start=max(0.02, 4.0 / args.steps))
+    sched = torch.optim.lr_scheduler.OneCycleLR(opt, max_lr=args.lr, total_steps=max(args.steps, 100),
+                                                pct_start=max(0.02, 4.0 / max(args.steps, 4)))
     t0 = time.time()
     log = []
-    for step in range(args.steps):
+    for step in range(args.steps if not args.eval else 0):
         g = sample_boundaries(torch, args.batch, dev, gen)
         scale = g.abs().amax(1, keepdim=True) + 1e-3
         # centre-line queries every step (the hot path) + a random interior subset (final phase)
@@ -194,6 +214,10 @@ def main():
         ec = ((net(g, Xc) - g @ Hc.T) / scale).abs()
         ef = ((net(g, Xf) - g @ Hf.T) / scale).abs()
     flat = net.flat()
+    if args.eval:
+        print(json.dumps({"val_centre_max_rel_err": float(ec.max()), "val_centre_mean_rel_err": float(ec.mean()),
+                          "val_interior_max_rel_err": float(ef.max()), "val_interior_mean_rel_err": float(ef.mean())}))
+        return
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     np.save(args.out, flat.astype(np.float32))
     meta = {"params": int(flat.size), "steps": args.steps, "batch": args.batch, "lr": args.lr, "seed": args.seed,
