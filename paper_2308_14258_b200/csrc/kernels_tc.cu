@@ -105,6 +105,35 @@ __device__ __forceinline__ float act_head(float x) {
     return gelu_erf(x);
   }
 }
+// Last layer + head on one 32-column TMEM chunk: acc += wo . act(x) for the
+// tanh form in packed fp32x2 (FMUL2/FFMA2; MUFU tanh per lane), same per-lane
+// arithmetic as act_head<1>; the erf form stays scalar.
+template <int GELU>
+__device__ __forceinline__ void head32(const uint32_t (&r)[32], const float* wo, f2& acc) {
+  if constexpr (GELU == 1) {
+    const f2 g0 = f2_make(kG0, kG0), g1 = f2_make(kG1, kG1);
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+      const f2 x = f2_make(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+      const f2 u = fmul2(x, ffma2(fmul2(x, x), g1, g0));
+      float u0, u1;
+      f2_split(u, u0, u1);
+      const f2 h = ffma2(x, f2_make(tanh_approx(u0), tanh_approx(u1)), x);
+      const float2 w = *reinterpret_cast<const float2*>(wo + 2 * e);
+      acc = ffma2(f2_make(w.x, w.y), h, acc);
+    }
+  } else {
+    float y0, y1;
+    f2_split(acc, y0, y1);
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      y0 = fmaf(wo[e], act_head<GELU>(__uint_as_float(r[e])), y0);
+      y1 = fmaf(wo[e + 1], act_head<GELU>(__uint_as_float(r[e + 1])), y1);
+    }
+    acc = f2_make(y0, y1);
+  }
+}
+
 // Activation of a layer feeding an MMA, 8 fp32 pre-activations -> 4 packed words of h' = 2 GELU.
 template <int GELU, int F16>
 __device__ __forceinline__ void act8(const float (&v)[8], uint32_t (&w)[4], uint32_t c0, uint32_t c1) {
@@ -565,10 +594,13 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
           const float4 a1 = *reinterpret_cast<const float4*>(S.w2 + cc * 8 + 4);
           const float4 b0 = *reinterpret_cast<const float4*>(S.w2 + kD + cc * 8);
           const float4 b1 = *reinterpret_cast<const float4*>(S.w2 + kD + cc * 8 + 4);
-          const float v[8] = {z0.x + fmaf(a0.x, qx, b0.x * qy), z0.y + fmaf(a0.y, qx, b0.y * qy),
-                              z0.z + fmaf(a0.z, qx, b0.z * qy), z0.w + fmaf(a0.w, qx, b0.w * qy),
-                              z1.x + fmaf(a1.x, qx, b1.x * qy), z1.y + fmaf(a1.y, qx, b1.y * qy),
-                              z1.z + fmaf(a1.z, qx, b1.z * qy), z1.w + fmaf(a1.w, qx, b1.w * qy)};
+          // z + W2 x_p in packed fp32x2: (z + b qy) + a qx per lane
+          const f2 QX = f2_make(qx, qx), QY = f2_make(qy, qy);
+          float v[8];
+          f2_split(ffma2(f2_make(a0.x, a0.y), QX, ffma2(f2_make(b0.x, b0.y), QY, f2_make(z0.x, z0.y))), v[0], v[1]);
+          f2_split(ffma2(f2_make(a0.z, a0.w), QX, ffma2(f2_make(b0.z, b0.w), QY, f2_make(z0.z, z0.w))), v[2], v[3]);
+          f2_split(ffma2(f2_make(a1.x, a1.y), QX, ffma2(f2_make(b1.x, b1.y), QY, f2_make(z1.x, z1.y))), v[4], v[5]);
+          f2_split(ffma2(f2_make(a1.z, a1.w), QX, ffma2(f2_make(b1.z, b1.w), QY, f2_make(z1.z, z1.w))), v[6], v[7]);
           uint32_t w[4];
           act8<GELU, F16>(v, w, c0, c1);
           st_shared_v4(a_base + sw128_off(row, cc * 8), w[0], w[1], w[2], w[3]);
@@ -576,7 +608,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       }
       fence_proxy_async();
       arrive_a();
-      float y = 0.f;
+      f2 yacc = f2_make(0.f, 0.f);
       for (int l = 0; l < nh; l++) {
         mbar_wait(&S.bars[kSlots2 + slot], pd);
         pd ^= 1u;
@@ -598,9 +630,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
               st_shared_v4(a_base + sw128_off(row, ch * 32 + c8 * 8), w[0], w[1], w[2], w[3]);
             }
           } else {
-            const float* wo = S.wo + ch * 32;
-#pragma unroll
-            for (int e = 0; e < 32; e++) y = fmaf(wo[e], act_head<GELU>(__uint_as_float(r[e])), y);
+            head32<GELU>(r, S.wo + ch * 32, yacc);
           }
         }
         tc_fence_before();
@@ -610,7 +640,9 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
         }
       }
       if (have_next) *reinterpret_cast<float4*>(zb + zi) = znext;
-      if (valid) sink_store(sink, sidx, p, y + bo);
+      float y0, y1;
+      f2_split(yacc, y0, y1);
+      if (valid) sink_store(sink, sidx, p, (y0 + y1) + bo);
     }
   }
   tc_fence_before();

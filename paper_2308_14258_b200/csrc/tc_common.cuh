@@ -108,6 +108,36 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
                : "memory");
 }
 
+// Packed fp32x2 arithmetic (FFMA2 / FMUL2 / FADD2 on sm_100a): two fp32 lanes
+// per instruction, IEEE round-to-nearest per lane — halves the FMA-pipe issue
+// cost of the fp32 parts of the epilogue without changing their numerics.
+struct f2 {
+  uint64_t v;
+};
+__device__ __forceinline__ f2 f2_make(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_split(f2 a, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
+}
+__device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return r;
+}
+__device__ __forceinline__ f2 fmul2(f2 a, f2 b) {
+  f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 fadd2(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+
 // Byte offset of (row, k) in a 128 x 128 16-bit SW128 K-major image (two 16 KB
 // K-halves; 16-byte chunk index XOR row mod 8).  Same formula as kernels_prep.
 __device__ __forceinline__ uint32_t sw128_off(int r, int k) {
