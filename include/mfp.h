@@ -106,7 +106,10 @@ typedef struct {
   int32_t conv_ch[5];
   int32_t d;
   int32_t n_hidden;
-  int32_t gelu;        /* 0: exact erf; 1: tanh approximation (bf16 path only)      */
+  int32_t gelu;        /* 0: erff-based GELU; 1: fast GELU on the tensor-core paths —
+                        * the same exact GELU x Phi(x) from fitted tanh / polynomial
+                        * forms, |error of 2 GELU| <= 4e-4 (reading GELU).
+                        * The fp32 path always uses erff.                          */
 } mfp_sdnet_desc;
 
 typedef struct {

@@ -48,7 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                "-I", inc, "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr",
-               "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
+               "-Xptxas", "-v" if verbose else "-O3", *os.environ.get("MFP_NVCC_EXTRA", "").split(),
+               "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
     failed = False

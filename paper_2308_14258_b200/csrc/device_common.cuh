@@ -14,18 +14,28 @@ __device__ __forceinline__ float gelu_erf(float x) {
   return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
 }
 
-// tanh approximation of GELU (bf16 path only, mfp_sdnet_desc.gelu = 1).
 __device__ __forceinline__ float tanh_approx(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float gelu_tanh(float x) {
-  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  float u = k0 * x * fmaf(k1, x * x, 1.0f);
-  float hx = 0.5f * x;
-  return fmaf(hx, tanh_approx(u), hx);
+
+// Fast GELU (mfp_sdnet_desc.gelu = 1; reading GELU): the tanh form
+// 0.5 x (1 + tanh(c0 x + c1 x^3)), c0 = sqrt(2/pi), c1 = 0.044715 c0, of the
+// exact GELU x Phi(x).  Max |error of 2 GELU| against erf: 9.5e-4 near
+// |x| = 2, but O(x^5) near 0 where most pre-activations sit.  Refitted
+// coefficients (tools/fit_gelu_poly.py) were tried: a minimax (c0, c1) halves
+// the max error yet doubled the measured fp16 field error (it is worse for
+// small |x|); a 3-coefficient clamped form is accurate everywhere but costs 11%
+// of the chain's throughput — DESIGN.md §7.
+constexpr float kGF0 = 0.7978845608028654f, kGF1 = 0.7978845608028654f * 0.044715f;
+
+// 2 GELU(x) (scalar).
+__device__ __forceinline__ float gelu2_fast(float x) {
+  const float u = x * fmaf(kGF1, x * x, kGF0);
+  return fmaf(x, tanh_approx(u), x);
 }
+__device__ __forceinline__ float gelu_fast(float x) { return 0.5f * gelu2_fast(x); }
 
 // Lattice accessors.  Anchor packed as a | b << 16 where
 // (a, b) are local vertical/horizontal line indices of the subdomain's left /
@@ -94,7 +104,7 @@ __device__ __forceinline__ void circ_window(const float (&v)[4], int lane, float
 
 template <int GELU>
 __device__ __forceinline__ float emb_act(float x) {
-  if constexpr (GELU == 1) return gelu_tanh(x);
+  if constexpr (GELU == 1) return gelu_fast(x);
   else return gelu_erf(x);
 }
 

@@ -42,83 +42,48 @@ constexpr int kWTile = kWImg * 2;                // 36 KB per hidden layer: weig
 constexpr int kOnes = kRows * 16 * 2;            // 4 KB constant A block: K columns 0/1 = 1
 constexpr int kTmemCols = 512;
 constexpr int kZRows = 4;                        // subdomains one 128-row tile can touch (q >= 61)
-constexpr float kG0 = 0.7978845608028654f;       // sqrt(2/pi)
-constexpr float kG1 = 0.7978845608028654f * 0.044715f;
 
 using namespace tcx;
 
-// Round two fp32 values to the operand type (lo -> bits 0-15).  fp16: F2FP
-// (cvt.rn).  bf16: truncation of the pre-activation by one byte permute — an
-// ALU-pipe op instead of an F2FP on the quarter-rate XU pipe that MUFU.TANH
-// already saturates (emulated cost: conditioning-scale error 3.5e-4 -> 4.1e-4
-// against the 3e-3 bar).  The GELU output fed to the next MMA is
-// produced by bf16x2 arithmetic (round-to-nearest).
+// Round two fp32 values to the operand type (lo -> bits 0-15), round-to-nearest
+// (F2FP: 64 instr/clk/SM on B200, not on the MUFU pipe — tools/ubench).
 template <int F16>
-__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
-  uint32_t r;
-  if constexpr (F16) {
-    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  } else {
-    r = __byte_perm(__float_as_uint(lo), __float_as_uint(hi), 0x7632);
-  }
-  return r;
-}
-template <int F16>
-__device__ __forceinline__ uint32_t pack2_rn(float lo, float hi) {  // constants
+__device__ __forceinline__ uint32_t pack2_rn(float lo, float hi) {
   uint32_t r;
   if constexpr (F16) asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   else asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
 
-// h' = x (1 + tanh(x (G0 + G1 x^2))) = 2 GELU_tanh(x) on two packed 16-bit lanes.
-template <int F16>
-__device__ __forceinline__ uint32_t gelu2x2(uint32_t x, uint32_t c0, uint32_t c1) {
-  uint32_t x2, t, u, th, h;
-  if constexpr (F16) {
-    asm("mul.rn.f16x2 %0, %1, %1;" : "=r"(x2) : "r"(x));
-    asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(t) : "r"(x2), "r"(c1), "r"(c0));
-    asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(u) : "r"(x), "r"(t));
-    asm("tanh.approx.f16x2 %0, %1;" : "=r"(th) : "r"(u));
-    asm("fma.rn.f16x2 %0, %1, %2, %1;" : "=r"(h) : "r"(x), "r"(th));
-  } else {
-    asm("mul.rn.bf16x2 %0, %1, %1;" : "=r"(x2) : "r"(x));
-    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(t) : "r"(x2), "r"(c1), "r"(c0));
-    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(u) : "r"(x), "r"(t));
-    asm("tanh.approx.bf16x2 %0, %1;" : "=r"(th) : "r"(u));
-    asm("fma.rn.bf16x2 %0, %1, %2, %1;" : "=r"(h) : "r"(x), "r"(th));
-  }
-  return h;
+// h' = 2 GELU(x) on an fp32 pair (fast form, device_common.cuh):
+// u = x (c0 + c1 x^2) (FMUL2, FFMA2, FMUL2), MUFU tanh per lane, h' = x + x tanh(u)
+// (FFMA2).  Measured on B200 (tools/ubench): FFMA2/FMUL2 64 instr/clk/SM (128
+// lanes), F2FP 64, HFMA2 64, PRMT 64, MUFU.TANH 16 lanes/clk — fewer FMA/ALU
+// cycles than packed 16-bit GELU arithmetic, and one rounding.  An FMA-pipe
+// polynomial for part of the pairs (to offload MUFU) measured slower: the
+// epilogue is issue/latency bound as much as MUFU bound, DESIGN.md §6.
+__device__ __forceinline__ f2 gelu2_mufu(f2 x) {
+  float u0, u1;
+  f2_split(fmul2(x, ffma2(fmul2(x, x), f2_make(kGF1, kGF1), f2_make(kGF0, kGF0))), u0, u1);
+  return ffma2(x, f2_make(tanh_approx(u0), tanh_approx(u1)), x);
 }
-
-
 
 // Activation of the fp32 last layer, up to the factor the head weights carry:
-// tanh form returns x (1 + tanh(x (G0 + G1 x^2))) = 2 GELU(x) (smem wo holds
-// wo / 2), erf form returns GELU(x) (smem wo holds wo).
+// fast form returns 2 GELU(x) (smem wo holds wo / 2), erf form returns GELU(x)
+// (smem wo holds wo).
 template <int GELU>
 __device__ __forceinline__ float act_head(float x) {
-  if constexpr (GELU == 1) {
-    const float u = x * fmaf(kG1, x * x, kG0);
-    return fmaf(x, tanh_approx(u), x);
-  } else {
-    return gelu_erf(x);
-  }
+  if constexpr (GELU == 1) return gelu2_fast(x);
+  else return gelu_erf(x);
 }
-// Last layer + head on one 32-column TMEM chunk: acc += wo . act(x) for the
-// tanh form in packed fp32x2 (FMUL2/FFMA2; MUFU tanh per lane), same per-lane
-// arithmetic as act_head<1>; the erf form stays scalar.
+// Last layer + head on one 32-column TMEM chunk: acc += wo . act(x), the fast
+// form in packed fp32x2; the erf form scalar.
 template <int GELU>
 __device__ __forceinline__ void head32(const uint32_t (&r)[32], const float* wo, f2& acc) {
   if constexpr (GELU == 1) {
-    const f2 g0 = f2_make(kG0, kG0), g1 = f2_make(kG1, kG1);
 #pragma unroll
     for (int e = 0; e < 16; e++) {
-      const f2 x = f2_make(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
-      const f2 u = fmul2(x, ffma2(fmul2(x, x), g1, g0));
-      float u0, u1;
-      f2_split(u, u0, u1);
-      const f2 h = ffma2(x, f2_make(tanh_approx(u0), tanh_approx(u1)), x);
+      const f2 h = gelu2_mufu(f2_make(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])));
       const float2 w = *reinterpret_cast<const float2*>(wo + 2 * e);
       acc = ffma2(f2_make(w.x, w.y), h, acc);
     }
@@ -134,15 +99,20 @@ __device__ __forceinline__ void head32(const uint32_t (&r)[32], const float* wo,
   }
 }
 
-// Activation of a layer feeding an MMA, 8 fp32 pre-activations -> 4 packed words of h' = 2 GELU.
+// Activation of a layer feeding an MMA: 8 fp32 pre-activations -> 4 packed
+// 16-bit words of h' = 2 GELU (weights carry the 1/2), one RN rounding each.
 template <int GELU, int F16>
-__device__ __forceinline__ void act8(const float (&v)[8], uint32_t (&w)[4], uint32_t c0, uint32_t c1) {
-  if constexpr (GELU == 1) {
+__device__ __forceinline__ void act8(const float (&v)[8], uint32_t (&w)[4]) {
 #pragma unroll
-    for (int e = 0; e < 4; e++) w[e] = gelu2x2<F16>(pack2<F16>(v[2 * e], v[2 * e + 1]), c0, c1);
-  } else {
-#pragma unroll
-    for (int e = 0; e < 4; e++) w[e] = pack2<F16>(2.f * gelu_erf(v[2 * e]), 2.f * gelu_erf(v[2 * e + 1]));
+  for (int e = 0; e < 4; e++) {
+    float h0, h1;
+    if constexpr (GELU == 1) {
+      f2_split(gelu2_mufu(f2_make(v[2 * e], v[2 * e + 1])), h0, h1);
+    } else {
+      h0 = 2.f * gelu_erf(v[2 * e]);
+      h1 = 2.f * gelu_erf(v[2 * e + 1]);
+    }
+    w[e] = pack2_rn<F16>(h0, h1);
   }
 }
 
@@ -267,7 +237,6 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, S
     const uint32_t a_base = smem_u32(S.A + slot * kTile);
     const uint32_t t_row = tmem + (uint32_t)(slot * kD) + ((uint32_t)(quad * 32) << 16);
     float* zb = S.zbuf + slot * kZRows * kD;
-    const uint32_t c0 = pack2_rn<F16>(kG0, kG0), c1 = pack2_rn<F16>(kG1, kG1);
     const float bo = __ldg(net.bo);
     // z staging: thread tid_s moves 4 consecutive floats of the tile's <= 4 subdomains
     const int zi = 4 * tid_s, zr_ = zi >> 7, zc = zi & 127;
@@ -310,7 +279,7 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, S
                               z1.x + fmaf(a1.x, qx, b1.x * qy), z1.y + fmaf(a1.y, qx, b1.y * qy),
                               z1.z + fmaf(a1.z, qx, b1.z * qy), z1.w + fmaf(a1.w, qx, b1.w * qy)};
           uint32_t w[4];
-          act8<GELU, F16>(v, w, c0, c1);
+          act8<GELU, F16>(v, w);
           st_shared_v4(a_base + sw128_off(row, cc * 8), w[0], w[1], w[2], w[3]);
         }
       }
@@ -338,7 +307,7 @@ k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, S
 #pragma unroll
                 for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[h][c8 * 8 + e]);  // bias already in D
                 uint32_t w[4];
-                act8<GELU, F16>(v, w, c0, c1);
+                act8<GELU, F16>(v, w);
                 st_shared_v4(a_base + sw128_off(row, (ch + h) * 32 + c8 * 8), w[0], w[1], w[2], w[3]);
               }
             } else {
@@ -405,7 +374,11 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAITC_%=:\n\t"
+#ifdef MFP_WAIT_SPIN
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+#else
       "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+#endif
       "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
@@ -550,9 +523,10 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
     const int row = quad * 32 + lane;
     const int tid_s = (warp - 2 - 4 * slot) * 32 + lane;
     const uint32_t a_base = smem_u32(S.A + slot * kTile);
+    const uint32_t a_row = a_base + (uint32_t)row * 128u;   // SW128 K-major row base (first K-half)
+    const int r7 = row & 7;
     const uint32_t t_row = tmem + (uint32_t)(slot * kD) + ((uint32_t)(quad * 32) << 16);
     float* zb = S.zbuf + slot * kZRows * kD;
-    const uint32_t c0 = pack2_rn<F16>(kG0, kG0), c1 = pack2_rn<F16>(kG1, kG1);
     const float bo = __ldg(net.bo);
     const int zi = 4 * tid_s, zr_ = zi >> 7, zc = zi & 127;
     auto row0_of = [&](int64_t j) -> int64_t { return (cid + j * ncl) * (2 * kRows) + rank * kRows; };
@@ -602,8 +576,8 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
           f2_split(ffma2(f2_make(a1.x, a1.y), QX, ffma2(f2_make(b1.x, b1.y), QY, f2_make(z1.x, z1.y))), v[4], v[5]);
           f2_split(ffma2(f2_make(a1.z, a1.w), QX, ffma2(f2_make(b1.z, b1.w), QY, f2_make(z1.z, z1.w))), v[6], v[7]);
           uint32_t w[4];
-          act8<GELU, F16>(v, w, c0, c1);
-          st_shared_v4(a_base + sw128_off(row, cc * 8), w[0], w[1], w[2], w[3]);
+          act8<GELU, F16>(v, w);
+          st_shared_v4(a_row + ((uint32_t)(cc >> 3) << 14) + ((uint32_t)((cc & 7) ^ r7) << 4), w[0], w[1], w[2], w[3]);
         }
       }
       fence_proxy_async();
@@ -620,14 +594,17 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
           tmem_ld32(t_row + (uint32_t)(ch * 32), r);
           tmem_wait_ld();
           if (!last) {
+            // SW128 address of (row, 32 ch + 8 c8): K-half ch / 2, 16-byte chunk (4 (ch & 1) + c8) ^ (row & 7)
+            const uint32_t a_kb = a_row + ((uint32_t)(ch >> 1) << 14);
+            const int cx = ((ch & 1) << 2) ^ r7;
 #pragma unroll
             for (int c8 = 0; c8 < 4; c8++) {
               float v[8];
 #pragma unroll
               for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[c8 * 8 + e]);
               uint32_t w[4];
-              act8<GELU, F16>(v, w, c0, c1);
-              st_shared_v4(a_base + sw128_off(row, ch * 32 + c8 * 8), w[0], w[1], w[2], w[3]);
+              act8<GELU, F16>(v, w);
+              st_shared_v4(a_kb + ((uint32_t)(cx ^ c8) << 4), w[0], w[1], w[2], w[3]);
             }
           } else {
             head32<GELU>(r, S.wo + ch * 32, yacc);

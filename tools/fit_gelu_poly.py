@@ -1,67 +1,95 @@
 #!/usr/bin/env python
-"""Minimax fit of the FMA-pipe GELU used for part of the tensor-core epilogue.
+"""Fits explored for the fast GELU of the tensor-core epilogues.
 
-The epilogue computes h' = 2 GELU_tanh(x) = x + e(x) with
-    e(x) = x tanh(G0 x + G1 x^3)          (even, 0 <= e <= |x|).
-MUFU tanh is the binding unit of the chain, so a fraction of the
-elements take a pure-FMA path instead:
-    t = x^2,  e ~= min(t R(min(t, T)), |x|),   R a degree-(n-1) polynomial,
-evaluated in fp32x2 (FFMA2).  This script finds R by linear-programming minimax
-on x in [0, a] (T = a^2), weighting the error by 1 / max(|h'(x)|, floor) so the
-relative error of h' is bounded where it is small (x < 0), and reports the
-max error over the whole line including the clamped tails.
+The epilogue produces h' = 2 GELU(x) = x (1 + S(x)), S(x) = erf(x / sqrt 2)
+(exact GELU, P:241 — the oracle's).  Two evaluations, chosen per element pair so
+that both the MUFU (tanh) pipe and the FMA pipe carry part of the load:
 
-    python tools/fit_gelu_poly.py --n 6 --a 3.4
+  (M) MUFU form:  S(x) ~= tanh(x (c0 + c1 x^2))                      [1 MUFU / element]
+      (the classic tanh GELU is c0 = sqrt(2/pi), c1 = 0.044715 c0 — its error
+      against erf is 9.5e-4 in h' but O(x^5) near 0.  The minimax refit of
+      (c0, c1) gives 5.4e-4 max yet is worse for small |x|, where most
+      pre-activations sit: measured fp16 field error doubled — not used.  A
+      third coefficient (with a clamp of x^2) reaches 5e-5 everywhere but costs
+      2 more instructions per pair: measured 11% slower — not used.  The kernels
+      keep the classic coefficients.)
+  (P) FMA form (measured slower on B200, not used — the epilogue is issue/latency
+      bound, not MUFU bound):  S(x) ~= x_c P(x_c^2),  x_c = clamp(x, -a, a),  S(a) = 1
+      (odd minimax polynomial with the end constraint, so |x| > a gives exactly
+      h' = 2x or 0; error dominated by x erfc(a / sqrt 2) near the clamp)
+
+Both fits minimise max |x (S_fit(x) - erf(x / sqrt 2))| = max |h'_fit - h'|.
+
+    python tools/fit_gelu_poly.py
 """
 import argparse
 
 import numpy as np
-from scipy.optimize import linprog
-
-G0 = 0.7978845608028654
-G1 = G0 * 0.044715
+from scipy.optimize import least_squares, linprog
+from scipy.special import erf
 
 
-def e_true(x):
-    return x * np.tanh(G0 * x + G1 * x ** 3)
+def s_mufu(c, x):
+    return np.tanh(x * (c[0] + x * x * c[1]))
 
 
-def fit(n, a, floor=0.05, npts=3000):
+def fit_mufu(x):
+    target = erf(x / np.sqrt(2.0))
+
+    def res(c, w=1.0):
+        return (s_mufu(c, x) - target) * x * w
+
+    c = least_squares(res, [0.7978845608, 0.0356774]).x
+    w = np.ones_like(x)
+    for _ in range(80):   # Lawson-style reweighting towards minimax
+        e = np.abs(res(c))
+        w = w * (1.0 + 4.0 * e / e.max())
+        w /= w.mean()
+        c = least_squares(lambda cc: res(cc, np.sqrt(w)), c).x
+    return c
+
+
+def fit_poly(n, a, npts=4000):
     x = np.linspace(0.0, a, npts)
     t = x * x
-    # unknowns: c_0..c_{n-1}, eps ; minimise eps s.t. |w (t R(t) - e)| <= eps, both signs of x
-    w = np.maximum(1.0 / np.maximum(np.abs(x + e_true(x)), floor), 1.0 / np.maximum(np.abs(-x + e_true(x)), floor))
-    V = (t[:, None] ** np.arange(n)[None, :]) * t[:, None]
-    A = np.vstack([np.hstack([w[:, None] * V, -np.ones((npts, 1))]), np.hstack([-w[:, None] * V, -np.ones((npts, 1))])])
-    b = np.concatenate([w * e_true(x), -w * e_true(x)])
-    c = np.zeros(n + 1)
-    c[-1] = 1.0
-    res = linprog(c, A_ub=A, b_ub=b, bounds=[(None, None)] * (n + 1), method="highs")
-    return res.x[:n], res.x[n]
+    target = erf(x / np.sqrt(2.0))
+    V = x[:, None] * t[:, None] ** np.arange(n)[None, :]
+    W = np.maximum(x, 0.05)[:, None]
+    A = np.vstack([np.hstack([W * V, -np.ones((npts, 1))]), np.hstack([-W * V, -np.ones((npts, 1))])])
+    b = np.concatenate([W[:, 0] * target, -W[:, 0] * target])
+    Aeq = np.hstack([a * (a * a) ** np.arange(n), [0.0]])[None, :]
+    r = linprog(np.r_[np.zeros(n), 1.0], A_ub=A, b_ub=b, A_eq=Aeq, b_eq=[1.0], bounds=[(None, None)] * (n + 1),
+                method="highs")
+    return r.x[:n]
 
 
-def approx(coef, a, x):
-    t = x * x
-    tc = np.minimum(t, a * a)
-    R = np.zeros_like(x)
-    for ck in coef[::-1]:
-        R = R * tc + ck
-    return x + np.minimum(t * R, np.abs(x))
+def h_exact(x):
+    return x * (1.0 + erf(x / np.sqrt(2.0)))
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--n", type=int, default=6)
-    ap.add_argument("--a", type=float, default=3.4)
+    ap.add_argument("--n", type=int, default=7)
+    ap.add_argument("--a", type=float, default=3.9)
     args = ap.parse_args()
-    coef, eps = fit(args.n, args.a)
-    x = np.linspace(-12, 12, 480001)
-    h = x + e_true(x)
-    err = np.abs(approx(coef.astype(np.float32).astype(np.float64), args.a, x) - h)
-    print(f"n={args.n} a={args.a} weighted minimax eps={eps:.3e}  max|dh'|={err.max():.3e}  "
-          f"max|dh'|/max(|h'|,0.05)={np.max(err / np.maximum(np.abs(h), 0.05)):.3e}")
-    print("coefficients (R(t) = sum c_k t^k):")
-    print(", ".join(f"{float(np.float32(c)):.9e}f" for c in coef))
+    xs = np.linspace(0.0, 9.0, 18001)
+    c = fit_mufu(xs).astype(np.float32)
+    x = np.linspace(-12, 12, 960001).astype(np.float32)
+    xd = x.astype(np.float64)
+    hm = xd * (1 + s_mufu(c.astype(np.float64), xd))
+    print(f"MUFU form  max|dh'| = {np.abs(hm - h_exact(xd)).max():.2e} (exact tanh)")
+    print("  kGF = {" + ", ".join(f"{v:.9e}f" for v in c) + "}")
+    p = fit_poly(args.n, args.a).astype(np.float32)
+    xc = np.clip(x, -args.a, args.a).astype(np.float32)
+    t = xc * xc
+    P = np.full_like(t, p[-1])
+    for ck in p[-2::-1]:
+        P = (P * t + ck).astype(np.float32)
+    hp = (x * (xc * P) + x).astype(np.float32).astype(np.float64)
+    print(f"FMA form   n={args.n} a={args.a}  max|dh'| = {np.abs(hp - h_exact(xd)).max():.2e} (fp32 Horner)")
+    print("  kGP = {" + ", ".join(f"{v:.9e}f" for v in p) + "}")
+    tanh_std = xd * (1 + np.tanh(0.7978845608 * xd * (1 + 0.044715 * xd * xd)))
+    print(f"classic tanh form max|dh'| = {np.abs(tanh_std - h_exact(xd)).max():.2e}")
 
 
 if __name__ == "__main__":
