@@ -383,6 +383,17 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ bool mbar_test_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // kind::f16, D fp32, M = 256 (pair), N = 128.
 template <int F16>
 constexpr uint32_t idesc2() {
@@ -410,7 +421,7 @@ struct Smem2 {
   uint8_t* W;      // [nh][18 KB]: this CTA's 64-row half + bias block
   uint8_t* A;      // [4][32 KB]
   uint8_t* ones;   // 4 KB
-  float* zbuf;     // [4][4][128]
+  float* zbuf;     // [4][4][128] (L0 = 0) / [4] x 2 KB layer-0 B blocks (L0 = 1)
   float* w2;       // [2][128]
   float* wo;       // [128]
   uint64_t* bars;  // a_full[4] (used in the even CTA), d_full[4]
@@ -435,7 +446,42 @@ size_t smem_bytes2(int n_hidden) {
          16 * kSlots2 + 16;
 }
 
-template <int GELU, int F16>
+// Layer-0 B block (L0 = 1): this CTA's 64 output features (rows) x K = 16,
+// SWIZZLE_NONE K-major (8-row x 16-byte core matrices, LBO 128 B, SBO 256 B).
+// K columns: 0-5 z_hi of the pair tile's <= 6 subdomains, 6-11 z_lo, 12/13
+// W2[:,0] hi/lo, 14/15 W2[:,1] hi/lo.  The A block (128 rows x K = 16, same
+// layout, in the first 4 KB of the slot's A image) holds the one-hot subdomain
+// selector twice and the query coordinates (exact in 16 bit: multiples of 1/32)
+// twice, so one K = 16 MMA yields z[s] + W2 x_p (Eq. 5) to ~2^-17 relative.
+__device__ __forceinline__ uint32_t l0_off(int r, int k) {
+  return (uint32_t)((r >> 3) * 256 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
+}
+template <int F16>
+__device__ __forceinline__ void split16(float v, uint16_t& hi, uint16_t& lo) {
+  if constexpr (F16) {
+    const __half h = __float2half_rn(v);
+    hi = __half_as_ushort(h);
+    lo = __half_as_ushort(__float2half_rn(v - __half2float(h)));
+  } else {
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    hi = __bfloat16_as_ushort(h);
+    lo = __bfloat16_as_ushort(__float2bfloat16_rn(v - __bfloat162float(h)));
+  }
+}
+constexpr int kL0Sub = 6;   // subdomains a 256-row pair tile can touch (q >= 61)
+
+// MFP_TRACE builds: per-event clock64 stamps of CTAs 0/1 (DESIGN.md §6 timeline).
+#ifdef MFP_TRACE
+__device__ unsigned long long g_trace[2][18][32][8][4];   // [cta][warp][tile][layer][event]
+#define MFP_TR(w, jt, l, ev)                                                                      \
+  do {                                                                                            \
+    if (blockIdx.x < 2 && (jt) < 32 && (l) < 8) g_trace[blockIdx.x][w][jt][l][ev] = clock64(); \
+  } while (0)
+#else
+#define MFP_TR(w, jt, l, ev) do { } while (0)
+#endif
+
+template <int GELU, int F16, int L0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, Sink sink) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -456,6 +502,19 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       S.wo[i] = (GELU == 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
       S.w2[i] = __ldg(net.W2 + 2 * i);
       S.w2[kD + i] = __ldg(net.W2 + 2 * i + 1);
+    }
+    if constexpr (L0) {
+      for (int i = threadIdx.x; i < kSlots2 * 64; i += kThreads2) {
+        const int sl = i >> 6, nl = i & 63, n = 64 * (int)rank + nl;
+        uint8_t* blk = reinterpret_cast<uint8_t*>(S.zbuf) + sl * 2048;
+        uint16_t h, lo;
+        split16<F16>(__ldg(net.W2 + 2 * n), h, lo);
+        *reinterpret_cast<uint16_t*>(blk + l0_off(nl, 12)) = h;
+        *reinterpret_cast<uint16_t*>(blk + l0_off(nl, 13)) = lo;
+        split16<F16>(__ldg(net.W2 + 2 * n + 1), h, lo);
+        *reinterpret_cast<uint16_t*>(blk + l0_off(nl, 14)) = h;
+        *reinterpret_cast<uint16_t*>(blk + l0_off(nl, 15)) = lo;
+      }
     }
     if (threadIdx.x < kRows) {
       const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
@@ -494,27 +553,58 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
     if (rank == 0 && lane == 0) {
       uint32_t pa[kSlots2] = {0u, 0u, 0u, 0u};
       const uint32_t ones_addr = smem_u32(S.ones);
+      // layer ll of the slot-s tile: the split-layer K = 16 step (L0) or hidden W_l (+ bias step)
+      auto issue = [&](int s, int ll, int64_t jt) {
+        MFP_TR(0, jt, ll, 0);
+        pa[s] ^= 1u;
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(s * kD);
+        if (L0 && ll == 0) {
+          mma2<F16>(d, nosw_desc(smem_u32(S.A + s * kTile)),
+                    nosw_desc(smem_u32(reinterpret_cast<uint8_t*>(S.zbuf) + s * 2048)), 0u);
+        } else {
+          const int l = ll - L0;
+          const uint32_t a0 = smem_u32(S.A + s * kTile), b0 = smem_u32(S.W + l * kHalf);
+#pragma unroll
+          for (int k = 0; k < kD / 16; k++) {
+            const uint32_t offa = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
+            const uint32_t offb = (uint32_t)((k >> 2) * 8192 + (k & 3) * 32);
+            mma2<F16>(d, sw128_desc(a0 + offa), sw128_desc(b0 + offb), k > 0 ? 1u : 0u);
+          }
+          mma2<F16>(d, nosw_desc(ones_addr), nosw_desc(b0 + 16384u), 1u);   // bias step
+        }
+        commit2(&S.bars[kSlots2 + s]);
+        MFP_TR(0, jt, ll, 1);
+      };
+#ifdef MFP_OOO_ISSUE
+      // out-of-order: serve whichever slot's operands are complete first
+      int64_t jt[kSlots2];
+      int lls[kSlots2];
+      for (int s = 0; s < kSlots2; s++) { jt[s] = s; lls[s] = 0; }
+      for (;;) {
+        bool any = false;
+#pragma unroll 1
+        for (int s = 0; s < kSlots2; s++) {
+          if (jt[s] >= nloc) continue;
+          any = true;
+          if (!mbar_test_cluster(&S.bars[s], pa[s])) continue;
+          issue(s, lls[s], jt[s]);
+          if (++lls[s] == nh + L0) { lls[s] = 0; jt[s] += kSlots2; }
+        }
+        if (!any) break;
+      }
+#else
       for (int64_t j0 = 0; j0 < nloc; j0 += kSlots2) {
-        for (int l = 0; l < nh; l++) {
+        for (int ll = 0; ll < nh + L0; ll++) {
 #pragma unroll
           for (int s = 0; s < kSlots2; s++) {
             if (j0 + s >= nloc) continue;
             mbar_wait_cluster(&S.bars[s], pa[s]);
-            pa[s] ^= 1u;
-            tc_fence_after();
-            const uint32_t a0 = smem_u32(S.A + s * kTile), b0 = smem_u32(S.W + l * kHalf);
-            const uint32_t d = tmem + (uint32_t)(s * kD);
-#pragma unroll
-            for (int k = 0; k < kD / 16; k++) {
-              const uint32_t offa = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
-              const uint32_t offb = (uint32_t)((k >> 2) * 8192 + (k & 3) * 32);
-              mma2<F16>(d, sw128_desc(a0 + offa), sw128_desc(b0 + offb), k > 0 ? 1u : 0u);
-            }
-            mma2<F16>(d, nosw_desc(ones_addr), nosw_desc(b0 + 16384u), 1u);   // bias step
-            commit2(&S.bars[kSlots2 + s]);
+            issue(s, ll, j0 + s);
           }
         }
       }
+#endif
     }
     __syncwarp();
   } else if (warp >= 2) {
@@ -539,16 +629,39 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(&S.bars[slot], 0u);
     };
-    if (slot < nloc) *reinterpret_cast<float4*>(zb + zi) = z_fetch(slot);
+    // L0 = 1: thread tid_s moves 3 of the tile's 6 x 64 z values (this CTA's feature half)
+    auto rowp_of = [&](int64_t j) -> int64_t { return (cid + j * ncl) * (2 * kRows); };
+    auto z3_fetch = [&](int64_t j, float (&zv)[3]) {
+      const int64_t sf = rowp_of(j) / q;
+#pragma unroll
+      for (int i = 0; i < 3; i++) {
+        const int idx = tid_s + 128 * i;
+        int64_t sidx = sf + (idx >> 6);
+        if (sidx > nsub - 1) sidx = nsub - 1;
+        zv[i] = __ldg(z + sidx * kD + 64 * rank + (idx & 63));
+      }
+    };
+    float z3[3] = {0.f, 0.f, 0.f};
+    uint8_t* const b0blk = reinterpret_cast<uint8_t*>(S.zbuf) + slot * 2048;
+    if constexpr (L0) {
+      if (slot < nloc) z3_fetch(slot, z3);
+    } else {
+      if (slot < nloc) *reinterpret_cast<float4*>(zb + zi) = z_fetch(slot);
+    }
     uint32_t pd = 0u;
     for (int64_t j = slot; j < nloc; j += kSlots2) {
+      if (lane == 0) MFP_TR(warp, j, 0, 3);
       const int64_t row0 = row0_of(j);
-      int64_t s_first = row0 / q;
+      int64_t s_first = (L0 ? rowp_of(j) : row0) / q;
       if (s_first > nsub - 1) s_first = nsub - 1;
-      named_sync(1 + slot, 128);
+      if constexpr (!L0) named_sync(1 + slot, 128);
       const bool have_next = j + kSlots2 < nloc;
       float4 znext = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (have_next) znext = z_fetch(j + kSlots2);
+      float z3n[3] = {0.f, 0.f, 0.f};
+      if (have_next) {
+        if constexpr (L0) z3_fetch(j + kSlots2, z3n);
+        else znext = z_fetch(j + kSlots2);
+      }
       const int64_t grow = row0 + row;
       const bool valid = grow < total_rows;
       const int64_t gr = valid ? grow : total_rows - 1;
@@ -556,7 +669,34 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       const int p = (int)(gr - sidx * q);
       float qx, qy;
       query_xy(q, p, &qx, &qy);
-      {
+      if constexpr (L0) {
+        // z hi/lo columns of the B block, then this row's A row (one-hot x2, qx x2, qy x2)
+#pragma unroll
+        for (int i = 0; i < 3; i++) {
+          const int idx = tid_s + 128 * i, jj = idx >> 6, nl = idx & 63;
+          uint16_t h, lo;
+          split16<F16>(z3[i], h, lo);
+          *reinterpret_cast<uint16_t*>(b0blk + l0_off(nl, jj)) = h;
+          *reinterpret_cast<uint16_t*>(b0blk + l0_off(nl, kL0Sub + jj)) = lo;
+        }
+        int zo = (int)(sidx - s_first);
+        if (zo < 0 || zo >= kL0Sub) zo = 0;   // rows past the end of the batch (not stored)
+        const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
+        uint32_t wd[8];
+#pragma unroll
+        for (int w = 0; w < 6; w++) {
+          const int k0 = 2 * w, k1 = 2 * w + 1;
+          wd[w] = ((k0 == zo || k0 == zo + kL0Sub) ? one : 0u) | (((k1 == zo || k1 == zo + kL0Sub) ? one : 0u) << 16);
+        }
+        uint16_t qh, ql;
+        split16<F16>(qx, qh, ql);
+        wd[6] = (uint32_t)qh | ((uint32_t)qh << 16);
+        split16<F16>(qy, qh, ql);
+        wd[7] = (uint32_t)qh | ((uint32_t)qh << 16);
+        const uint32_t ab = a_base + l0_off(row, 0);
+        st_shared_v4(ab, wd[0], wd[1], wd[2], wd[3]);
+        st_shared_v4(ab + 128, wd[4], wd[5], wd[6], wd[7]);
+      } else {
         int zo = (int)(sidx - s_first);
         if (zo < 0 || zo >= kZRows) zo = 0;   // rows past the end of the batch (not stored)
         const float* zr = zb + zo * kD;
@@ -582,12 +722,14 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       }
       fence_proxy_async();
       arrive_a();
+      if (lane == 0) MFP_TR(warp, j, 0, 0);
       f2 yacc = f2_make(0.f, 0.f);
-      for (int l = 0; l < nh; l++) {
+      for (int l = 0; l < nh + L0; l++) {
         mbar_wait(&S.bars[kSlots2 + slot], pd);
+        if (lane == 0) MFP_TR(warp, j, l, 1);
         pd ^= 1u;
         tc_fence_after();
-        const bool last = (l == nh - 1);
+        const bool last = (l == nh + L0 - 1);
 #pragma unroll 1
         for (int ch = 0; ch < kD / 32; ch++) {
           uint32_t r[32];
@@ -614,9 +756,15 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
         if (!last) {
           fence_proxy_async();
           arrive_a();
+          if (lane == 0) MFP_TR(warp, j, l + 1, 0);
         }
       }
-      if (have_next) *reinterpret_cast<float4*>(zb + zi) = znext;
+      if constexpr (L0) {
+#pragma unroll
+        for (int i = 0; i < 3; i++) z3[i] = z3n[i];
+      } else {
+        if (have_next) *reinterpret_cast<float4*>(zb + zi) = znext;
+      }
       float y0, y1;
       f2_split(yacc, y0, y1);
       if (valid) sink_store(sink, sidx, p, (y0 + y1) + bo);
@@ -635,6 +783,13 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
 
 bool chain_tc_available() { return true; }
 
+#ifdef MFP_TRACE
+extern "C" int mfp_debug_trace(void* host, size_t bytes) {
+  const size_t n = bytes < sizeof(tc2::g_trace) ? bytes : sizeof(tc2::g_trace);
+  return cudaMemcpyFromSymbol(host, tc2::g_trace, n) == cudaSuccess ? (int)n : -1;
+}
+#endif
+
 // Variant: 2 = CTA pair (default), 1 = single-CTA 3-slot kernel (MFP_CHAIN_VARIANT=1,
 // kept for A/B measurement).
 static int chain_variant() {
@@ -649,10 +804,14 @@ static int chain_variant() {
 // Opt-in shared-memory sizes, set once from mfp_init (never inside a graph capture).
 void tc_kernel_attributes() {
   const int mx2 = (int)tc2::smem_bytes2(kMaxHidden);
-  cudaFuncSetAttribute(tc2::k_chain_tc2<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
-  cudaFuncSetAttribute(tc2::k_chain_tc2<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
-  cudaFuncSetAttribute(tc2::k_chain_tc2<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
-  cudaFuncSetAttribute(tc2::k_chain_tc2<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<0, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<0, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<0, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<0, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<1, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<1, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<1, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<1, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
   const int mx = (int)tc::smem_bytes(kMaxHidden);
   cudaFuncSetAttribute(tc::k_chain_tc<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(tc::k_chain_tc<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
@@ -669,13 +828,17 @@ void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const 
     const int64_t ptiles = (rows + 2 * tc::kRows - 1) / (2 * tc::kRows);
     const int64_t pairs = num_sms / 2;
     const int grid = 2 * (int)(ptiles < pairs ? ptiles : pairs);
+    // MFP_L0_SIMT=1: split layer z + W2 x_p on the CUDA cores (A/B), else one K = 16 MMA
+    static const int l0 = (getenv("MFP_L0_SIMT") && getenv("MFP_L0_SIMT")[0] == '1') ? 0 : 1;
+#define MFP_TC2(G, F, L) tc2::k_chain_tc2<G, F, L><<<grid, tc2::kThreads2, sm, s>>>(z, rows, q, net, sink)
+#define MFP_TC2L(G, F) do { if (l0) MFP_TC2(G, F, 1); else MFP_TC2(G, F, 0); } while (0)
     if (net.f16) {
-      if (net.gelu_tanh) tc2::k_chain_tc2<1, 1><<<grid, tc2::kThreads2, sm, s>>>(z, rows, q, net, sink);
-      else tc2::k_chain_tc2<0, 1><<<grid, tc2::kThreads2, sm, s>>>(z, rows, q, net, sink);
+      if (net.gelu_tanh) MFP_TC2L(1, 1); else MFP_TC2L(0, 1);
     } else {
-      if (net.gelu_tanh) tc2::k_chain_tc2<1, 0><<<grid, tc2::kThreads2, sm, s>>>(z, rows, q, net, sink);
-      else tc2::k_chain_tc2<0, 0><<<grid, tc2::kThreads2, sm, s>>>(z, rows, q, net, sink);
+      if (net.gelu_tanh) MFP_TC2L(1, 0); else MFP_TC2L(0, 0);
     }
+#undef MFP_TC2L
+#undef MFP_TC2
     return;
   }
   const size_t sm = tc::smem_bytes(net.n_hidden);
