@@ -21,8 +21,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // Blocking wait on an mbarrier phase.  Default: try_wait with a suspend-time
 // hint (the SASS loop carries a NANOSLEEP); MFP_WAIT_SPIN builds a plain
 // try_wait loop (hardware-defined blocking window) for A/B measurement.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#ifdef MFP_WAIT_SPIN
+#if defined(MFP_WAIT_NS)
+  // poll with an explicit back-off: a waiting warp issues ~3 instructions per
+  // MFP_WAIT_NS ns instead of a tight try_wait loop
+  while (!mbar_test(bar, parity)) __nanosleep(MFP_WAIT_NS);
+#elif defined(MFP_WAIT_SPIN)
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
@@ -115,6 +120,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+// tcgen05.wait::ld that also pins the registers of the load it completes, so
+// the compiler cannot hoist their uses above the wait (double-buffered loads:
+// issue ld(c + 1), work on chunk c, then wait with chunk c + 1's registers).
+__device__ __forceinline__ void tmem_wait_ld_dep16(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15])
+               :
+               : "memory");
+}
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)

@@ -34,11 +34,11 @@ t0 = T[T > 0].min()
 T = np.where(T > 0, T - t0, -1)
 for tile in range(12):
     slot = tile % 4
-    warps = [2 + 4 * slot + q for q in range(4)]
+    warps = [4 * slot + q for q in range(4)]
     line = [f"tile {tile:2d} slot {slot}"]
     for l in range(4):
         arr = [T[w_, tile, l, 0] for w_ in warps]
         wake = [T[w_, tile, l, 1] for w_ in warps]
-        iss = T[0, tile, l, 0], T[0, tile, l, 1]
+        iss = T[17, tile, l, 0], T[17, tile, l, 1]
         line.append(f"L{l}: arr {min(arr)}..{max(arr)} iss {iss[0]}/{iss[1]} wake {min(wake)}..{max(wake)}")
     print(" | ".join(line))
