@@ -378,31 +378,46 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Cross-CTA handshakes use the default (.cta) scope, as CUTLASS's cluster
+// barriers do: .release.cluster / .acquire.cluster compile to MEMBAR.ALL.GPU
+// (waits for every outstanding global load/store of the arriving thread, e.g.
+// the next tile's z prefetch and the scatter stores) and CCTL.IVALL (an L1
+// invalidate per wait) — measured as ~750-cycle stalls on the MMA issue path.
+// Operand visibility to the tensor core is established by fence.proxy.async
+// before the arrive (MFP_CLUSTER_SCOPE=1 builds the cluster-scoped variant).
 __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+#ifdef MFP_CLUSTER_SCOPE
   asm volatile(
       "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
       "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
       "r"(cta)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+#ifdef MFP_CLUSTER_SCOPE
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAITC_%=:\n\t"
-#ifdef MFP_WAIT_SPIN
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-#else
       "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
-#endif
       "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#else
+  mbar_wait(bar, parity);
+#endif
 }
 __device__ __forceinline__ bool mbar_test_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
@@ -674,6 +689,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       int64_t s_first = (L0 ? rowp_of(j) : row0) / q;
       if (s_first > nsub - 1) s_first = nsub - 1;
       if constexpr (!L0) named_sync(1 + slot, 128);
+      if (lane == 0) MFP_TR(warp, j, 2, 3);
       const bool have_next = j + kSlots2 < nloc;
       float4 znext = make_float4(0.f, 0.f, 0.f, 0.f);
       float z3n[3] = {0.f, 0.f, 0.f};
@@ -739,6 +755,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
           st_shared_v4(a_row + ((uint32_t)(cc >> 3) << 14) + ((uint32_t)((cc & 7) ^ r7) << 4), w[0], w[1], w[2], w[3]);
         }
       }
+      if (lane == 0) MFP_TR(warp, j, 1, 3);
       fence_proxy_async();
       arrive_a();
       if (lane == 0) MFP_TR(warp, j, 0, 0);
@@ -787,6 +804,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
           work16(rb, c16 + 1);
           if (c16 + 2 < kD / 16) tmem_wait_ld_dep16(ra);
         }
+        if (lane == 0) MFP_TR(warp, j, l, 2);
 #ifdef MFP_EXPERIMENT_NO_TMEM_LD
 #undef tmem_ld16
 #endif
@@ -819,6 +837,266 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
 
 }  // namespace tc2
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant with 8 epilogue warps per slot (tc3): 3 slots x 8 warps,
+// two warps per TMEM lane quadrant splitting the 128 columns (64 each).  The
+// chain epilogue is latency bound at 4 warps per SMSP (removing
+// MUFU, TMEM loads or the smem stores one at a time barely moves it), so this
+// trades one tile slot for 1.5x the warps (6 per SMSP) at 72 registers.
+namespace tc3 {
+using namespace tc;
+using tc2::cluster_rank;
+using tc2::cluster_sync;
+using tc2::mbar_arrive_remote;
+using tc2::mbar_wait_cluster;
+using tc2::mma2;
+using tc2::commit2;
+
+constexpr int kSlots3 = 3;
+constexpr int kEpi3 = 8 * kSlots3;                 // 24 epilogue warps
+constexpr int kAlloc3 = kEpi3, kIssue3 = kEpi3 + 1;  // issuer: highest warp id
+constexpr int kThreads3 = 32 * (kEpi3 + 2);        // 832
+constexpr int kHalf3 = kWImg;
+
+struct Smem3 {
+  uint8_t* W;      // [nh][18 KB]
+  uint8_t* A;      // [3][32 KB]
+  uint8_t* ones;   // 4 KB
+  float* zbuf;     // [3][4][128]
+  float* w2;       // [2][128]
+  float* wo;       // [128]
+  float* ypart;    // [3][128] head partial sums of the upper column half
+  uint64_t* bars;  // a_full[3], d_full[3]
+  uint32_t* tmem_slot;
+};
+
+__device__ __forceinline__ Smem3 carve3(uint8_t* raw, int nh) {
+  Smem3 s;
+  s.W = raw;
+  s.A = raw + nh * kHalf3;
+  s.ones = s.A + kSlots3 * kTile;
+  s.zbuf = (float*)(s.ones + kOnes);
+  s.w2 = s.zbuf + kSlots3 * kZRows * kD;
+  s.wo = s.w2 + 2 * kD;
+  s.ypart = s.wo + kD;
+  s.bars = (uint64_t*)(s.ypart + kSlots3 * kD);
+  s.tmem_slot = (uint32_t*)(s.bars + 2 * kSlots3);
+  return s;
+}
+
+size_t smem_bytes3(int n_hidden) {
+  return (size_t)n_hidden * kHalf3 + kSlots3 * kTile + kOnes +
+         4 * ((size_t)kSlots3 * kZRows * kD + 3 * kD + kSlots3 * kD) + 16 * kSlots3 + 16;
+}
+
+template <int GELU, int F16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads3, 1)
+k_chain_tc3(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, Sink sink) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int nh = net.n_hidden;
+  const Smem3 S = carve3(smem_raw, nh);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+
+  {
+    for (int l = 0; l < nh; l++) {
+      const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(net.Wh_sw2) +
+                                                        (size_t)l * 2 * kHalf3 + rank * kHalf3);
+      uint4* dst = reinterpret_cast<uint4*>(S.W + l * kHalf3);
+      for (int i = threadIdx.x; i < kHalf3 / 16; i += kThreads3) dst[i] = __ldg(src + i);
+    }
+    for (int i = threadIdx.x; i < kD; i += kThreads3) {
+      S.wo[i] = (GELU == 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
+      S.w2[i] = __ldg(net.W2 + 2 * i);
+      S.w2[kD + i] = __ldg(net.W2 + 2 * i + 1);
+    }
+    if (threadIdx.x < kRows) {
+      const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
+      const int r = threadIdx.x;
+      *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + (r & 7) * 16) = make_uint4(one | (one << 16), 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + 128 + (r & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSlots3; s++) {
+      mbar_init(&S.bars[s], 16);            // a_full[s]: 8 warps x 2 CTAs
+      mbar_init(&S.bars[kSlots3 + s], 1);   // d_full[s]: multicast commit
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kAlloc3) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *S.tmem_slot;
+
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int64_t ntiles = (total_rows + 2 * kRows - 1) / (2 * kRows);
+  const int64_t nloc = ntiles > cid ? (ntiles - cid + ncl - 1) / ncl : 0;
+  const int64_t nsub = total_rows / q;
+
+  if (warp == kIssue3) {
+    if (rank == 0 && lane == 0) {
+      uint32_t pa[kSlots3] = {0u, 0u, 0u};
+      const uint32_t ones_addr = smem_u32(S.ones);
+      for (int64_t j0 = 0; j0 < nloc; j0 += kSlots3) {
+        for (int l = 0; l < nh; l++) {
+#pragma unroll
+          for (int s = 0; s < kSlots3; s++) {
+            if (j0 + s >= nloc) continue;
+            mbar_wait_cluster(&S.bars[s], pa[s]);
+            pa[s] ^= 1u;
+            tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)(s * kD);
+            const uint32_t a0 = smem_u32(S.A + s * kTile), b0 = smem_u32(S.W + l * kHalf3);
+#pragma unroll
+            for (int k = 0; k < kD / 16; k++) {
+              const uint32_t offa = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
+              const uint32_t offb = (uint32_t)((k >> 2) * 8192 + (k & 3) * 32);
+              mma2<F16>(d, sw128_desc(a0 + offa), sw128_desc(b0 + offb), k > 0 ? 1u : 0u);
+            }
+            mma2<F16>(d, nosw_desc(ones_addr), nosw_desc(b0 + 16384u), 1u);
+            commit2(&S.bars[kSlots3 + s]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp < kEpi3) {
+    const int slot = warp >> 3;
+    const int half = (warp >> 2) & 1;               // column half: 64 half .. 64 half + 63
+    const int quad = warp & 3;                      // TMEM lane quadrant
+    const int row = quad * 32 + lane;
+    const int tid8 = (half * 4 + quad) * 32 + lane;  // 0..255 within the slot
+    const uint32_t a_row = smem_u32(S.A + slot * kTile) + (uint32_t)row * 128u;
+    const int r7 = row & 7;
+    const uint32_t t_row = tmem + (uint32_t)(slot * kD + 64 * half) + ((uint32_t)(quad * 32) << 16);
+    float* zb = S.zbuf + slot * kZRows * kD;
+    const float bo = __ldg(net.bo);
+    const int zi = 2 * tid8, zr_ = zi >> 7, zc = zi & 127;
+    auto row0_of = [&](int64_t j) -> int64_t { return (cid + j * ncl) * (2 * kRows) + rank * kRows; };
+    auto z_fetch = [&](int64_t j) -> float2 {
+      int64_t sidx = row0_of(j) / q + zr_;
+      if (sidx > nsub - 1) sidx = nsub - 1;
+      return __ldg(reinterpret_cast<const float2*>(z + sidx * kD + zc));
+    };
+    auto arrive_a = [&]() {
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&S.bars[slot], 0u);
+    };
+    auto store8 = [&](int g, const uint32_t (&w)[4]) {   // 8-column group g of this row
+      st_shared_v4(a_row + ((uint32_t)(g >> 3) << 14) + ((uint32_t)((g & 7) ^ r7) << 4), w[0], w[1], w[2], w[3]);
+    };
+    if (slot < nloc) *reinterpret_cast<float2*>(zb + zi) = z_fetch(slot);
+    uint32_t pd = 0u;
+    for (int64_t j = slot; j < nloc; j += kSlots3) {
+      const int64_t row0 = row0_of(j);
+      int64_t s_first = row0 / q;
+      if (s_first > nsub - 1) s_first = nsub - 1;
+      named_sync(1 + slot, 256);                    // zbuf of this tile visible to the slot's 8 warps
+      const bool have_next = j + kSlots3 < nloc;
+      float2 znext = make_float2(0.f, 0.f);
+      if (have_next) znext = z_fetch(j + kSlots3);
+      const int64_t grow = row0 + row;
+      const bool valid = grow < total_rows;
+      const int64_t gr = valid ? grow : total_rows - 1;
+      const int64_t sidx = gr / q;
+      const int p = (int)(gr - sidx * q);
+      float qx, qy;
+      query_xy(q, p, &qx, &qy);
+      {
+        int zo = (int)(sidx - s_first);
+        if (zo < 0 || zo >= kZRows) zo = 0;
+        const float* zr = zb + zo * kD;
+        const f2 QX = f2_make(qx, qx), QY = f2_make(qy, qy);
+#pragma unroll 2
+        for (int i = 0; i < 8; i++) {
+          const int cc = 8 * half + i;
+          const float4 z0 = *reinterpret_cast<const float4*>(zr + cc * 8);
+          const float4 z1 = *reinterpret_cast<const float4*>(zr + cc * 8 + 4);
+          const float4 a0 = *reinterpret_cast<const float4*>(S.w2 + cc * 8);
+          const float4 a1 = *reinterpret_cast<const float4*>(S.w2 + cc * 8 + 4);
+          const float4 b0 = *reinterpret_cast<const float4*>(S.w2 + kD + cc * 8);
+          const float4 b1 = *reinterpret_cast<const float4*>(S.w2 + kD + cc * 8 + 4);
+          float v[8];
+          f2_split(ffma2(f2_make(a0.x, a0.y), QX, ffma2(f2_make(b0.x, b0.y), QY, f2_make(z0.x, z0.y))), v[0], v[1]);
+          f2_split(ffma2(f2_make(a0.z, a0.w), QX, ffma2(f2_make(b0.z, b0.w), QY, f2_make(z0.z, z0.w))), v[2], v[3]);
+          f2_split(ffma2(f2_make(a1.x, a1.y), QX, ffma2(f2_make(b1.x, b1.y), QY, f2_make(z1.x, z1.y))), v[4], v[5]);
+          f2_split(ffma2(f2_make(a1.z, a1.w), QX, ffma2(f2_make(b1.z, b1.w), QY, f2_make(z1.z, z1.w))), v[6], v[7]);
+          uint32_t w[4];
+          act8<GELU, F16>(v, w);
+          store8(cc, w);
+        }
+      }
+      fence_proxy_async();
+      arrive_a();
+      f2 yacc = f2_make(0.f, 0.f);
+      for (int l = 0; l < nh; l++) {
+        mbar_wait(&S.bars[kSlots3 + slot], pd);
+        pd ^= 1u;
+        tc_fence_after();
+        const bool last = (l == nh - 1);
+        auto work16 = [&](const uint32_t (&r)[16], int c16) {
+          if (!last) {
+#pragma unroll
+            for (int c8 = 0; c8 < 2; c8++) {
+              float v[8];
+#pragma unroll
+              for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[c8 * 8 + e]);
+              uint32_t w[4];
+              act8<GELU, F16>(v, w);
+              store8(8 * half + 2 * c16 + c8, w);
+            }
+          } else {
+            head32<GELU, 16>(r, S.wo + 64 * half + c16 * 16, yacc);
+          }
+        };
+        uint32_t ra[16], rb[16];
+        tmem_ld16(t_row, ra);
+        tmem_wait_ld_dep16(ra);
+        tmem_ld16(t_row + 16u, rb);
+        work16(ra, 0);
+        tmem_wait_ld_dep16(rb);
+        tmem_ld16(t_row + 32u, ra);
+        work16(rb, 1);
+        tmem_wait_ld_dep16(ra);
+        tmem_ld16(t_row + 48u, rb);
+        work16(ra, 2);
+        tmem_wait_ld_dep16(rb);
+        work16(rb, 3);
+        tc_fence_before();
+        if (!last) {
+          fence_proxy_async();
+          arrive_a();
+        }
+      }
+      if (have_next) *reinterpret_cast<float2*>(zb + zi) = znext;
+      float y0, y1;
+      f2_split(yacc, y0, y1);
+      if (half) S.ypart[slot * kD + row] = y0 + y1;
+      named_sync(4 + slot, 256);                    // upper-half partial sums visible
+      if (!half && valid) sink_store(sink, sidx, p, ((y0 + y1) + S.ypart[slot * kD + row]) + bo);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == kAlloc3) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  }
+}
+
+}  // namespace tc3
+
 bool chain_tc_available() { return true; }
 
 #ifdef MFP_TRACE
@@ -834,13 +1112,18 @@ static int chain_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("MFP_CHAIN_VARIANT");
-    v = (e && e[0] == '1') ? 1 : 2;
+    v = (e && (e[0] == '1' || e[0] == '3')) ? e[0] - '0' : 2;
   }
   return v;
 }
 
 // Opt-in shared-memory sizes, set once from mfp_init (never inside a graph capture).
 void tc_kernel_attributes() {
+  const int mx3 = (int)tc3::smem_bytes3(kMaxHidden);
+  cudaFuncSetAttribute(tc3::k_chain_tc3<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx3);
+  cudaFuncSetAttribute(tc3::k_chain_tc3<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx3);
+  cudaFuncSetAttribute(tc3::k_chain_tc3<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx3);
+  cudaFuncSetAttribute(tc3::k_chain_tc3<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx3);
   const int mx2 = (int)tc2::smem_bytes2(kMaxHidden);
   cudaFuncSetAttribute(tc2::k_chain_tc2<0, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
   cudaFuncSetAttribute(tc2::k_chain_tc2<0, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
@@ -861,6 +1144,20 @@ void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const 
                      cudaStream_t s) {
   if (B <= 0) return;
   const int64_t rows = B * q;
+  if (chain_variant() == 3) {
+    const size_t sm = tc3::smem_bytes3(net.n_hidden);
+    const int64_t ptiles = (rows + 2 * tc::kRows - 1) / (2 * tc::kRows);
+    const int64_t pairs = num_sms / 2;
+    const int grid = 2 * (int)(ptiles < pairs ? ptiles : pairs);
+#define MFP_TC3(G, F) tc3::k_chain_tc3<G, F><<<grid, tc3::kThreads3, sm, s>>>(z, rows, q, net, sink)
+    if (net.f16) {
+      if (net.gelu_tanh) MFP_TC3(1, 1); else MFP_TC3(0, 1);
+    } else {
+      if (net.gelu_tanh) MFP_TC3(1, 0); else MFP_TC3(0, 0);
+    }
+#undef MFP_TC3
+    return;
+  }
   if (chain_variant() == 2) {
     const size_t sm = tc2::smem_bytes2(net.n_hidden);
     const int64_t ptiles = (rows + 2 * tc::kRows - 1) / (2 * tc::kRows);

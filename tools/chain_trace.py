@@ -30,15 +30,39 @@ f.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 assert f(buf.ctypes.data, buf.nbytes) > 0
 np.save("gpurun_out/chain_trace.npy", buf)
 T = buf[0].astype(np.int64)
-t0 = T[T > 0].min()
-T = np.where(T > 0, T - t0, -1)
-for tile in range(12):
+acts, rts, iss, exe, comp, fin, l0, l0s, tails = [], [], [], [], [], [], [], [], []
+L = 3   # layers with an MMA (L0 SIMT default); MFP_L0_MMA=1 -> 4
+if (T[17, 5, 3, 0] > 0):
+    L = 4
+for tile in range(4, 28):
     slot = tile % 4
-    warps = [4 * slot + q for q in range(4)]
-    line = [f"tile {tile:2d} slot {slot}"]
-    for l in range(4):
-        arr = [T[w_, tile, l, 0] for w_ in warps]
-        wake = [T[w_, tile, l, 1] for w_ in warps]
-        iss = T[17, tile, l, 0], T[17, tile, l, 1]
-        line.append(f"L{l}: arr {min(arr)}..{max(arr)} iss {iss[0]}/{iss[1]} wake {min(wake)}..{max(wake)}")
-    print(" | ".join(line))
+    ws = [4 * slot + q for q in range(4)]
+    g = lambda l, ev, f: f(T[w, tile, l, ev] for w in ws)
+    for l in range(L):
+        arr, wake = g(l, 0, max), g(l, 1, max)
+        if arr <= 0 or wake <= 0:
+            continue
+        rts.append(wake - arr)
+        iw, ic = T[17, tile, l, 0], T[17, tile, l, 1]
+        if iw > 0:
+            iss.append(iw - arr)
+            exe.append(ic - iw)
+        if l < L - 1:
+            a2 = g(l + 1, 0, max)
+            e2 = g(l, 2, max)
+            if a2 > 0 and e2 > 0:
+                acts.append(a2 - g(l, 1, min))
+                comp.append(e2 - g(l, 1, min))
+                fin.append(a2 - e2)
+    st, ns, ea = g(0, 3, min), g(2, 3, max), g(1, 3, max)
+    if st > 0 and ns > 0 and ea > 0:
+        l0s.append(ns - st)
+        l0.append(ea - ns)
+    if tile + 4 < 32:
+        nst = min(T[w, tile + 4, 0, 3] for w in ws)
+        if nst > 0:
+            tails.append(nst - g(L - 1, 1, max))
+m = lambda v: float(np.mean(v)) if v else -1
+print(f"layers {L}: act phase {m(acts):.0f} (compute {m(comp):.0f}, fence+arrive {m(fin):.0f}) | round trip {m(rts):.0f} "
+      f"(issuer wait after CTA0 arrivals {m(iss):.0f}, issue->commit {m(exe):.0f}) | L0: tile start->z sync {m(l0s):.0f}, "
+      f"sync->compute end {m(l0):.0f} | head+tail {m(tails):.0f}")
