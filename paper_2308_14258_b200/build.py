@@ -1,6 +1,6 @@
 """Build libmfp.so in-tree with nvcc for sm_100a (no torch types in the ABI).
 
-    python -m paper_2308_14258_b200.build [--force]
+    python paper_2308_14258_b200/build.py [--force]
 """
 from __future__ import annotations
 

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmfp.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"libmfp.so not built at {LIB_PATH}: run `python -m paper_2308_14258_b200.build`")
+    raise ImportError(f"libmfp.so not built at {LIB_PATH}: run `python paper_2308_14258_b200/build.py`")
 
 _lib = ctypes.CDLL(LIB_PATH)
 

@@ -4,7 +4,7 @@
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
-python -m paper_2308_14258_b200.build > gpurun_out/build.log 2>&1
+python paper_2308_14258_b200/build.py > gpurun_out/build.log 2>&1
 timeout 600 python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
 timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1
 tail -3 gpurun_out/gpu_tests.log

@@ -1,7 +1,7 @@
 for v in "" "-DMFP_EXPERIMENT_FAKE_TANH" "-DMFP_EXPERIMENT_NO_ACT"; do
-MFP_NVCC_EXTRA="$v" python -m paper_2308_14258_b200.build --force > gpurun_out/build.log 2>&1
+MFP_NVCC_EXTRA="$v" python paper_2308_14258_b200/build.py --force > gpurun_out/build.log 2>&1
 timeout 600 python bench.py --no-converge --steps 3 > gpurun_out/bench_x.json 2>> gpurun_out/bench.err
 python -c "
 import json,sys; d=json.loads(open('gpurun_out/bench_x.json').read().strip().splitlines()[-1]); print('variant [$v]', round(d['value']/1e6,2), d['roofline']['chain_ms_per_launch'])"
 done
-python -m paper_2308_14258_b200.build --force >> gpurun_out/build.log 2>&1
+python paper_2308_14258_b200/build.py --force >> gpurun_out/build.log 2>&1

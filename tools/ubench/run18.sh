@@ -1,4 +1,4 @@
-python -m paper_2308_14258_b200.build > gpurun_out/build.log 2>&1
+python paper_2308_14258_b200/build.py > gpurun_out/build.log 2>&1
 MFP_CHAIN_VARIANT=3 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/gpu_tests3.log 2>&1; tail -1 gpurun_out/gpu_tests3.log; grep -E "^E .*assert|FAILED|Error" gpurun_out/gpu_tests3.log | head -5
 MFP_CHAIN_VARIANT=3 timeout 600 python bench.py --no-converge --steps 5 > gpurun_out/bench3.json 2>> gpurun_out/bench.err
 timeout 600 python bench.py --no-converge --steps 5 > gpurun_out/bench.json 2>> gpurun_out/bench.err

@@ -1,4 +1,4 @@
-python -m paper_2308_14258_b200.build --force > gpurun_out/build.log 2>&1
+python paper_2308_14258_b200/build.py --force > gpurun_out/build.log 2>&1
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/gpu_tests.log 2>&1; tail -1 gpurun_out/gpu_tests.log; grep -E "^E .*assert|FAILED|Error" gpurun_out/gpu_tests.log | head -5
 MFP_CHAIN_VARIANT=3 timeout 900 python -m pytest tests -m gpu -q -x -k "tensorcore or batch or fitted" > gpurun_out/gpu_tests3.log 2>&1; tail -1 gpurun_out/gpu_tests3.log
 timeout 600 python bench.py --no-converge --steps 5 > gpurun_out/bench.json 2>> gpurun_out/bench.err

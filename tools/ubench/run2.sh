@@ -1,6 +1,6 @@
 set -x
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/pipes2 tools/ubench/pipes2.cu && /tmp/pipes2 > gpurun_out/pipes2.txt 2>&1
-python -m paper_2308_14258_b200.build > gpurun_out/build.log 2>&1
+python paper_2308_14258_b200/build.py > gpurun_out/build.log 2>&1
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log
 timeout 600 python bench.py --no-converge > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
 cat gpurun_out/pipes2.txt

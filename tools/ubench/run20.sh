@@ -1,5 +1,5 @@
-MFP_NVCC_EXTRA="-DMFP_TRACE" python -m paper_2308_14258_b200.build --force > gpurun_out/build.log 2>&1
+MFP_NVCC_EXTRA="-DMFP_TRACE" python paper_2308_14258_b200/build.py --force > gpurun_out/build.log 2>&1
 timeout 300 python tools/chain_trace.py > gpurun_out/trace.txt 2>&1; tail -3 gpurun_out/trace.txt
-MFP_NVCC_EXTRA="-DMFP_TRACE -DMFP_EXPERIMENT_NO_ACT" python -m paper_2308_14258_b200.build --force > gpurun_out/build.log 2>&1
+MFP_NVCC_EXTRA="-DMFP_TRACE -DMFP_EXPERIMENT_NO_ACT" python paper_2308_14258_b200/build.py --force > gpurun_out/build.log 2>&1
 timeout 300 python tools/chain_trace.py > gpurun_out/trace_noact.txt 2>&1; tail -3 gpurun_out/trace_noact.txt
-python -m paper_2308_14258_b200.build --force >> gpurun_out/build.log 2>&1
+python paper_2308_14258_b200/build.py --force >> gpurun_out/build.log 2>&1

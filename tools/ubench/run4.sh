@@ -1,4 +1,4 @@
-python -m paper_2308_14258_b200.build > gpurun_out/build.log 2>&1
+python paper_2308_14258_b200/build.py > gpurun_out/build.log 2>&1
 for np in 0 1 2; do for p in 1 2; do MFP_GELU_POLY=$np timeout 300 python tools/wfit_err.py $p; done; done > gpurun_out/wfit_err.txt 2>&1
 cat gpurun_out/wfit_err.txt
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log; grep -E "^E .*assert|FAILED" gpurun_out/gpu_tests.log | head

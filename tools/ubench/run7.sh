@@ -1,7 +1,7 @@
-python -m paper_2308_14258_b200.build --force > gpurun_out/build.log 2>&1
+python paper_2308_14258_b200/build.py --force > gpurun_out/build.log 2>&1
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; tail -2 gpurun_out/gpu_tests.log; grep -E "^E .*assert|FAILED" gpurun_out/gpu_tests.log | head
 timeout 600 python bench.py --no-converge --steps 5 > gpurun_out/bench.json 2>> gpurun_out/bench.err
-MFP_NVCC_EXTRA="-DMFP_WAIT_SPIN" python -m paper_2308_14258_b200.build --force >> gpurun_out/build.log 2>&1
+MFP_NVCC_EXTRA="-DMFP_WAIT_SPIN" python paper_2308_14258_b200/build.py --force >> gpurun_out/build.log 2>&1
 timeout 600 python bench.py --no-converge --steps 5 > gpurun_out/bench_spin.json 2>> gpurun_out/bench.err
 for f in gpurun_out/bench.json gpurun_out/bench_spin.json; do python -c "
 import json,sys; d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', round(d['value']/1e6,2), d['roofline']['chain_ms_per_launch'])"; done
