@@ -161,6 +161,85 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ boundary IO roofline
+IO_N = 16384   # 16385^2 grid: 134 MB line lattice + 134 MB batch, together > 126 MB L2
+
+
+def boundary_io_bench(mfp, torch, peaks, reps: int = 10, flush_l2: bool = True) -> dict:
+    """a1 gather and a6 scatter (+ a8 update-norm reduction) as standalone kernels
+    (mfp_gather_phase / mfp_scatter_phase) on a lattice larger than L2, phase 0
+    (262,144 subdomains), L2 flushed before every launch (outside the events):
+    achieved GB/s of ALGORITHMIC bytes vs the measured HBM copy bandwidth."""
+    from mfp_inputs import gp_boundary
+    stream = torch.cuda.Stream()
+    cfg = mfp.make_config(IO_N, IO_N, precision=mfp.FP32, subsolver=mfp.EXACT_LAPLACE, check_every=16)
+    m = mfp.Mfp(cfg, mfp.make_net(), None, stream=stream)
+    g = torch.from_numpy(gp_boundary(IO_N, IO_N, 0)).cuda()
+    m.solve_device(g, 1, 0.0, None)                  # a real lattice state (one exact iteration)
+    B, _ = mfp.mfp_gather_phase(m.ctx, 0, 0)
+    gb = torch.empty((B, 128), dtype=torch.float32, device="cuda")
+    pred = torch.randn((B, 61), dtype=torch.float32, device="cuda")
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+
+    def timed(fn):
+        ms = 0.0
+        for i in range(reps + 2):
+            if flush_l2:
+                with torch.cuda.stream(stream):
+                    flush.fill_(float(i))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            if i >= 2:
+                ms += e0.elapsed_time(e1)
+        return ms / reps
+
+    ms_g = timed(lambda: mfp.mfp_gather_phase(m.ctx, 0, 0, gb, B))
+    ms_s = timed(lambda: mfp.mfp_scatter_phase(m.ctx, 0, 0, pred, B, want_norm=False))
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    gbytes, sbytes = 128 * 4 * 2, 61 * 4 * 2 + 62 * 4   # per subdomain
+    out = {"workload": f"{IO_N + 1}^2 grid, phase 0 = {B} subdomains; lattice "
+                       f"{m.lines_bytes() / 1e6:.0f} MB (> L2), L2 flushed before each launch",
+           "peak_gbs": hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
+           "gather": {"kernel": "k_gather_phase (a1)", "us": 1000 * ms_g, "bytes_per_subdomain": gbytes,
+                      "note": "512 B perimeter read + 512 B batch write",
+                      "gbs": B * gbytes / (ms_g / 1000) / 1e9},
+           "scatter": {"kernel": "k_scatter_phase + k_reduce_max (a6 + a8)", "us": 1000 * ms_s,
+                       "bytes_per_subdomain": sbytes,
+                       "note": "244 B predictions + 244 B old values read, 248 B written (centre twice)",
+                       "gbs": B * sbytes / (ms_s / 1000) / 1e9}}
+    for k in ("gather", "scatter"):
+        out[k]["frac"] = out[k]["gbs"] / hbm
+    m.close()
+    del flush
+    return out
+
+
+def sdnet_batch_sweep(m, torch, stream, sizes=(1024, 2048, 4096, 8192, 16384, 32768, 65536), reps: int = 5):
+    """C3 row of BASELINE.json: batched SDNet inference throughput (mfp_sdnet_batch,
+    61 centre-line queries) over batch sizes; N(0,1) boundary vectors."""
+    from mfp_inputs import random_boundaries
+    out = []
+    for B in sizes:
+        gb = torch.from_numpy(random_boundaries(B, seed=7)).cuda()
+        y = torch.empty((B, 61), dtype=torch.float32, device="cuda")
+        torch.cuda.synchronize()
+        m.sdnet_batch(gb, out=y)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(m.stream)
+        for _ in range(reps):
+            m.sdnet_batch(gb, out=y)
+        e1.record(m.stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        out.append({"batch": B, "ms": ms, "predictions_per_s": B / (ms / 1000.0)})
+    return out
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
@@ -357,6 +436,10 @@ def main():
                         "including the final phase (the MAE needs the field); stop rule of P:179"}
             mf.close()
 
+    bio = sweep = None
+    if world == 1:
+        sweep = sdnet_batch_sweep(m, torch, stream)
+        bio = boundary_io_bench(mfp, torch, peaks)
     cpu = None
     if rank == 0 and world == 1:
         rate, n, dt, thr = cpu_oracle_rate()
@@ -369,7 +452,7 @@ def main():
                 "config": bench_config(T, grid, tensor),
                 "points_iter_per_s": (NX + 1) * (NY + 1) * T * args.steps / (ms / 1000.0),
                 "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
-                "time_to_converge": ttc, "clocks": clk.summary(),
+                "time_to_converge": ttc, "sdnet_batch_sweep": sweep, "boundary_io": bio, "clocks": clk.summary(),
                 "halo": {"bytes_per_iter_rank0": rep.halo_bytes_sent / max(rep.iterations, 1),
                          "msgs_per_iter": rep.halo_msgs_per_iter}}
         print(json.dumps(line), flush=True)

@@ -216,6 +216,33 @@ mfp_status mfp_solve_device(mfp_ctx* ctx, const float* g_dev, int32_t max_iters,
 mfp_status mfp_sdnet_batch(mfp_ctx* ctx, const float* gb, int64_t B,
                            int32_t query_set, float* out, void* stream);
 
+/* Standalone "Boundaries IO" of one phase — the unfused form of the
+ * solve's gather (fused there into the embed) and scatter (fused into the chain
+ * epilogue): mfp_gather_phase -> mfp_sdnet_batch -> mfp_scatter_phase is one
+ * phase of Algorithm 2.  `rank`: 0 for single-rank contexts, the rank
+ * index for MFP_ALL_RANKS contexts.  Both run asynchronously on the context
+ * stream unless a host result is requested.
+ *
+ * mfp_gather_phase (a1, P:23 / P:43): gb (DEVICE, cap x 4m fp32) receives the
+ * perimeter (G1 order) of every subdomain the rank computes in `phase` (0..3,
+ * G2 order), read from its current lattice; *B_out = their number (required
+ * rows).  ax_out / ay_out (HOST, cap int32 each, both or neither) receive the
+ * global lower-left anchors in row order — mfp_plan_anchors' order, except that
+ * with R > 1 phase 0 lists its phase0_interior subdomains first.  gb, ax_out and
+ * ay_out all NULL = size query.  INVALID if cap < B. */
+mfp_status mfp_gather_phase(mfp_ctx* ctx, int32_t rank, int32_t phase, float* gb, int64_t cap,
+                            int64_t* B_out, int32_t* ax_out, int32_t* ay_out);
+/* mfp_scatter_phase (a6 + a8, "the center lines of one subdomain are the
+ * boundary of another"): pred (DEVICE, B x 61 fp32, G3 order, rows in
+ * mfp_gather_phase's order; B must equal the phase's count) overwrite the
+ * centre-line cells of the rank's lattice (the centre point in both line
+ * arrays).  The kernel also reduces the update norm max |new - old| over the
+ * written cells (per-block warp-shuffle max, then one reduction kernel); if
+ * update_max (HOST, nullable) is given the call waits and stores it, and returns
+ * NONFINITE when a prediction is NaN/Inf (the lattice is written regardless). */
+mfp_status mfp_scatter_phase(mfp_ctx* ctx, int32_t rank, int32_t phase, const float* pred, int64_t B,
+                             float* update_max);
+
 /* Run ONE phase (class 0..3 in G2 order) on the current lattice of every local
  * rank, without exchange (debug / sampled parity at full size). */
 mfp_status mfp_step_phase(mfp_ctx* ctx, int32_t phase);

@@ -78,6 +78,8 @@ struct mfp_ctx {
   float* gather = nullptr;   // rank 0, NCCL: other ranks' blocks
   unsigned int* delta = nullptr;  // [2]
   unsigned int* hdelta = nullptr;  // pinned
+  unsigned int* iomax = nullptr;   // scatter block maxima (a6 standalone)
+  unsigned int* ioout = nullptr;   // [2] reduced update norm + non-finite flag
   int num_sms = 148;
   int launches = 0;
   bool poisoned = false;
@@ -174,6 +176,8 @@ void carve(mfp_ctx* c, void* base, size_t* total) {
   dn.HfT = cv.take<float>((size_t)kNB * kQF);
   c->gstage = cv.take<float>((size_t)2 * (c->cfg.nx + c->cfg.ny));
   c->delta = cv.take<unsigned int>(4);
+  c->iomax = cv.take<unsigned int>(148 * 8);   // >= scatter_grid(B) for any B
+  c->ioout = cv.take<unsigned int>(2);
   const bool need_full = (c->rank == MFP_ALL_RANKS || c->rank == 0);
   c->full = need_full ? cv.take<float>((size_t)(c->cfg.nx + 1) * (c->cfg.ny + 1)) : nullptr;
   if (c->rank == 0 && c->R > 1) c->gather = cv.take<float>((size_t)(c->cfg.nx + 1) * (c->cfg.ny + 1));
@@ -783,6 +787,63 @@ mfp_status mfp_sdnet_batch(mfp_ctx* c, const float* gb, int64_t B, int32_t query
   cudaError_t e = cudaGetLastError();
   c->stream = saved;
   if (e != cudaSuccess) return fail(c, MFP_ERR_CUDA, cudaGetErrorString(e));
+  return MFP_OK;
+}
+
+static mfp_status io_args(mfp_ctx* c, int32_t rank, int32_t phase, RankState** out) {
+  if (!c) return MFP_ERR_INVALID;
+  if (c->poisoned) return MFP_ERR_STATE;
+  if (phase < 0 || phase > 3) return fail(c, MFP_ERR_INVALID, "phase must be 0..3");
+  const int idx = c->rank == MFP_ALL_RANKS ? rank : 0;
+  if ((c->rank != MFP_ALL_RANKS && rank != 0 && rank != c->rank) || idx < 0 || idx >= (int)c->ranks.size())
+    return fail(c, MFP_ERR_INVALID, "rank out of range");
+  *out = &c->ranks[idx];
+  return MFP_OK;
+}
+
+mfp_status mfp_gather_phase(mfp_ctx* c, int32_t rank, int32_t phase, float* gb, int64_t cap, int64_t* B_out,
+                            int32_t* ax_out, int32_t* ay_out) {
+  RankState* rs = nullptr;
+  if (mfp_status st = io_args(c, rank, phase, &rs)) return st;
+  const RankPlan& p = rs->plan;
+  const int64_t B = (int64_t)p.phase_anchor[phase].size();
+  if (B_out) *B_out = B;
+  if (!gb && !ax_out && !ay_out) return MFP_OK;   // size query
+  if (cap < B) return fail(c, MFP_ERR_INVALID, "gather_phase: cap < number of subdomains");
+  if ((ax_out == nullptr) != (ay_out == nullptr)) return fail(c, MFP_ERR_INVALID, "ax_out/ay_out: both or neither");
+  if (ax_out)
+    for (int64_t i = 0; i < B; i++) {
+      const uint32_t pk = p.phase_anchor[phase][(size_t)i];
+      ax_out[i] = p.lat.RX0 + kH * (int32_t)(pk & 0xffffu);
+      ay_out[i] = p.lat.RY0 + kH * (int32_t)(pk >> 16);
+    }
+  if (gb) {
+    launch_gather_phase(rs->lat, p.lat, rs->anchors[phase], B, gb, c->stream);
+    c->launches++;
+    CK(cudaGetLastError());
+  }
+  return MFP_OK;
+}
+
+mfp_status mfp_scatter_phase(mfp_ctx* c, int32_t rank, int32_t phase, const float* pred, int64_t B,
+                             float* update_max) {
+  RankState* rs = nullptr;
+  if (mfp_status st = io_args(c, rank, phase, &rs)) return st;
+  const RankPlan& p = rs->plan;
+  if (B != (int64_t)p.phase_anchor[phase].size() || (B > 0 && !pred))
+    return fail(c, MFP_ERR_INVALID, "scatter_phase: B must equal the phase's subdomain count");
+  launch_scatter_phase(rs->lat, p.lat, rs->anchors[phase], B, pred, c->iomax, c->ioout, c->stream);
+  c->launches += B > 0 ? 2 : 1;
+  CK(cudaGetLastError());
+  if (update_max) {
+    unsigned int h[2];
+    CK(cudaMemcpyAsync(h, c->ioout, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float v;
+    memcpy(&v, &h[0], sizeof(v));
+    *update_max = v;
+    if (h[1]) return fail(c, MFP_ERR_NONFINITE, "scatter_phase: non-finite prediction");
+  }
   return MFP_OK;
 }
 

@@ -135,6 +135,13 @@ void launch_chain_fp32(const float* z, int64_t B, int q, const DevNet& net, cons
 bool chain_tc_available();
 void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const Sink& sink,
                      int num_sms, cudaStream_t s);
+// standalone boundary IO (kernels_boundary_io.cu): a1 gather, a6 scatter + update norm, a8 reduction
+int scatter_grid(int64_t B);
+void launch_gather_phase(const float* lat, const LatticeGeom& L, const uint32_t* anchors, int64_t B, float* gb,
+                         cudaStream_t s);
+void launch_scatter_phase(float* lat, const LatticeGeom& L, const uint32_t* anchors, int64_t B, const float* pred,
+                          unsigned int* blockmax /* scatter_grid(B) */, unsigned int* out /* [2] */,
+                          cudaStream_t s);
 void launch_delta(const float* lat, const float* snap, const int64_t* segs, int nseg,
                   unsigned int* out /* [0]=max bits, [1]=nonfinite flag */, cudaStream_t s);
 void launch_pack(const float* lat, const int32_t* idx, int64_t n, float* buf, cudaStream_t s);

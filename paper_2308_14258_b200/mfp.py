@@ -99,6 +99,8 @@ _SIGS = {
     "mfp_plan_anchors": [_P(mfp_config), _i32, _i32, _P(_i32), _P(_i32), _i64, _P(_i64)],
     "mfp_plan_halo": [_P(mfp_config), _i32, _i32, _i32, _P(_i32), _P(_i32), _P(_i32), _i64, _P(_i64)],
     "mfp_cost_model": [_f64] * 8 + [_P(_f64)] * 3,
+    "mfp_gather_phase": [_vp, _i32, _i32, _vp, _i64, _P(_i64), _P(_i32), _P(_i32)],
+    "mfp_scatter_phase": [_vp, _i32, _i32, _vp, _i64, _P(ctypes.c_float)],
     "mfp_nccl_get_unique_id": [_vp],
     "mfp_nccl_comm_init": [_i32, _vp, _i32, _P(_vp)],
     "mfp_nccl_comm_destroy": [_vp],
@@ -187,6 +189,29 @@ def mfp_solve_device(ctx, g_dev, max_iters: int, tol: float, u_dev) -> mfp_repor
 
 def mfp_sdnet_batch(ctx, gb_dev, B: int, query_set: int, out_dev, stream=None) -> None:
     _check(_lib.mfp_sdnet_batch(ctx, _ptr(gb_dev), B, query_set, _ptr(out_dev), stream), ctx)
+
+
+def mfp_gather_phase(ctx, rank: int, phase: int, gb_dev=None, cap: int = 0, want_anchors: bool = False):
+    """a1 standalone: returns (B, anchors (B, 2) int32 (ax, ay) or None); gb_dev=None and
+    want_anchors=False is a size query."""
+    B = _i64(0)
+    _check(_lib.mfp_gather_phase(ctx, rank, phase, None, 0, ctypes.byref(B), None, None), ctx)
+    ax = ay = None
+    if want_anchors:
+        ax, ay = np.zeros(max(B.value, 1), np.int32), np.zeros(max(B.value, 1), np.int32)
+    if gb_dev is not None or want_anchors:
+        _check(_lib.mfp_gather_phase(ctx, rank, phase, _ptr(gb_dev), max(cap, B.value if gb_dev is None else cap),
+                                     ctypes.byref(B), None if ax is None else ax.ctypes.data_as(_P(_i32)),
+                                     None if ay is None else ay.ctypes.data_as(_P(_i32))), ctx)
+    anchors = np.stack([ax[:B.value], ay[:B.value]], 1) if want_anchors else None
+    return B.value, anchors
+
+
+def mfp_scatter_phase(ctx, rank: int, phase: int, pred_dev, B: int, want_norm: bool = True):
+    """a6 + a8 standalone: returns the update norm max |new - old| (syncs) or None."""
+    v = ctypes.c_float(0.0)
+    _check(_lib.mfp_scatter_phase(ctx, rank, phase, _ptr(pred_dev), B, ctypes.byref(v) if want_norm else None), ctx)
+    return v.value if want_norm else None
 
 
 def mfp_step_phase(ctx, phase: int) -> None:
@@ -336,8 +361,35 @@ class Mfp:
     def step_phase(self, phase: int):
         mfp_step_phase(self.ctx, phase)
 
+    def _io_rank(self, rank):
+        return 0 if self.rank != ALL_RANKS else (0 if rank is None else rank)
+
+    def gather_phase(self, phase: int, out=None, rank: int | None = None, want_anchors: bool = False):
+        """Perimeters (B, 128) of the phase's subdomains from the current lattice (a1)."""
+        import torch
+
+        r = self._io_rank(rank)
+        B, _ = mfp_gather_phase(self.ctx, r, phase)
+        if out is None:
+            out = torch.empty((max(B, 1), 128), dtype=torch.float32, device="cuda")
+        self._enter()
+        _, anc = mfp_gather_phase(self.ctx, r, phase, out, out.shape[0], want_anchors)
+        self._leave()
+        return (out[:B], anc) if want_anchors else out[:B]
+
+    def scatter_phase(self, phase: int, pred, rank: int | None = None, want_norm: bool = True):
+        """Write (B, 61) centre-line predictions onto the lattice (a6); returns max |new - old|."""
+        self._enter()
+        v = mfp_scatter_phase(self.ctx, self._io_rank(rank), phase, pred, pred.shape[0], want_norm)
+        self._leave()
+        return v
+
     def profile(self, iters: int) -> mfp_profile:
         return mfp_profile_iterations(self.ctx, iters)
+
+    def lines_bytes(self, rank: int | None = None) -> int:
+        info = mfp_plan_query(self.cfg, self.ranks[0] if rank is None else rank)
+        return 4 * (info.n_hlines * info.hline_len + info.n_vlines * info.vline_len)
 
     def close(self):
         if getattr(self, "ctx", None) is not None:
