@@ -649,6 +649,12 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
     const uint32_t a_base = smem_u32(S.A + slot * kTile);
     const uint32_t a_row = a_base + (uint32_t)row * 128u;   // SW128 K-major row base (first K-half)
     const int r7 = row & 7;
+    // the eight swizzled 16-byte chunk addresses of this row (SW128: chunk j of a
+    // 128 B row lives at (j ^ row % 8) * 16); with the column loops unrolled every
+    // operand store is one of these plus an immediate K-half offset
+    uint32_t a_sw[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) a_sw[j] = a_row + ((uint32_t)(j ^ r7) << 4);
     const uint32_t t_row = tmem + (uint32_t)(slot * kD) + ((uint32_t)(quad * 32) << 16);
     float* zb = S.zbuf + slot * kZRows * kD;
     const float bo = __ldg(net.bo);
@@ -735,8 +741,11 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
         int zo = (int)(sidx - s_first);
         if (zo < 0 || zo >= kZRows) zo = 0;   // rows past the end of the batch (not stored)
         const float* zr = zb + zo * kD;
-#pragma unroll 2
-        for (int cc = 0; cc < kD / 8; cc++) {
+#pragma unroll 1
+        for (int kh = 0; kh < 2; kh++) {   // K-half of the A image
+#pragma unroll
+        for (int j8 = 0; j8 < 8; j8++) {   // 8-column group within the K-half
+          const int cc = 8 * kh + j8;
           const float4 z0 = *reinterpret_cast<const float4*>(zr + cc * 8);
           const float4 z1 = *reinterpret_cast<const float4*>(zr + cc * 8 + 4);
           const float4 a0 = *reinterpret_cast<const float4*>(S.w2 + cc * 8);
@@ -752,7 +761,8 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
           f2_split(ffma2(f2_make(a1.z, a1.w), QX, ffma2(f2_make(b1.z, b1.w), QY, f2_make(z1.z, z1.w))), v[6], v[7]);
           uint32_t w[4];
           act8<GELU, F16>(v, w);
-          st_shared_v4(a_row + ((uint32_t)(cc >> 3) << 14) + ((uint32_t)((cc & 7) ^ r7) << 4), w[0], w[1], w[2], w[3]);
+          st_shared_v4(a_sw[j8] + ((uint32_t)kh << 14), w[0], w[1], w[2], w[3]);
+        }
         }
       }
       if (lane == 0) MFP_TR(warp, j, 1, 3);
@@ -780,7 +790,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
               uint32_t w[4];
               act8<GELU, F16>(v, w);
 #ifndef MFP_EXPERIMENT_NO_STS
-              st_shared_v4(a_row + ((uint32_t)(g >> 3) << 14) + ((uint32_t)((g & 7) ^ r7) << 4), w[0], w[1], w[2], w[3]);
+              st_shared_v4(a_sw[g & 7] + ((uint32_t)(g >> 3) << 14), w[0], w[1], w[2], w[3]);
 #else
               if (w[0] == 0x12345678u && w[1] == 0x9abcdef0u) st_shared_v4(a_row, w[0], w[1], w[2], w[3]);
 #endif
@@ -795,7 +805,11 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
 #endif
         tmem_ld16(t_row, ra);
         tmem_wait_ld_dep16(ra);
+#ifdef MFP_EPI_DYN
 #pragma unroll 1
+#else
+#pragma unroll
+#endif
         for (int c16 = 0; c16 < kD / 16; c16 += 2) {
           tmem_ld16(t_row + (uint32_t)((c16 + 1) * 16), rb);
           work16(ra, c16);
