@@ -743,6 +743,35 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
         const float* zr = zb + zo * kD;
 #pragma unroll 1
         for (int kh = 0; kh < 2; kh++) {   // K-half of the A image
+#ifndef MFP_SPLIT8
+          // 16 columns (two 8-column groups, 8 element pairs) per block, as in the
+          // hidden-layer epilogue: twice the independent GELU chains of one group
+#pragma unroll
+          for (int j16 = 0; j16 < 4; j16++) {
+            const int c0 = 64 * kh + 16 * j16;
+            float4 zz[4], aa[4], bb[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+              zz[i] = *reinterpret_cast<const float4*>(zr + c0 + 4 * i);
+              aa[i] = *reinterpret_cast<const float4*>(S.w2 + c0 + 4 * i);
+              bb[i] = *reinterpret_cast<const float4*>(S.w2 + kD + c0 + 4 * i);
+            }
+            const f2 QX = f2_make(qx, qx), QY = f2_make(qy, qy);
+            float v[16];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+              f2_split(ffma2(f2_make(aa[i].x, aa[i].y), QX, ffma2(f2_make(bb[i].x, bb[i].y), QY, f2_make(zz[i].x, zz[i].y))),
+                       v[4 * i], v[4 * i + 1]);
+              f2_split(ffma2(f2_make(aa[i].z, aa[i].w), QX, ffma2(f2_make(bb[i].z, bb[i].w), QY, f2_make(zz[i].z, zz[i].w))),
+                       v[4 * i + 2], v[4 * i + 3]);
+            }
+            uint32_t w[8];
+            act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v), *reinterpret_cast<uint32_t(*)[4]>(w));
+            act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v + 8), *reinterpret_cast<uint32_t(*)[4]>(w + 4));
+            st_shared_v4(a_sw[2 * j16] + ((uint32_t)kh << 14), w[0], w[1], w[2], w[3]);
+            st_shared_v4(a_sw[2 * j16 + 1] + ((uint32_t)kh << 14), w[4], w[5], w[6], w[7]);
+          }
+#else
 #pragma unroll
         for (int j8 = 0; j8 < 8; j8++) {   // 8-column group within the K-half
           const int cc = 8 * kh + j8;
@@ -763,6 +792,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
           act8<GELU, F16>(v, w);
           st_shared_v4(a_sw[j8] + ((uint32_t)kh << 14), w[0], w[1], w[2], w[3]);
         }
+#endif
         }
       }
       if (lane == 0) MFP_TR(warp, j, 1, 3);
