@@ -358,7 +358,13 @@ def main():
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"
                 if tensor else "derived fp32 SIMT peak (DESIGN.md §7)",
                 "chain_ms_per_launch": chain_ms, "chain_share_of_iteration":
-                    prof.chain_ms_total / (prof.ms_per_iter * prof.iterations)}
+                    prof.chain_ms_total / (prof.ms_per_iter * prof.iterations),
+                "iteration_breakdown_ms": {
+                    "iteration": prof.ms_per_iter, "chain_per_phase": prof.ms_chain,
+                    "gather_embed_per_phase": prof.ms_gather_embed, "halo": prof.ms_halo,
+                    "delta_per_check": prof.ms_delta,
+                    "note": "mfp_profile_iterations: CUDA events around every kernel (no graphs), "
+                            "so the iteration here includes launch gaps the graph-replayed solve avoids"}}
 
     # time-to-converge (SDNet bf16, tol 1e-3 max|g|, c = 16)
     ttc = None

@@ -1,31 +1,35 @@
-// kernels_tc.cu — SDNet MLP chain on the 5th-generation tensor cores (N4),
+// kernels_tc.cu — SDNet MLP chain on the 5th-generation tensor cores (a3-a6),
 // bf16 or fp16 operands, fp32 accumulation in TMEM.
 //
 // The hidden GEMM chain h <- GELU(h W_l^T + b_l) is the path's one
 // dense contraction: rows = (subdomain, query) pairs packed densely
 // (row = s*q + p), K = N = d = 128.  Design:
-//   * persistent CTAs (one per SM), 128-row tiles (UMMA M = 128, N = 128,
-//     K = 16 x 8 per layer + one K = 16 bias step), fp32 accumulators in TMEM
-//     (3 slots x 128 columns);
-//   * the n_hidden weight matrices stay resident in shared memory for the
-//     whole kernel as 16-bit SWIZZLE_128B K-major images (B operand), pre-
+//   * persistent CTA pairs (cluster of 2 on one TPC, 74 pairs), 256-row pair
+//     tiles, tcgen05.mma.cta_group::2 with M = 256, N = 128, K = 16 x 8 per
+//     layer + one K = 16 bias step, fp32 accumulators in TMEM (4 tile slots x
+//     128 columns per CTA);
+//   * each CTA keeps its 64-row half of every hidden weight matrix resident in
+//     shared memory as 16-bit SWIZZLE_128B K-major images (B operand), pre-
 //     scaled by 1/2 (exact) because the epilogue produces h' = 2 GELU(x); each
 //     image carries a bias block (b = b_hi + b_lo in two K columns) that a
 //     constant ones-column A block adds on the tensor core;
-//   * warp 0 issues tcgen05.mma from one lane and commits to an mbarrier;
-//     warp 1 owns the TMEM allocation; warps 2..13 form three epilogue
-//     warpgroups, one per tile slot, so up to three tiles are in flight and
-//     the GELU pipes (MUFU tanh is the binding unit) stay fed
-//     while other tiles sit in the tensor core;
-//   * epilogue of a layer feeding another MMA: tcgen05.ld -> round to 16 bit
-//     -> packed GELU (HFMA2 + MUFU tanh) -> st.shared into the swizzled A
-//     operand -> fence.proxy.async -> mbarrier arrive;
+//   * one lane of the even CTA's highest warp issues the MMAs, commits are
+//     multicast to both CTAs' mbarriers; 16 epilogue warps per CTA form four
+//     warpgroups, one per tile slot, so four tiles are in flight and the GELU
+//     pipes (MUFU tanh bounds) stay fed while other tiles sit in
+//     the tensor core;
+//   * epilogue of a layer feeding another MMA: tcgen05.ld (16 columns, double
+//     buffered) -> packed fp32 GELU (FFMA2 + MUFU tanh) -> one RN rounding to
+//     16 bit -> st.shared into the swizzled A operand -> fence.proxy.async ->
+//     mbarrier arrive (remote for the odd CTA);
 //   * the layer-1 input is Eq. 5's broadcasted sum GELU(z[s] + W2 x_p): z of
-//     the <= 4 subdomains of a tile staged in smem (prefetched into registers
-//     one tile ahead), W2 x_p recomputed with two FMAs per element (no Q table
-//     in smem); the last layer's epilogue stays fp32 (GELU + head dot
+//     the <= 4 subdomains of a tile staged in smem with W2's constant half
+//     folded in (one FMA per element on the centre lines), prefetched one tile
+//     ahead; the last layer's epilogue stays fp32 (GELU + head dot
 //     y = wo.h + bo; the head cancels strongly) followed by the
-//     fused scatter onto the lattice (N5).
+//     fused scatter onto the lattice (a6) or the final-phase field (a9).
+#include <type_traits>
+
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -35,10 +39,7 @@ namespace mfp {
 namespace tc {
 
 constexpr int kRows = 128;
-constexpr int kSlots = 3;
-constexpr int kThreads = 32 * (2 + 4 * kSlots);  // 448
 constexpr int kTile = kRows * kD * 2;            // 32 KB 16-bit operand image
-constexpr int kWTile = kWImg * 2;                // 36 KB per hidden layer: weights (SW128) + bias block
 constexpr int kOnes = kRows * 16 * 2;            // 4 KB constant A block: K columns 0/1 = 1
 constexpr int kTmemCols = 512;
 constexpr int kZRows = 4;                        // subdomains one 128-row tile can touch (q >= 61)
@@ -63,17 +64,9 @@ __device__ __forceinline__ uint32_t pack2_rn(float lo, float hi) {
 // polynomial for part of the pairs (to offload MUFU) measured slower: the
 // epilogue is issue/latency bound as much as MUFU bound, DESIGN.md §6.
 __device__ __forceinline__ f2 gelu2_mufu(f2 x) {
-#if defined(MFP_EXPERIMENT_NO_ACT)      // timing experiment only: no GELU at all
-  return x;
-#else
   float u0, u1;
   f2_split(fmul2(x, ffma2(fmul2(x, x), f2_make(kGF1, kGF1), f2_make(kGF0, kGF0))), u0, u1);
-#if defined(MFP_EXPERIMENT_FAKE_TANH)   // timing experiment only: clamp instead of MUFU tanh
-  return ffma2(x, f2_make(fminf(fmaxf(u0, -1.f), 1.f), fminf(fmaxf(u1, -1.f), 1.f)), x);
-#else
   return ffma2(x, f2_make(tanh_approx(u0), tanh_approx(u1)), x);
-#endif
-#endif
 }
 
 // Activation of the fp32 last layer, up to the factor the head weights carry:
@@ -124,227 +117,6 @@ __device__ __forceinline__ void act8(const float (&v)[8], uint32_t (&w)[4]) {
   }
 }
 
-struct Smem {
-  uint8_t* W;      // [nh][36 KB]
-  uint8_t* A;      // [3][32 KB]
-  uint8_t* ones;   // 4 KB
-  float* zbuf;     // [3][4][128]
-  float* w2;       // [2][128]: W2[:,0], W2[:,1]
-  float* wo;       // [128]
-  uint64_t* bars;  // a_full[3], d_full[3]
-  uint32_t* tmem_slot;
-};
-
-// `raw` is the 1024-byte aligned dynamic shared window (SWIZZLE_128B operand
-// images need 1024-byte aligned atoms); plain pointer offsets keep the shared
-// address space visible to the compiler (LDS/STS, not generic LD/ST).
-__device__ __forceinline__ Smem carve(uint8_t* raw, int nh) {
-  Smem s;
-  s.W = raw;
-  s.A = raw + nh * kWTile;
-  s.ones = s.A + kSlots * kTile;
-  s.zbuf = (float*)(s.ones + kOnes);
-  s.w2 = s.zbuf + kSlots * kZRows * kD;
-  s.wo = s.w2 + 2 * kD;
-  s.bars = (uint64_t*)(s.wo + kD);
-  s.tmem_slot = (uint32_t*)(s.bars + 2 * kSlots);
-  return s;
-}
-
-size_t smem_bytes(int n_hidden) {
-  return (size_t)n_hidden * kWTile + kSlots * kTile + kOnes + 4 * ((size_t)kSlots * kZRows * kD + 3 * kD) +
-         16 * kSlots + 16;
-}
-
-template <int GELU, int F16>
-__global__ void __launch_bounds__(kThreads, 1)
-k_chain_tc(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, Sink sink) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const int nh = net.n_hidden;
-  const Smem S = carve(smem_raw, nh);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // ---- prologue: resident weight images / tables, barriers, TMEM
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(net.Wh_sw);
-    uint4* dst = reinterpret_cast<uint4*>(S.W);
-    for (int i = threadIdx.x; i < nh * kWTile / 16; i += kThreads) dst[i] = __ldg(src + i);
-    for (int i = threadIdx.x; i < kD; i += kThreads) {
-      S.wo[i] = (GELU == 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
-      S.w2[i] = __ldg(net.W2 + 2 * i);
-      S.w2[kD + i] = __ldg(net.W2 + 2 * i + 1);
-    }
-    // constant A block of the bias step: row r, K columns 0/1 = 1.0, others 0
-    if (threadIdx.x < kRows) {
-      const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
-      const int r = threadIdx.x;
-      *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + (r & 7) * 16) = make_uint4(one | (one << 16), 0u, 0u, 0u);
-      *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + 128 + (r & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
-    }
-  }
-  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();  // SW128 atoms need 1024 B alignment
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kSlots; s++) {
-      mbar_init(&S.bars[s], 128);           // a_full[s]: the slot's 128 epilogue threads
-      mbar_init(&S.bars[kSlots + s], 1);    // d_full[s]: tcgen05.commit
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
-                 "r"(kTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  fence_proxy_async();  // generic-proxy writes of W / ones visible to the tensor core
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *S.tmem_slot;
-
-  const int64_t ntiles = (total_rows + kRows - 1) / kRows;
-  const int64_t nloc = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const int64_t nsub = total_rows / q;
-
-  if (warp == 0) {
-    // ---- MMA issuer: round-robin over (tile group, layer, slot).  (Serving
-    // slots out of order with mbarrier.test_wait polling measured slower: the
-    // poll loop steals issue slots from the epilogue warps on its SMSP.)
-    if (lane == 0) {
-      uint32_t pa[kSlots] = {0u, 0u, 0u};
-      const uint32_t ones_desc_addr = smem_u32(S.ones);
-      for (int64_t j0 = 0; j0 < nloc; j0 += kSlots) {
-        for (int l = 0; l < nh; l++) {
-#pragma unroll
-          for (int s = 0; s < kSlots; s++) {
-            if (j0 + s >= nloc) continue;
-            mbar_wait(&S.bars[s], pa[s]);
-            pa[s] ^= 1u;
-            tc_fence_after();
-            const uint32_t a0 = smem_u32(S.A + s * kTile), b0 = smem_u32(S.W + l * kWTile);
-            const uint32_t d = tmem + (uint32_t)(s * kD);
-#pragma unroll
-            for (int k = 0; k < kD / 16; k++) {
-              const uint32_t off = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
-              mma_f16<F16>(d, sw128_desc(a0 + off), sw128_desc(b0 + off), k > 0 ? 1u : 0u);
-            }
-            // bias step: D += [1 1 0..] [b_hi b_lo 0..]^T
-            mma_f16<F16>(d, nosw_desc(ones_desc_addr), nosw_desc(b0 + (uint32_t)(kWImgW * 2)), 1u);
-            mma_commit(&S.bars[kSlots + s]);
-          }
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp >= 2) {
-    // ---- epilogue: warpgroup `slot` owns every third local tile
-    const int slot = (warp - 2) >> 2;
-    const int quad = warp & 3;                       // TMEM lane quadrant of this warp
-    const int row = quad * 32 + lane;                // tile row == TMEM lane
-    const int tid_s = (warp - 2 - 4 * slot) * 32 + lane;  // 0..127 within the slot
-    const uint32_t a_base = smem_u32(S.A + slot * kTile);
-    const uint32_t t_row = tmem + (uint32_t)(slot * kD) + ((uint32_t)(quad * 32) << 16);
-    float* zb = S.zbuf + slot * kZRows * kD;
-    const float bo = __ldg(net.bo);
-    // z staging: thread tid_s moves 4 consecutive floats of the tile's <= 4 subdomains
-    const int zi = 4 * tid_s, zr_ = zi >> 7, zc = zi & 127;
-    auto z_fetch = [&](int64_t j) -> float4 {
-      const int64_t t = blockIdx.x + j * (int64_t)gridDim.x;
-      int64_t sidx = (t * kRows) / q + zr_;
-      if (sidx > nsub - 1) sidx = nsub - 1;
-      return __ldg(reinterpret_cast<const float4*>(z + sidx * kD + zc));
-    };
-    if (slot < nloc) *reinterpret_cast<float4*>(zb + zi) = z_fetch(slot);
-    uint32_t pd = 0u;
-    for (int64_t j = slot; j < nloc; j += kSlots) {
-      const int64_t tile = blockIdx.x + j * (int64_t)gridDim.x;
-      const int64_t row0 = tile * kRows;
-      const int64_t s_first = row0 / q;
-      named_sync(1 + slot, 128);                     // zbuf of this tile visible
-      const bool have_next = j + kSlots < nloc;
-      float4 znext = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (have_next) znext = z_fetch(j + kSlots);    // prefetch, consumed after the last layer
-      const int64_t grow = row0 + row;
-      const bool valid = grow < total_rows;
-      const int64_t gr = valid ? grow : total_rows - 1;
-      const int64_t sidx = gr / q;
-      const int p = (int)(gr - sidx * q);
-      float qx, qy;
-      query_xy(q, p, &qx, &qy);
-      // layer-1 input (Eq. 5): h' = 2 GELU(z[s] + W2 x_p) -> A operand
-      {
-        const float* zr = zb + (int)(sidx - s_first) * kD;
-#pragma unroll 2
-        for (int cc = 0; cc < kD / 8; cc++) {
-          const float4 z0 = *reinterpret_cast<const float4*>(zr + cc * 8);
-          const float4 z1 = *reinterpret_cast<const float4*>(zr + cc * 8 + 4);
-          const float4 a0 = *reinterpret_cast<const float4*>(S.w2 + cc * 8);
-          const float4 a1 = *reinterpret_cast<const float4*>(S.w2 + cc * 8 + 4);
-          const float4 b0 = *reinterpret_cast<const float4*>(S.w2 + kD + cc * 8);
-          const float4 b1 = *reinterpret_cast<const float4*>(S.w2 + kD + cc * 8 + 4);
-          const float v[8] = {z0.x + fmaf(a0.x, qx, b0.x * qy), z0.y + fmaf(a0.y, qx, b0.y * qy),
-                              z0.z + fmaf(a0.z, qx, b0.z * qy), z0.w + fmaf(a0.w, qx, b0.w * qy),
-                              z1.x + fmaf(a1.x, qx, b1.x * qy), z1.y + fmaf(a1.y, qx, b1.y * qy),
-                              z1.z + fmaf(a1.z, qx, b1.z * qy), z1.w + fmaf(a1.w, qx, b1.w * qy)};
-          uint32_t w[4];
-          act8<GELU, F16>(v, w);
-          st_shared_v4(a_base + sw128_off(row, cc * 8), w[0], w[1], w[2], w[3]);
-        }
-      }
-      fence_proxy_async();
-      mbar_arrive(&S.bars[slot]);
-      float y = 0.f;
-      for (int l = 0; l < nh; l++) {
-        mbar_wait(&S.bars[kSlots + slot], pd);
-        pd ^= 1u;
-        tc_fence_after();
-        const bool last = (l == nh - 1);
-        // two 32-column TMEM loads in flight per wait
-#pragma unroll 1
-        for (int ch = 0; ch < kD / 32; ch += 2) {
-          uint32_t r[2][32];
-          tmem_ld32(t_row + (uint32_t)(ch * 32), r[0]);
-          tmem_ld32(t_row + (uint32_t)(ch * 32 + 32), r[1]);
-          tmem_wait_ld();
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            if (!last) {
-#pragma unroll
-              for (int c8 = 0; c8 < 4; c8++) {
-                float v[8];
-#pragma unroll
-                for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[h][c8 * 8 + e]);  // bias already in D
-                uint32_t w[4];
-                act8<GELU, F16>(v, w);
-                st_shared_v4(a_base + sw128_off(row, (ch + h) * 32 + c8 * 8), w[0], w[1], w[2], w[3]);
-              }
-            } else {
-              const float* wo = S.wo + (ch + h) * 32;
-#pragma unroll
-              for (int e = 0; e < 32; e++) y = fmaf(wo[e], act_head<GELU>(__uint_as_float(r[h][e])), y);
-            }
-          }
-        }
-        tc_fence_before();
-        if (!last) {
-          fence_proxy_async();
-          mbar_arrive(&S.bars[slot]);
-        }
-      }
-      // every thread of the slot finished reading zbuf (the layer MMAs needed
-      // all 128 arrivals), so the prefetched z of the next tile can land
-      if (have_next) *reinterpret_cast<float4*>(zb + zi) = znext;
-      if (valid) sink_store(sink, sidx, p, y + bo);   // fused scatter (N5)
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
-  }
-}
-
 }  // namespace tc
 
 // ---------------------------------------------------------------------------
@@ -384,45 +156,13 @@ __device__ __forceinline__ void cluster_sync() {
 // the next tile's z prefetch and the scatter stores) and CCTL.IVALL (an L1
 // invalidate per wait) — measured as ~750-cycle stalls on the MMA issue path.
 // Operand visibility to the tensor core is established by fence.proxy.async
-// before the arrive (MFP_CLUSTER_SCOPE=1 builds the cluster-scoped variant).
+// before the arrive.
 __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
-#ifdef MFP_CLUSTER_SCOPE
-  asm volatile(
-      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
-      "r"(cta)
-      : "memory");
-#else
   asm volatile(
       "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
       "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
       "r"(cta)
       : "memory");
-#endif
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-#ifdef MFP_CLUSTER_SCOPE
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
-      "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-#else
-  mbar_wait(bar, parity);
-#endif
-}
-__device__ __forceinline__ bool mbar_test_cluster(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
 }
 // kind::f16, D fp32, M = 256 (pair), N = 128.
 template <int F16>
@@ -451,8 +191,8 @@ struct Smem2 {
   uint8_t* W;      // [nh][18 KB]: this CTA's 64-row half + bias block
   uint8_t* A;      // [4][32 KB]
   uint8_t* ones;   // 4 KB
-  float* zbuf;     // [4][4][128] (L0 = 0) / [4] x 2 KB layer-0 B blocks (L0 = 1)
-  float* w2;       // [2][128]
+  float* zbuf;     // [4 slots][2][4 subdomains][128]: z + W2[:,0]/2, z + W2[:,1]/2
+  float* w2;       // [2][128]: W2[:,0], W2[:,1]
   float* wo;       // [128]
   uint64_t* bars;  // a_full[4] (used in the even CTA), d_full[4]
   uint32_t* tmem_slot;
@@ -464,7 +204,7 @@ __device__ __forceinline__ Smem2 carve2(uint8_t* raw, int nh) {
   s.A = raw + nh * kHalf;
   s.ones = s.A + kSlots2 * kTile;
   s.zbuf = (float*)(s.ones + kOnes);
-  s.w2 = s.zbuf + kSlots2 * kZRows * kD;
+  s.w2 = s.zbuf + kSlots2 * 2 * kZRows * kD;
   s.wo = s.w2 + 2 * kD;
   s.bars = (uint64_t*)(s.wo + kD);
   s.tmem_slot = (uint32_t*)(s.bars + 2 * kSlots2);
@@ -472,33 +212,9 @@ __device__ __forceinline__ Smem2 carve2(uint8_t* raw, int nh) {
 }
 
 size_t smem_bytes2(int n_hidden) {
-  return (size_t)n_hidden * kHalf + kSlots2 * kTile + kOnes + 4 * ((size_t)kSlots2 * kZRows * kD + 3 * kD) +
+  return (size_t)n_hidden * kHalf + kSlots2 * kTile + kOnes + 4 * ((size_t)kSlots2 * 2 * kZRows * kD + 3 * kD) +
          16 * kSlots2 + 16;
 }
-
-// Layer-0 B block (L0 = 1): this CTA's 64 output features (rows) x K = 16,
-// SWIZZLE_NONE K-major (8-row x 16-byte core matrices, LBO 128 B, SBO 256 B).
-// K columns: 0-5 z_hi of the pair tile's <= 6 subdomains, 6-11 z_lo, 12/13
-// W2[:,0] hi/lo, 14/15 W2[:,1] hi/lo.  The A block (128 rows x K = 16, same
-// layout, in the first 4 KB of the slot's A image) holds the one-hot subdomain
-// selector twice and the query coordinates (exact in 16 bit: multiples of 1/32)
-// twice, so one K = 16 MMA yields z[s] + W2 x_p (Eq. 5) to ~2^-17 relative.
-__device__ __forceinline__ uint32_t l0_off(int r, int k) {
-  return (uint32_t)((r >> 3) * 256 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
-}
-template <int F16>
-__device__ __forceinline__ void split16(float v, uint16_t& hi, uint16_t& lo) {
-  if constexpr (F16) {
-    const __half h = __float2half_rn(v);
-    hi = __half_as_ushort(h);
-    lo = __half_as_ushort(__float2half_rn(v - __half2float(h)));
-  } else {
-    const __nv_bfloat16 h = __float2bfloat16_rn(v);
-    hi = __bfloat16_as_ushort(h);
-    lo = __bfloat16_as_ushort(__float2bfloat16_rn(v - __bfloat162float(h)));
-  }
-}
-constexpr int kL0Sub = 6;   // subdomains a 256-row pair tile can touch (q >= 61)
 
 // MFP_TRACE builds: per-event clock64 stamps of CTAs 0/1 (DESIGN.md §6 timeline).
 #ifdef MFP_TRACE
@@ -511,7 +227,9 @@ __device__ unsigned long long g_trace[2][18][32][8][4];   // [cta][warp][tile][l
 #define MFP_TR(w, jt, l, ev) do { } while (0)
 #endif
 
-template <int GELU, int F16, int L0>
+// Pair tile t of this cluster = rows [256 t, 256 t + 256) of the batch (row =
+// subdomain * q + query, packed densely); the even CTA owns the first 128.
+template <int GELU, int F16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, Sink sink) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -520,7 +238,8 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
 
-  // ---- prologue
+  // ---- prologue: this CTA's weight half-images, head / split-layer vectors,
+  // the constant ones block of the bias step, barriers, TMEM
   {
     for (int l = 0; l < nh; l++) {
       const uint4* src =
@@ -532,19 +251,6 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       S.wo[i] = (GELU == 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
       S.w2[i] = __ldg(net.W2 + 2 * i);
       S.w2[kD + i] = __ldg(net.W2 + 2 * i + 1);
-    }
-    if constexpr (L0) {
-      for (int i = threadIdx.x; i < kSlots2 * 64; i += kThreads2) {
-        const int sl = i >> 6, nl = i & 63, n = 64 * (int)rank + nl;
-        uint8_t* blk = reinterpret_cast<uint8_t*>(S.zbuf) + sl * 2048;
-        uint16_t h, lo;
-        split16<F16>(__ldg(net.W2 + 2 * n), h, lo);
-        *reinterpret_cast<uint16_t*>(blk + l0_off(nl, 12)) = h;
-        *reinterpret_cast<uint16_t*>(blk + l0_off(nl, 13)) = lo;
-        split16<F16>(__ldg(net.W2 + 2 * n + 1), h, lo);
-        *reinterpret_cast<uint16_t*>(blk + l0_off(nl, 14)) = h;
-        *reinterpret_cast<uint16_t*>(blk + l0_off(nl, 15)) = lo;
-      }
     }
     if (threadIdx.x < kRows) {
       const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
@@ -580,72 +286,40 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
   const int64_t nsub = total_rows / q;
 
   if (warp == kIssueWarp) {
+    // ---- MMA issuer (one lane of the even CTA), slots served in order
     if (rank == 0 && lane == 0) {
       uint32_t pa[kSlots2] = {0u, 0u, 0u, 0u};
       const uint32_t ones_addr = smem_u32(S.ones);
-      // layer ll of the slot-s tile: the split-layer K = 16 step (L0) or hidden W_l (+ bias step)
-      auto issue = [&](int s, int ll, int64_t jt) {
-        MFP_TR(kIssueWarp, jt, ll, 0);
-        pa[s] ^= 1u;
-        tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(s * kD);
-#ifdef MFP_EXPERIMENT_NO_MMA
-        if (true) {
-        } else
-#endif
-        if (L0 && ll == 0) {
-          mma2<F16>(d, nosw_desc(smem_u32(S.A + s * kTile)),
-                    nosw_desc(smem_u32(reinterpret_cast<uint8_t*>(S.zbuf) + s * 2048)), 0u);
-        } else {
-          const int l = ll - L0;
-          const uint32_t a0 = smem_u32(S.A + s * kTile), b0 = smem_u32(S.W + l * kHalf);
-#pragma unroll
-          for (int k = 0; k < kD / 16; k++) {
-            const uint32_t offa = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
-            const uint32_t offb = (uint32_t)((k >> 2) * 8192 + (k & 3) * 32);
-            mma2<F16>(d, sw128_desc(a0 + offa), sw128_desc(b0 + offb), k > 0 ? 1u : 0u);
-          }
-          mma2<F16>(d, nosw_desc(ones_addr), nosw_desc(b0 + 16384u), 1u);   // bias step
-        }
-        commit2(&S.bars[kSlots2 + s]);
-        MFP_TR(kIssueWarp, jt, ll, 1);
-      };
-#ifdef MFP_OOO_ISSUE
-      // out-of-order: serve whichever slot's operands are complete first
-      int64_t jt[kSlots2];
-      int lls[kSlots2];
-      for (int s = 0; s < kSlots2; s++) { jt[s] = s; lls[s] = 0; }
-      for (;;) {
-        bool any = false;
-#pragma unroll 1
-        for (int s = 0; s < kSlots2; s++) {
-          if (jt[s] >= nloc) continue;
-          any = true;
-          if (!mbar_test_cluster(&S.bars[s], pa[s])) continue;
-          issue(s, lls[s], jt[s]);
-          if (++lls[s] == nh + L0) { lls[s] = 0; jt[s] += kSlots2; }
-        }
-        if (!any) break;
-      }
-#else
       for (int64_t j0 = 0; j0 < nloc; j0 += kSlots2) {
-        for (int ll = 0; ll < nh + L0; ll++) {
+        for (int l = 0; l < nh; l++) {
 #pragma unroll
           for (int s = 0; s < kSlots2; s++) {
             if (j0 + s >= nloc) continue;
-            mbar_wait_cluster(&S.bars[s], pa[s]);
-            issue(s, ll, j0 + s);
+            mbar_wait(&S.bars[s], pa[s]);   // both CTAs' A operands of layer l written
+            MFP_TR(kIssueWarp, j0 + s, l, 0);
+            pa[s] ^= 1u;
+            tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)(s * kD);
+            const uint32_t a0 = smem_u32(S.A + s * kTile), b0 = smem_u32(S.W + l * kHalf);
+#pragma unroll
+            for (int k = 0; k < kD / 16; k++) {
+              const uint32_t offa = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
+              const uint32_t offb = (uint32_t)((k >> 2) * 8192 + (k & 3) * 32);
+              mma2<F16>(d, sw128_desc(a0 + offa), sw128_desc(b0 + offb), k > 0 ? 1u : 0u);
+            }
+            mma2<F16>(d, nosw_desc(ones_addr), nosw_desc(b0 + 16384u), 1u);   // bias step
+            commit2(&S.bars[kSlots2 + s]);
+            MFP_TR(kIssueWarp, j0 + s, l, 1);
           }
         }
       }
-#endif
     }
     __syncwarp();
   } else if (warp < kEpiWarps) {
+    // ---- epilogue warpgroup of tile slot `slot`; thread = one row of the tile
     const int slot = warp >> 2;
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
-    const int tid_s = quad * 32 + lane;
     const uint32_t a_base = smem_u32(S.A + slot * kTile);
     const uint32_t a_row = a_base + (uint32_t)row * 128u;   // SW128 K-major row base (first K-half)
     const int r7 = row & 7;
@@ -656,53 +330,43 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
 #pragma unroll
     for (int j = 0; j < 8; j++) a_sw[j] = a_row + ((uint32_t)(j ^ r7) << 4);
     const uint32_t t_row = tmem + (uint32_t)(slot * kD) + ((uint32_t)(quad * 32) << 16);
-    float* zb = S.zbuf + slot * kZRows * kD;
+    float* zb = S.zbuf + slot * 2 * kZRows * kD;
     const float bo = __ldg(net.bo);
-    const int zi = 4 * tid_s, zr_ = zi >> 7, zc = zi & 127;
+    const int zi = 4 * row, zr_ = zi >> 7, zc = zi & 127;
     auto row0_of = [&](int64_t j) -> int64_t { return (cid + j * ncl) * (2 * kRows) + rank * kRows; };
     auto z_fetch = [&](int64_t j) -> float4 {
       int64_t sidx = row0_of(j) / q + zr_;
       if (sidx > nsub - 1) sidx = nsub - 1;
       return __ldg(reinterpret_cast<const float4*>(z + sidx * kD + zc));
     };
+    // z of the tile's <= 4 subdomains, staged with the constant half of the split
+    // layer folded in: z + W2[:,0]/2 (vertical centre line, x/m = 1/2) and
+    // z + W2[:,1]/2 (horizontal centre line, y/m = 1/2), so that a centre-line
+    // row needs one FMA per element for Eq. 5's broadcasted sum
+    auto z_stage = [&](const float4 v) {
+      const float4 a = *reinterpret_cast<const float4*>(S.w2 + zc);
+      const float4 b = *reinterpret_cast<const float4*>(S.w2 + kD + zc);
+      *reinterpret_cast<float4*>(zb + zi) =
+          make_float4(fmaf(0.5f, a.x, v.x), fmaf(0.5f, a.y, v.y), fmaf(0.5f, a.z, v.z), fmaf(0.5f, a.w, v.w));
+      *reinterpret_cast<float4*>(zb + kZRows * kD + zi) =
+          make_float4(fmaf(0.5f, b.x, v.x), fmaf(0.5f, b.y, v.y), fmaf(0.5f, b.z, v.z), fmaf(0.5f, b.w, v.w));
+    };
     auto arrive_a = [&]() {
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(&S.bars[slot], 0u);
     };
-    // L0 = 1: thread tid_s moves 3 of the tile's 6 x 64 z values (this CTA's feature half)
-    auto rowp_of = [&](int64_t j) -> int64_t { return (cid + j * ncl) * (2 * kRows); };
-    auto z3_fetch = [&](int64_t j, float (&zv)[3]) {
-      const int64_t sf = rowp_of(j) / q;
-#pragma unroll
-      for (int i = 0; i < 3; i++) {
-        const int idx = tid_s + 128 * i;
-        int64_t sidx = sf + (idx >> 6);
-        if (sidx > nsub - 1) sidx = nsub - 1;
-        zv[i] = __ldg(z + sidx * kD + 64 * rank + (idx & 63));
-      }
-    };
-    float z3[3] = {0.f, 0.f, 0.f};
-    uint8_t* const b0blk = reinterpret_cast<uint8_t*>(S.zbuf) + slot * 2048;
-    if constexpr (L0) {
-      if (slot < nloc) z3_fetch(slot, z3);
-    } else {
-      if (slot < nloc) *reinterpret_cast<float4*>(zb + zi) = z_fetch(slot);
-    }
+    if (slot < nloc) z_stage(z_fetch(slot));
     uint32_t pd = 0u;
     for (int64_t j = slot; j < nloc; j += kSlots2) {
       if (lane == 0) MFP_TR(warp, j, 0, 3);
       const int64_t row0 = row0_of(j);
-      int64_t s_first = (L0 ? rowp_of(j) : row0) / q;
+      int64_t s_first = row0 / q;
       if (s_first > nsub - 1) s_first = nsub - 1;
-      if constexpr (!L0) named_sync(1 + slot, 128);
+      named_sync(1 + slot, 128);   // this tile's staged z visible to the slot's 4 warps
       if (lane == 0) MFP_TR(warp, j, 2, 3);
       const bool have_next = j + kSlots2 < nloc;
       float4 znext = make_float4(0.f, 0.f, 0.f, 0.f);
-      float z3n[3] = {0.f, 0.f, 0.f};
-      if (have_next) {
-        if constexpr (L0) z3_fetch(j + kSlots2, z3n);
-        else znext = z_fetch(j + kSlots2);
-      }
+      if (have_next) znext = z_fetch(j + kSlots2);
       const int64_t grow = row0 + row;
       const bool valid = grow < total_rows;
       const int64_t gr = valid ? grow : total_rows - 1;
@@ -710,148 +374,98 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       const int p = (int)(gr - sidx * q);
       float qx, qy;
       query_xy(q, p, &qx, &qy);
-      if constexpr (L0) {
-        // z hi/lo columns of the B block, then this row's A row (one-hot x2, qx x2, qy x2)
-#pragma unroll
-        for (int i = 0; i < 3; i++) {
-          const int idx = tid_s + 128 * i, jj = idx >> 6, nl = idx & 63;
-          uint16_t h, lo;
-          split16<F16>(z3[i], h, lo);
-          *reinterpret_cast<uint16_t*>(b0blk + l0_off(nl, jj)) = h;
-          *reinterpret_cast<uint16_t*>(b0blk + l0_off(nl, kL0Sub + jj)) = lo;
-        }
-        int zo = (int)(sidx - s_first);
-        if (zo < 0 || zo >= kL0Sub) zo = 0;   // rows past the end of the batch (not stored)
-        const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
-        uint32_t wd[8];
-#pragma unroll
-        for (int w = 0; w < 6; w++) {
-          const int k0 = 2 * w, k1 = 2 * w + 1;
-          wd[w] = ((k0 == zo || k0 == zo + kL0Sub) ? one : 0u) | (((k1 == zo || k1 == zo + kL0Sub) ? one : 0u) << 16);
-        }
-        uint16_t qh, ql;
-        split16<F16>(qx, qh, ql);
-        wd[6] = (uint32_t)qh | ((uint32_t)qh << 16);
-        split16<F16>(qy, qh, ql);
-        wd[7] = (uint32_t)qh | ((uint32_t)qh << 16);
-        const uint32_t ab = a_base + l0_off(row, 0);
-        st_shared_v4(ab, wd[0], wd[1], wd[2], wd[3]);
-        st_shared_v4(ab + 128, wd[4], wd[5], wd[6], wd[7]);
-      } else {
-        int zo = (int)(sidx - s_first);
-        if (zo < 0 || zo >= kZRows) zo = 0;   // rows past the end of the batch (not stored)
-        const float* zr = zb + zo * kD;
+      int zo = (int)(sidx - s_first);
+      if (zo < 0 || zo >= kZRows) zo = 0;   // rows past the end of the batch (not stored)
+
+      // ---- split layer (Eq. 5, a3): h' = 2 GELU(z[s] + W2 x_p) -> A operand,
+      // 16 columns (8 independent element pairs) per block
+      const bool centre = (q == kQC);
+      const bool vert = p < kM - 1;
+      // centre lines: (z + W2[:,0]/2) + W2[:,1] y  or  (z + W2[:,1]/2) + W2[:,0] x;
+      // general queries (final phase): (z + W2[:,0]/2) + W2[:,0] (x - 1/2) + W2[:,1] y
+      const float* zs = zb + ((centre && !vert) ? kZRows * kD : 0) + zo * kD;
+      const float* w1s = S.w2 + ((centre && vert) ? kD : 0);
+      const float q1 = centre ? (vert ? qy : qx) : qx - 0.5f;
 #pragma unroll 1
-        for (int kh = 0; kh < 2; kh++) {   // K-half of the A image
-#ifndef MFP_SPLIT8
-          // 16 columns (two 8-column groups, 8 element pairs) per block, as in the
-          // hidden-layer epilogue: twice the independent GELU chains of one group
+      for (int kh = 0; kh < 2; kh++) {   // K-half of the A image
 #pragma unroll
-          for (int j16 = 0; j16 < 4; j16++) {
-            const int c0 = 64 * kh + 16 * j16;
-            float4 zz[4], aa[4], bb[4];
+        for (int j16 = 0; j16 < 4; j16++) {
+          const int c0 = 64 * kh + 16 * j16;
+          float v[16];
+          const f2 Q1 = f2_make(q1, q1);
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
-              zz[i] = *reinterpret_cast<const float4*>(zr + c0 + 4 * i);
-              aa[i] = *reinterpret_cast<const float4*>(S.w2 + c0 + 4 * i);
-              bb[i] = *reinterpret_cast<const float4*>(S.w2 + kD + c0 + 4 * i);
+          for (int i = 0; i < 4; i++) {
+            const float4 zz = *reinterpret_cast<const float4*>(zs + c0 + 4 * i);
+            const float4 aa = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
+            f2 v01 = ffma2(f2_make(aa.x, aa.y), Q1, f2_make(zz.x, zz.y));
+            f2 v23 = ffma2(f2_make(aa.z, aa.w), Q1, f2_make(zz.z, zz.w));
+            if (!centre) {
+              const float4 bb = *reinterpret_cast<const float4*>(S.w2 + kD + c0 + 4 * i);
+              const f2 QY = f2_make(qy, qy);
+              v01 = ffma2(f2_make(bb.x, bb.y), QY, v01);
+              v23 = ffma2(f2_make(bb.z, bb.w), QY, v23);
             }
-            const f2 QX = f2_make(qx, qx), QY = f2_make(qy, qy);
-            float v[16];
-#pragma unroll
-            for (int i = 0; i < 4; i++) {
-              f2_split(ffma2(f2_make(aa[i].x, aa[i].y), QX, ffma2(f2_make(bb[i].x, bb[i].y), QY, f2_make(zz[i].x, zz[i].y))),
-                       v[4 * i], v[4 * i + 1]);
-              f2_split(ffma2(f2_make(aa[i].z, aa[i].w), QX, ffma2(f2_make(bb[i].z, bb[i].w), QY, f2_make(zz[i].z, zz[i].w))),
-                       v[4 * i + 2], v[4 * i + 3]);
-            }
-            uint32_t w[8];
-            act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v), *reinterpret_cast<uint32_t(*)[4]>(w));
-            act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v + 8), *reinterpret_cast<uint32_t(*)[4]>(w + 4));
-            st_shared_v4(a_sw[2 * j16] + ((uint32_t)kh << 14), w[0], w[1], w[2], w[3]);
-            st_shared_v4(a_sw[2 * j16 + 1] + ((uint32_t)kh << 14), w[4], w[5], w[6], w[7]);
+            f2_split(v01, v[4 * i], v[4 * i + 1]);
+            f2_split(v23, v[4 * i + 2], v[4 * i + 3]);
           }
-#else
-#pragma unroll
-        for (int j8 = 0; j8 < 8; j8++) {   // 8-column group within the K-half
-          const int cc = 8 * kh + j8;
-          const float4 z0 = *reinterpret_cast<const float4*>(zr + cc * 8);
-          const float4 z1 = *reinterpret_cast<const float4*>(zr + cc * 8 + 4);
-          const float4 a0 = *reinterpret_cast<const float4*>(S.w2 + cc * 8);
-          const float4 a1 = *reinterpret_cast<const float4*>(S.w2 + cc * 8 + 4);
-          const float4 b0 = *reinterpret_cast<const float4*>(S.w2 + kD + cc * 8);
-          const float4 b1 = *reinterpret_cast<const float4*>(S.w2 + kD + cc * 8 + 4);
-          // z + W2 x_p in packed fp32x2: (z + b qy) + a qx per lane
-          const f2 QX = f2_make(qx, qx), QY = f2_make(qy, qy);
-          float v[8];
-          f2_split(ffma2(f2_make(a0.x, a0.y), QX, ffma2(f2_make(b0.x, b0.y), QY, f2_make(z0.x, z0.y))), v[0], v[1]);
-          f2_split(ffma2(f2_make(a0.z, a0.w), QX, ffma2(f2_make(b0.z, b0.w), QY, f2_make(z0.z, z0.w))), v[2], v[3]);
-          f2_split(ffma2(f2_make(a1.x, a1.y), QX, ffma2(f2_make(b1.x, b1.y), QY, f2_make(z1.x, z1.y))), v[4], v[5]);
-          f2_split(ffma2(f2_make(a1.z, a1.w), QX, ffma2(f2_make(b1.z, b1.w), QY, f2_make(z1.z, z1.w))), v[6], v[7]);
-          uint32_t w[4];
-          act8<GELU, F16>(v, w);
-          st_shared_v4(a_sw[j8] + ((uint32_t)kh << 14), w[0], w[1], w[2], w[3]);
-        }
-#endif
+          uint32_t w[8];
+          act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v), *reinterpret_cast<uint32_t(*)[4]>(w));
+          act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v + 8), *reinterpret_cast<uint32_t(*)[4]>(w + 4));
+          st_shared_v4(a_sw[2 * j16] + ((uint32_t)kh << 14), w[0], w[1], w[2], w[3]);
+          st_shared_v4(a_sw[2 * j16 + 1] + ((uint32_t)kh << 14), w[4], w[5], w[6], w[7]);
         }
       }
       if (lane == 0) MFP_TR(warp, j, 1, 3);
       fence_proxy_async();
       arrive_a();
       if (lane == 0) MFP_TR(warp, j, 0, 0);
+
+      // ---- hidden layers (a4) and head (a5): TMEM accumulator -> GELU ->
+      // next A operand, or GELU + head dot on the last layer
       f2 yacc = f2_make(0.f, 0.f);
-      for (int l = 0; l < nh + L0; l++) {
+      for (int l = 0; l < nh; l++) {
         mbar_wait(&S.bars[kSlots2 + slot], pd);
         if (lane == 0) MFP_TR(warp, j, l, 1);
         pd ^= 1u;
         tc_fence_after();
-        const bool last = (l == nh + L0 - 1);
-        // 16-column chunks, double-buffered: the TMEM read of chunk c + 1 (TMEM
-        // read bandwidth, 64 B/clk/SM, is a binding resource of this kernel)
-        // overlaps the activation of chunk c.
-        auto work16 = [&](const uint32_t (&r)[16], int c16) {
-          if (!last) {
+        // one layer over the 8 16-column TMEM chunks, loads double-buffered (the
+        // read of chunk c + 1 overlaps the activation of chunk c); LAST (a
+        // compile-time tag) selects 16-bit A operand or head dot
+        auto layer_epi = [&](auto last_tag) {
+          constexpr bool LAST = decltype(last_tag)::value;
+          auto work16 = [&](const uint32_t (&r)[16], int c16) {
+            if constexpr (!LAST) {
 #pragma unroll
-            for (int c8 = 0; c8 < 2; c8++) {
-              const int g = 2 * c16 + c8;   // 8-column group: K-half g / 8, 16-byte chunk (g % 8) ^ (row % 8)
-              float v[8];
+              for (int c8 = 0; c8 < 2; c8++) {
+                const int g = 2 * c16 + c8;   // 8-column group: K-half g / 8, chunk g % 8
+                float v[8];
 #pragma unroll
-              for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[c8 * 8 + e]);
-              uint32_t w[4];
-              act8<GELU, F16>(v, w);
-#ifndef MFP_EXPERIMENT_NO_STS
-              st_shared_v4(a_sw[g & 7] + ((uint32_t)(g >> 3) << 14), w[0], w[1], w[2], w[3]);
-#else
-              if (w[0] == 0x12345678u && w[1] == 0x9abcdef0u) st_shared_v4(a_row, w[0], w[1], w[2], w[3]);
-#endif
+                for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[c8 * 8 + e]);
+                uint32_t w[4];
+                act8<GELU, F16>(v, w);
+                st_shared_v4(a_sw[g & 7] + ((uint32_t)(g >> 3) << 14), w[0], w[1], w[2], w[3]);
+              }
+            } else {
+              head32<GELU, 16>(r, S.wo + c16 * 16, yacc);
             }
-          } else {
-            head32<GELU, 16>(r, S.wo + c16 * 16, yacc);
+          };
+          uint32_t ra[16], rb[16];
+          tmem_ld16(t_row, ra);
+          tmem_wait_ld_dep16(ra);
+#pragma unroll
+          for (int c16 = 0; c16 < kD / 16; c16 += 2) {
+            tmem_ld16(t_row + (uint32_t)((c16 + 1) * 16), rb);
+            work16(ra, c16);
+            tmem_wait_ld_dep16(rb);
+            if (c16 + 2 < kD / 16) tmem_ld16(t_row + (uint32_t)((c16 + 2) * 16), ra);
+            work16(rb, c16 + 1);
+            if (c16 + 2 < kD / 16) tmem_wait_ld_dep16(ra);
           }
         };
-        uint32_t ra[16], rb[16];
-#ifdef MFP_EXPERIMENT_NO_TMEM_LD
-#define tmem_ld16(addr, r) do { _Pragma("unroll") for (int _e = 0; _e < 16; _e++) r[_e] = (addr) + _e; } while (0)
-#endif
-        tmem_ld16(t_row, ra);
-        tmem_wait_ld_dep16(ra);
-#ifdef MFP_EPI_DYN
-#pragma unroll 1
-#else
-#pragma unroll
-#endif
-        for (int c16 = 0; c16 < kD / 16; c16 += 2) {
-          tmem_ld16(t_row + (uint32_t)((c16 + 1) * 16), rb);
-          work16(ra, c16);
-          tmem_wait_ld_dep16(rb);
-          if (c16 + 2 < kD / 16) tmem_ld16(t_row + (uint32_t)((c16 + 2) * 16), ra);
-          work16(rb, c16 + 1);
-          if (c16 + 2 < kD / 16) tmem_wait_ld_dep16(ra);
-        }
+        const bool last = (l == nh - 1);
+        if (last) layer_epi(std::true_type{});
+        else layer_epi(std::false_type{});
         if (lane == 0) MFP_TR(warp, j, l, 2);
-#ifdef MFP_EXPERIMENT_NO_TMEM_LD
-#undef tmem_ld16
-#endif
         tc_fence_before();
         if (!last) {
           fence_proxy_async();
@@ -859,15 +473,10 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
           if (lane == 0) MFP_TR(warp, j, l + 1, 0);
         }
       }
-      if constexpr (L0) {
-#pragma unroll
-        for (int i = 0; i < 3; i++) z3[i] = z3n[i];
-      } else {
-        if (have_next) *reinterpret_cast<float4*>(zb + zi) = znext;
-      }
+      if (have_next) z_stage(znext);
       float y0, y1;
       f2_split(yacc, y0, y1);
-      if (valid) sink_store(sink, sidx, p, (y0 + y1) + bo);
+      if (valid) sink_store(sink, sidx, p, (y0 + y1) + bo);   // a6 / final-phase field
     }
   }
   tc_fence_before();
@@ -881,265 +490,6 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
 
 }  // namespace tc2
 
-// ---------------------------------------------------------------------------
-// CTA-pair variant with 8 epilogue warps per slot (tc3): 3 slots x 8 warps,
-// two warps per TMEM lane quadrant splitting the 128 columns (64 each).  The
-// chain epilogue is latency bound at 4 warps per SMSP (removing
-// MUFU, TMEM loads or the smem stores one at a time barely moves it), so this
-// trades one tile slot for 1.5x the warps (6 per SMSP) at 72 registers.
-namespace tc3 {
-using namespace tc;
-using tc2::cluster_rank;
-using tc2::cluster_sync;
-using tc2::mbar_arrive_remote;
-using tc2::mbar_wait_cluster;
-using tc2::mma2;
-using tc2::commit2;
-
-constexpr int kSlots3 = 3;
-constexpr int kEpi3 = 8 * kSlots3;                 // 24 epilogue warps
-constexpr int kAlloc3 = kEpi3, kIssue3 = kEpi3 + 1;  // issuer: highest warp id
-constexpr int kThreads3 = 32 * (kEpi3 + 2);        // 832
-constexpr int kHalf3 = kWImg;
-
-struct Smem3 {
-  uint8_t* W;      // [nh][18 KB]
-  uint8_t* A;      // [3][32 KB]
-  uint8_t* ones;   // 4 KB
-  float* zbuf;     // [3][4][128]
-  float* w2;       // [2][128]
-  float* wo;       // [128]
-  float* ypart;    // [3][128] head partial sums of the upper column half
-  uint64_t* bars;  // a_full[3], d_full[3]
-  uint32_t* tmem_slot;
-};
-
-__device__ __forceinline__ Smem3 carve3(uint8_t* raw, int nh) {
-  Smem3 s;
-  s.W = raw;
-  s.A = raw + nh * kHalf3;
-  s.ones = s.A + kSlots3 * kTile;
-  s.zbuf = (float*)(s.ones + kOnes);
-  s.w2 = s.zbuf + kSlots3 * kZRows * kD;
-  s.wo = s.w2 + 2 * kD;
-  s.ypart = s.wo + kD;
-  s.bars = (uint64_t*)(s.ypart + kSlots3 * kD);
-  s.tmem_slot = (uint32_t*)(s.bars + 2 * kSlots3);
-  return s;
-}
-
-size_t smem_bytes3(int n_hidden) {
-  return (size_t)n_hidden * kHalf3 + kSlots3 * kTile + kOnes +
-         4 * ((size_t)kSlots3 * kZRows * kD + 3 * kD + kSlots3 * kD) + 16 * kSlots3 + 16;
-}
-
-template <int GELU, int F16>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads3, 1)
-k_chain_tc3(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, Sink sink) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const int nh = net.n_hidden;
-  const Smem3 S = carve3(smem_raw, nh);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-
-  {
-    for (int l = 0; l < nh; l++) {
-      const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(net.Wh_sw2) +
-                                                        (size_t)l * 2 * kHalf3 + rank * kHalf3);
-      uint4* dst = reinterpret_cast<uint4*>(S.W + l * kHalf3);
-      for (int i = threadIdx.x; i < kHalf3 / 16; i += kThreads3) dst[i] = __ldg(src + i);
-    }
-    for (int i = threadIdx.x; i < kD; i += kThreads3) {
-      S.wo[i] = (GELU == 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
-      S.w2[i] = __ldg(net.W2 + 2 * i);
-      S.w2[kD + i] = __ldg(net.W2 + 2 * i + 1);
-    }
-    if (threadIdx.x < kRows) {
-      const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
-      const int r = threadIdx.x;
-      *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + (r & 7) * 16) = make_uint4(one | (one << 16), 0u, 0u, 0u);
-      *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + 128 + (r & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
-    }
-  }
-  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kSlots3; s++) {
-      mbar_init(&S.bars[s], 16);            // a_full[s]: 8 warps x 2 CTAs
-      mbar_init(&S.bars[kSlots3 + s], 1);   // d_full[s]: multicast commit
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == kAlloc3) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
-                 "r"(kTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-  }
-  fence_proxy_async();
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem = *S.tmem_slot;
-
-  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  const int64_t ntiles = (total_rows + 2 * kRows - 1) / (2 * kRows);
-  const int64_t nloc = ntiles > cid ? (ntiles - cid + ncl - 1) / ncl : 0;
-  const int64_t nsub = total_rows / q;
-
-  if (warp == kIssue3) {
-    if (rank == 0 && lane == 0) {
-      uint32_t pa[kSlots3] = {0u, 0u, 0u};
-      const uint32_t ones_addr = smem_u32(S.ones);
-      for (int64_t j0 = 0; j0 < nloc; j0 += kSlots3) {
-        for (int l = 0; l < nh; l++) {
-#pragma unroll
-          for (int s = 0; s < kSlots3; s++) {
-            if (j0 + s >= nloc) continue;
-            mbar_wait_cluster(&S.bars[s], pa[s]);
-            pa[s] ^= 1u;
-            tc_fence_after();
-            const uint32_t d = tmem + (uint32_t)(s * kD);
-            const uint32_t a0 = smem_u32(S.A + s * kTile), b0 = smem_u32(S.W + l * kHalf3);
-#pragma unroll
-            for (int k = 0; k < kD / 16; k++) {
-              const uint32_t offa = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
-              const uint32_t offb = (uint32_t)((k >> 2) * 8192 + (k & 3) * 32);
-              mma2<F16>(d, sw128_desc(a0 + offa), sw128_desc(b0 + offb), k > 0 ? 1u : 0u);
-            }
-            mma2<F16>(d, nosw_desc(ones_addr), nosw_desc(b0 + 16384u), 1u);
-            commit2(&S.bars[kSlots3 + s]);
-          }
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp < kEpi3) {
-    const int slot = warp >> 3;
-    const int half = (warp >> 2) & 1;               // column half: 64 half .. 64 half + 63
-    const int quad = warp & 3;                      // TMEM lane quadrant
-    const int row = quad * 32 + lane;
-    const int tid8 = (half * 4 + quad) * 32 + lane;  // 0..255 within the slot
-    const uint32_t a_row = smem_u32(S.A + slot * kTile) + (uint32_t)row * 128u;
-    const int r7 = row & 7;
-    const uint32_t t_row = tmem + (uint32_t)(slot * kD + 64 * half) + ((uint32_t)(quad * 32) << 16);
-    float* zb = S.zbuf + slot * kZRows * kD;
-    const float bo = __ldg(net.bo);
-    const int zi = 2 * tid8, zr_ = zi >> 7, zc = zi & 127;
-    auto row0_of = [&](int64_t j) -> int64_t { return (cid + j * ncl) * (2 * kRows) + rank * kRows; };
-    auto z_fetch = [&](int64_t j) -> float2 {
-      int64_t sidx = row0_of(j) / q + zr_;
-      if (sidx > nsub - 1) sidx = nsub - 1;
-      return __ldg(reinterpret_cast<const float2*>(z + sidx * kD + zc));
-    };
-    auto arrive_a = [&]() {
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote(&S.bars[slot], 0u);
-    };
-    auto store8 = [&](int g, const uint32_t (&w)[4]) {   // 8-column group g of this row
-      st_shared_v4(a_row + ((uint32_t)(g >> 3) << 14) + ((uint32_t)((g & 7) ^ r7) << 4), w[0], w[1], w[2], w[3]);
-    };
-    if (slot < nloc) *reinterpret_cast<float2*>(zb + zi) = z_fetch(slot);
-    uint32_t pd = 0u;
-    for (int64_t j = slot; j < nloc; j += kSlots3) {
-      const int64_t row0 = row0_of(j);
-      int64_t s_first = row0 / q;
-      if (s_first > nsub - 1) s_first = nsub - 1;
-      named_sync(1 + slot, 256);                    // zbuf of this tile visible to the slot's 8 warps
-      const bool have_next = j + kSlots3 < nloc;
-      float2 znext = make_float2(0.f, 0.f);
-      if (have_next) znext = z_fetch(j + kSlots3);
-      const int64_t grow = row0 + row;
-      const bool valid = grow < total_rows;
-      const int64_t gr = valid ? grow : total_rows - 1;
-      const int64_t sidx = gr / q;
-      const int p = (int)(gr - sidx * q);
-      float qx, qy;
-      query_xy(q, p, &qx, &qy);
-      {
-        int zo = (int)(sidx - s_first);
-        if (zo < 0 || zo >= kZRows) zo = 0;
-        const float* zr = zb + zo * kD;
-        const f2 QX = f2_make(qx, qx), QY = f2_make(qy, qy);
-#pragma unroll 2
-        for (int i = 0; i < 8; i++) {
-          const int cc = 8 * half + i;
-          const float4 z0 = *reinterpret_cast<const float4*>(zr + cc * 8);
-          const float4 z1 = *reinterpret_cast<const float4*>(zr + cc * 8 + 4);
-          const float4 a0 = *reinterpret_cast<const float4*>(S.w2 + cc * 8);
-          const float4 a1 = *reinterpret_cast<const float4*>(S.w2 + cc * 8 + 4);
-          const float4 b0 = *reinterpret_cast<const float4*>(S.w2 + kD + cc * 8);
-          const float4 b1 = *reinterpret_cast<const float4*>(S.w2 + kD + cc * 8 + 4);
-          float v[8];
-          f2_split(ffma2(f2_make(a0.x, a0.y), QX, ffma2(f2_make(b0.x, b0.y), QY, f2_make(z0.x, z0.y))), v[0], v[1]);
-          f2_split(ffma2(f2_make(a0.z, a0.w), QX, ffma2(f2_make(b0.z, b0.w), QY, f2_make(z0.z, z0.w))), v[2], v[3]);
-          f2_split(ffma2(f2_make(a1.x, a1.y), QX, ffma2(f2_make(b1.x, b1.y), QY, f2_make(z1.x, z1.y))), v[4], v[5]);
-          f2_split(ffma2(f2_make(a1.z, a1.w), QX, ffma2(f2_make(b1.z, b1.w), QY, f2_make(z1.z, z1.w))), v[6], v[7]);
-          uint32_t w[4];
-          act8<GELU, F16>(v, w);
-          store8(cc, w);
-        }
-      }
-      fence_proxy_async();
-      arrive_a();
-      f2 yacc = f2_make(0.f, 0.f);
-      for (int l = 0; l < nh; l++) {
-        mbar_wait(&S.bars[kSlots3 + slot], pd);
-        pd ^= 1u;
-        tc_fence_after();
-        const bool last = (l == nh - 1);
-        auto work16 = [&](const uint32_t (&r)[16], int c16) {
-          if (!last) {
-#pragma unroll
-            for (int c8 = 0; c8 < 2; c8++) {
-              float v[8];
-#pragma unroll
-              for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[c8 * 8 + e]);
-              uint32_t w[4];
-              act8<GELU, F16>(v, w);
-              store8(8 * half + 2 * c16 + c8, w);
-            }
-          } else {
-            head32<GELU, 16>(r, S.wo + 64 * half + c16 * 16, yacc);
-          }
-        };
-        uint32_t ra[16], rb[16];
-        tmem_ld16(t_row, ra);
-        tmem_wait_ld_dep16(ra);
-        tmem_ld16(t_row + 16u, rb);
-        work16(ra, 0);
-        tmem_wait_ld_dep16(rb);
-        tmem_ld16(t_row + 32u, ra);
-        work16(rb, 1);
-        tmem_wait_ld_dep16(ra);
-        tmem_ld16(t_row + 48u, rb);
-        work16(ra, 2);
-        tmem_wait_ld_dep16(rb);
-        work16(rb, 3);
-        tc_fence_before();
-        if (!last) {
-          fence_proxy_async();
-          arrive_a();
-        }
-      }
-      if (have_next) *reinterpret_cast<float2*>(zb + zi) = znext;
-      float y0, y1;
-      f2_split(yacc, y0, y1);
-      if (half) S.ypart[slot * kD + row] = y0 + y1;
-      named_sync(4 + slot, 256);                    // upper-half partial sums visible
-      if (!half && valid) sink_store(sink, sidx, p, ((y0 + y1) + S.ypart[slot * kD + row]) + bo);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();
-  if (warp == kAlloc3) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
-  }
-}
-
-}  // namespace tc3
 
 bool chain_tc_available() { return true; }
 
@@ -1150,88 +500,31 @@ extern "C" int mfp_debug_trace(void* host, size_t bytes) {
 }
 #endif
 
-// Variant: 2 = CTA pair (default), 1 = single-CTA 3-slot kernel (MFP_CHAIN_VARIANT=1,
-// kept for A/B measurement).
-static int chain_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MFP_CHAIN_VARIANT");
-    v = (e && (e[0] == '1' || e[0] == '3')) ? e[0] - '0' : 2;
-  }
-  return v;
-}
-
-// Opt-in shared-memory sizes, set once from mfp_init (never inside a graph capture).
+// Opt-in shared-memory size, set once from mfp_init (never inside a graph capture).
 void tc_kernel_attributes() {
-  const int mx3 = (int)tc3::smem_bytes3(kMaxHidden);
-  cudaFuncSetAttribute(tc3::k_chain_tc3<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx3);
-  cudaFuncSetAttribute(tc3::k_chain_tc3<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx3);
-  cudaFuncSetAttribute(tc3::k_chain_tc3<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx3);
-  cudaFuncSetAttribute(tc3::k_chain_tc3<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx3);
   const int mx2 = (int)tc2::smem_bytes2(kMaxHidden);
-  cudaFuncSetAttribute(tc2::k_chain_tc2<0, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
-  cudaFuncSetAttribute(tc2::k_chain_tc2<0, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
-  cudaFuncSetAttribute(tc2::k_chain_tc2<0, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
-  cudaFuncSetAttribute(tc2::k_chain_tc2<0, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
-  cudaFuncSetAttribute(tc2::k_chain_tc2<1, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
-  cudaFuncSetAttribute(tc2::k_chain_tc2<1, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
-  cudaFuncSetAttribute(tc2::k_chain_tc2<1, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
-  cudaFuncSetAttribute(tc2::k_chain_tc2<1, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
-  const int mx = (int)tc::smem_bytes(kMaxHidden);
-  cudaFuncSetAttribute(tc::k_chain_tc<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(tc::k_chain_tc<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(tc::k_chain_tc<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(tc::k_chain_tc<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
 }
 
+// Persistent grid: one CTA pair per TPC (74 clusters), or fewer for small batches.
 void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const Sink& sink, int num_sms,
                      cudaStream_t s) {
   if (B <= 0) return;
   const int64_t rows = B * q;
-  if (chain_variant() == 3) {
-    const size_t sm = tc3::smem_bytes3(net.n_hidden);
-    const int64_t ptiles = (rows + 2 * tc::kRows - 1) / (2 * tc::kRows);
-    const int64_t pairs = num_sms / 2;
-    const int grid = 2 * (int)(ptiles < pairs ? ptiles : pairs);
-#define MFP_TC3(G, F) tc3::k_chain_tc3<G, F><<<grid, tc3::kThreads3, sm, s>>>(z, rows, q, net, sink)
-    if (net.f16) {
-      if (net.gelu_tanh) MFP_TC3(1, 1); else MFP_TC3(0, 1);
-    } else {
-      if (net.gelu_tanh) MFP_TC3(1, 0); else MFP_TC3(0, 0);
-    }
-#undef MFP_TC3
-    return;
-  }
-  if (chain_variant() == 2) {
-    const size_t sm = tc2::smem_bytes2(net.n_hidden);
-    const int64_t ptiles = (rows + 2 * tc::kRows - 1) / (2 * tc::kRows);
-    const int64_t pairs = num_sms / 2;
-    const int grid = 2 * (int)(ptiles < pairs ? ptiles : pairs);
-    // Split layer z + W2 x_p: on the CUDA cores from the smem z tile (default),
-    // or MFP_L0_MMA=1 as one K = 16 MMA — which costs a fourth TMEM read of the
-    // accumulator per tile (TMEM read bandwidth binds): slower.
-    static const int l0 = (getenv("MFP_L0_MMA") && getenv("MFP_L0_MMA")[0] == '1') ? 1 : 0;
-#define MFP_TC2(G, F, L) tc2::k_chain_tc2<G, F, L><<<grid, tc2::kThreads2, sm, s>>>(z, rows, q, net, sink)
-#define MFP_TC2L(G, F) do { if (l0) MFP_TC2(G, F, 1); else MFP_TC2(G, F, 0); } while (0)
-    if (net.f16) {
-      if (net.gelu_tanh) MFP_TC2L(1, 1); else MFP_TC2L(0, 1);
-    } else {
-      if (net.gelu_tanh) MFP_TC2L(1, 0); else MFP_TC2L(0, 0);
-    }
-#undef MFP_TC2L
-#undef MFP_TC2
-    return;
-  }
-  const size_t sm = tc::smem_bytes(net.n_hidden);
-  const int64_t tiles = (rows + tc::kRows - 1) / tc::kRows;
-  const int grid = (int)(tiles < num_sms ? tiles : num_sms);
+  const size_t sm = tc2::smem_bytes2(net.n_hidden);
+  const int64_t ptiles = (rows + 2 * tc::kRows - 1) / (2 * tc::kRows);
+  const int64_t pairs = num_sms / 2;
+  const int grid = 2 * (int)(ptiles < pairs ? ptiles : pairs);
+#define MFP_TC2(G, F) tc2::k_chain_tc2<G, F><<<grid, tc2::kThreads2, sm, s>>>(z, rows, q, net, sink)
   if (net.f16) {
-    if (net.gelu_tanh) tc::k_chain_tc<1, 1><<<grid, tc::kThreads, sm, s>>>(z, rows, q, net, sink);
-    else tc::k_chain_tc<0, 1><<<grid, tc::kThreads, sm, s>>>(z, rows, q, net, sink);
+    if (net.gelu_tanh) MFP_TC2(1, 1); else MFP_TC2(0, 1);
   } else {
-    if (net.gelu_tanh) tc::k_chain_tc<1, 0><<<grid, tc::kThreads, sm, s>>>(z, rows, q, net, sink);
-    else tc::k_chain_tc<0, 0><<<grid, tc::kThreads, sm, s>>>(z, rows, q, net, sink);
+    if (net.gelu_tanh) MFP_TC2(1, 0); else MFP_TC2(0, 0);
   }
+#undef MFP_TC2
 }
 
 }  // namespace mfp

@@ -31,9 +31,7 @@ assert f(buf.ctypes.data, buf.nbytes) > 0
 np.save("gpurun_out/chain_trace.npy", buf)
 T = buf[0].astype(np.int64)
 acts, rts, iss, exe, comp, fin, l0, l0s, tails = [], [], [], [], [], [], [], [], []
-L = 3   # layers with an MMA (L0 SIMT default); MFP_L0_MMA=1 -> 4
-if (T[17, 5, 3, 0] > 0):
-    L = 4
+L = 3   # layers with an MMA (the split layer runs on the CUDA cores)
 for tile in range(4, 28):
     slot = tile % 4
     ws = [4 * slot + q for q in range(4)]
