@@ -94,6 +94,19 @@ struct mfp_ctx {
 
 namespace {
 
+}  // namespace
+
+bool mfp::pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MFP_NO_PDL");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+namespace {
+
 const int kKindGather = 0, kKindChain = 1, kKindExact = 2, kKindHalo = 3, kKindDelta = 4;
 
 mfp_status fail(mfp_ctx* c, mfp_status st, const std::string& msg) {

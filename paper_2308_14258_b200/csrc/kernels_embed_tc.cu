@@ -71,6 +71,8 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_launch_dependents();
+  pdl_wait();      // the lattice (previous phase's scatter) and z's readers complete from here on
   const int i0 = 4 * lane;
   const uint32_t a_hi = smem_u32(sAhi), a_lo = smem_u32(sAlo);
   uint32_t phase = 0u;
@@ -167,9 +169,9 @@ void launch_embed_tc(const float* lat, const LatticeGeom& L, const uint32_t* anc
   if (blocks > 148) blocks = 148;
   const size_t sm = emb::smem_bytes();
   if (net.gelu_tanh)
-    emb::k_embed_tc<1><<<(int)blocks, emb::kThreadsE, sm, s>>>(lat, L, anchors, gb, B, net, z);
+    launch_pdl(emb::k_embed_tc<1>, (int)blocks, emb::kThreadsE, sm, s, lat, L, anchors, gb, B, net, z);
   else
-    emb::k_embed_tc<0><<<(int)blocks, emb::kThreadsE, sm, s>>>(lat, L, anchors, gb, B, net, z);
+    launch_pdl(emb::k_embed_tc<0>, (int)blocks, emb::kThreadsE, sm, s, lat, L, anchors, gb, B, net, z);
 }
 
 }  // namespace mfp

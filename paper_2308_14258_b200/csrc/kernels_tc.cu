@@ -279,6 +279,8 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
   cluster_sync();  // both CTAs' barriers initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tmem = *S.tmem_slot;
+  pdl_launch_dependents();
+  pdl_wait();      // z (embed) and the lattice (previous phases) complete from here on
 
   const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int64_t ntiles = (total_rows + 2 * kRows - 1) / (2 * kRows);
@@ -518,7 +520,7 @@ void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const 
   const int64_t ptiles = (rows + 2 * tc::kRows - 1) / (2 * tc::kRows);
   const int64_t pairs = num_sms / 2;
   const int grid = 2 * (int)(ptiles < pairs ? ptiles : pairs);
-#define MFP_TC2(G, F) tc2::k_chain_tc2<G, F><<<grid, tc2::kThreads2, sm, s>>>(z, rows, q, net, sink)
+#define MFP_TC2(G, F) launch_pdl(tc2::k_chain_tc2<G, F>, grid, tc2::kThreads2, sm, s, z, rows, q, net, sink)
   if (net.f16) {
     if (net.gelu_tanh) MFP_TC2(1, 1); else MFP_TC2(0, 1);
   } else {

@@ -116,6 +116,26 @@ struct Sink {
   float* out;
 };
 
+// Launch with programmatic stream serialization (PDL, see tc_common.cuh) so the
+// kernel's prologue overlaps its predecessor's tail; MFP_NO_PDL=1 launches
+// plainly (A/B).  The kernel must call griddepcontrol.wait before touching
+// anything its predecessors write.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // ---- kernel launchers (kernels_*.cu) --------------------------------------
 void launch_init_lattice(float* lat, const LatticeGeom& L, int nx, int ny, const float* g,
                          cudaStream_t s);
