@@ -47,6 +47,9 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--precision", default="bf16", choices=["bf16", "fp16", "fp32"])
     p.add_argument("--no-converge", action="store_true")
+    p.add_argument("--no-extras", action="store_true",
+                   help="skip the legs after the timed region (e2e, sweep, boundary IO, CPU baseline): "
+                        "used for the ncu launch list of the step")
     return p.parse_args()
 
 
@@ -321,6 +324,17 @@ def main():
 
     # e2e through the public host API: H2D of g + D2H of u inside the timed
     # region, from / into pinned host buffers
+    if args.no_extras:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": PRED_PER_ITER * T * args.steps / (ms / 1000.0),
+                              "unit": "predictions/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                              "ms_per_step": ms / args.steps, "note": "--no-extras (launch-list run)"}), flush=True)
+        m.close()
+        if comm is not None:
+            mfp.mfp_nccl_comm_destroy(comm)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     u_pin = torch.empty((NY + 1, NX + 1) if rank == 0 else (1, 1), dtype=torch.float32).pin_memory()
     g_pin = torch.from_numpy(g_host).pin_memory()
     u_host, g_host = u_pin.numpy(), g_pin.numpy()

@@ -47,6 +47,12 @@ def closed_form_boundary(nx: int, ny: int, f, h: float = 1.0 / 64.0) -> np.ndarr
     return np.asarray(f(p[:, 0], p[:, 1]), np.float64)
 
 
+def sine_boundary(nx: int, ny: int, h: float = 1.0 / 64.0) -> np.ndarray:
+    """The paper's evaluation boundary g(x) = sin(2 pi x) (Fig. gfnet-eval),
+    x in domain units (64 points per unit), on every boundary point (fp64)."""
+    return closed_form_boundary(nx, ny, lambda x, y: np.sin(2.0 * np.pi * x), h)
+
+
 def sobol_2d(k: int) -> tuple[float, float]:
     import warnings
 

@@ -703,6 +703,7 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
   }
   if (cfg->subsolver == MFP_SDNET) {
     CK(cudaMemcpyAsync(c->params, params, n_params * sizeof(float), cudaMemcpyHostToDevice, s));
+    for (int i = 0; i < 89; i++) c->dn.convw[i] = params[i];   // MFCK order: conv1 w, b, conv2 w, b
     CK(cudaMemsetAsync((void*)c->dn.Wh_sw, 0, (size_t)net->n_hidden * kWImg * 2, s));
     CK(cudaMemsetAsync((void*)c->dn.Wh_sw2, 0, (size_t)net->n_hidden * kWImg * 2, s));
     PrepArgs a;

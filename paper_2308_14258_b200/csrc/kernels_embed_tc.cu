@@ -31,6 +31,65 @@ constexpr int kPerWarp = kRowsE / 16;
 
 size_t smem_bytes() { return 4 * (size_t)kImg + 4 * (96 + kD) + 64; }
 
+// The conv stack of TWO subdomains at once: every value is an fp32 pair
+// (subdomain A, subdomain B) at the same perimeter position, so each weight is
+// one broadcast operand of a packed FFMA2 (half the FMA instructions of the
+// scalar stack, twice the independent work per lane); weights come from the
+// kernel-parameter constant bank (DevNet::convw).
+__device__ __forceinline__ f2 shfl2(f2 v, int src) {
+  return f2{__shfl_sync(0xffffffffu, v.v, src)};
+}
+__device__ __forceinline__ void circ_window2(const f2 (&v)[4], int lane, f2 (&w)[8]) {
+  const int left = (lane + 31) & 31, right = (lane + 1) & 31;
+  w[0] = shfl2(v[2], left);
+  w[1] = shfl2(v[3], left);
+  w[2] = v[0]; w[3] = v[1]; w[4] = v[2]; w[5] = v[3];
+  w[6] = shfl2(v[0], right);
+  w[7] = shfl2(v[1], right);
+}
+template <int GELU>
+__device__ __forceinline__ f2 emb_act2(f2 x) {
+  if constexpr (GELU == 1) {
+    float u0, u1;
+    f2_split(fmul2(x, ffma2(fmul2(x, x), f2_make(kGF1, kGF1), f2_make(kGF0, kGF0))), u0, u1);
+    const f2 hx = fmul2(x, f2_make(0.5f, 0.5f));
+    return ffma2(hx, f2_make(tanh_approx(u0), tanh_approx(u1)), hx);   // x/2 (1 + tanh u)
+  } else {
+    float a, b;
+    f2_split(x, a, b);
+    return f2_make(gelu_erf(a), gelu_erf(b));
+  }
+}
+template <int GELU>
+__device__ __forceinline__ void conv_stack2(const f2 (&g4)[4], int lane, const DevNet& net, f2 (&e)[4]) {
+  const float* cw = net.convw;
+  f2 win[8];
+  circ_window2(g4, lane, win);
+  f2 acc2[4];
+#pragma unroll
+  for (int p = 0; p < 4; p++) acc2[p] = f2_make(cw[88], cw[88]);
+#pragma unroll
+  for (int o = 0; o < kC1; o++) {
+    f2 c1v[4];
+#pragma unroll
+    for (int p = 0; p < 4; p++) {
+      f2 v = f2_make(cw[40 + o], cw[40 + o]);
+#pragma unroll
+      for (int t = 0; t < kK; t++) v = ffma2(f2_make(cw[o * kK + t], cw[o * kK + t]), win[p + t], v);
+      c1v[p] = emb_act2<GELU>(v);
+    }
+    f2 w2[8];
+    circ_window2(c1v, lane, w2);
+#pragma unroll
+    for (int p = 0; p < 4; p++)
+#pragma unroll
+      for (int t = 0; t < kK; t++)
+        acc2[p] = ffma2(f2_make(cw[48 + o * kK + t], cw[48 + o * kK + t]), w2[p + t], acc2[p]);
+  }
+#pragma unroll
+  for (int p = 0; p < 4; p++) e[p] = emb_act2<GELU>(acc2[p]);
+}
+
 template <int GELU>
 __global__ void __launch_bounds__(kThreadsE, 1)
 k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ anchors,
@@ -86,11 +145,21 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
       gpre[j] = gb ? __ldg(reinterpret_cast<const float4*>(gb + s * kNB + i0)) : gather4(lat, L, __ldg(anchors + s), lane);
     }
 #pragma unroll
-    for (int j = 0; j < kPerWarp; j++) {
-      const int row = warp * kPerWarp + j;
-      const float g4[4] = {gpre[j].x, gpre[j].y, gpre[j].z, gpre[j].w};
+    for (int jp = 0; jp < kPerWarp; jp += 2) {
+      const f2 g4[4] = {f2_make(gpre[jp].x, gpre[jp + 1].x), f2_make(gpre[jp].y, gpre[jp + 1].y),
+                        f2_make(gpre[jp].z, gpre[jp + 1].z), f2_make(gpre[jp].w, gpre[jp + 1].w)};
+      f2 e2[4];
+      conv_stack2<GELU>(g4, lane, net, e2);
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+      const int row = warp * kPerWarp + jp + h;
       float e[4];
-      conv_stack<GELU>(g4, lane, sCw, e);
+#pragma unroll
+      for (int p = 0; p < 4; p++) {
+        float lo, hi;
+        f2_split(e2[p], lo, hi);
+        e[p] = h ? hi : lo;
+      }
       // e = e_hi + e_lo, both bf16 (round to nearest)
       uint32_t h01, h23, l01, l23;
       asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h01) : "f"(e[1]), "f"(e[0]));
@@ -102,6 +171,7 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
       const uint32_t off = sw128_off(row, i0) + (uint32_t)((i0 & 7) * 2);
       asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a_hi + off), "r"(h01), "r"(h23) : "memory");
       asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a_lo + off), "r"(l01), "r"(l23) : "memory");
+      }
     }
     fence_proxy_async();
     __syncthreads();

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle
-from mfp_inputs import closed_form_boundary, gp_boundary
+from mfp_inputs import boundary_points, closed_form_boundary, gp_boundary
 from tests._refsolve import dst_laplace, sparse_laplace
 
 M = 32
@@ -113,6 +113,38 @@ def test_exp_sin_vs_discrete_solution():
     X, Y = np.meshgrid(np.arange(nx + 1) * h, np.arange(ny + 1) * h)
     err = np.max(np.abs(res.u - f(X, Y)))
     assert 1e-8 < err < 1e-5
+
+
+def sine_discrete_solution(nx, ny, h):
+    """Closed-form solution of the 5-point Dirichlet problem with g = sin(2 pi x)
+     when nx h is an integer: separation of variables on the grid,
+    u_ij = sin(2 pi i h) v_j, v_{j+1} + v_{j-1} = (4 - 2 cos 2 pi h) v_j, v_0 = v_ny = 1
+    => v_j = (sinh(l (ny - j)) + sinh(l j)) / sinh(l ny), cosh l = 2 - cos(2 pi h)."""
+    lam = np.arccosh(2.0 - np.cos(2.0 * np.pi * h))
+    j = np.arange(ny + 1)
+    v = (np.sinh(lam * (ny - j)) + np.sinh(lam * j)) / np.sinh(lam * ny)
+    return np.sin(2.0 * np.pi * np.arange(nx + 1) * h)[None, :] * v[:, None]
+
+
+def test_sine_boundary_discrete_closed_form():
+    """P:158's evaluation boundary sin(2 pi x): the converged exact-subsolver MFP
+    equals the grid's separable closed form to 1e-8 (and that closed form is the
+    continuous solution sin(2 pi x)(sinh 2pi(H-y) + sinh 2pi y)/sinh 2pi H to O(h^2))."""
+    from mfp_inputs import sine_boundary
+    nx, ny = 2 * M, 4 * M            # 1 x 2 units (the paper's smallest domain, P:167)
+    h = 1.0 / 64.0
+    g = sine_boundary(nx, ny, h)
+    ref = sine_discrete_solution(nx, ny, h)
+    bp = boundary_points(nx, ny)
+    assert np.max(np.abs(ref[bp[:, 1], bp[:, 0]] - g)) < 1e-14   # the closed form meets g
+    assert np.max(np.abs(ref - dst_laplace(nx, ny, g))) < 1e-12    # and is the discrete solution
+    res = oracle.mfp_run(oracle.MfpConfig(nx, ny, subsolver="exact"), g, t=2000, tol=1e-14)
+    assert np.max(np.abs(res.u - ref)) < 1e-8
+    X, Y = np.meshgrid(np.arange(nx + 1) * h, np.arange(ny + 1) * h)
+    H = ny * h
+    cont = np.sin(2 * np.pi * X) * (np.sinh(2 * np.pi * (H - Y)) + np.sinh(2 * np.pi * Y)) / np.sinh(2 * np.pi * H)
+    err = np.max(np.abs(ref - cont))
+    assert 1e-6 < err < 2e-3                                     # O((2 pi h)^2) discretisation gap
 
 
 def test_linearity():
