@@ -101,6 +101,18 @@ def sample_boundaries(torch, n, device, gen):
     mask = (torch.rand(k, 4, device=device, generator=gen) < 0.35).float()
     mask = mask.repeat_interleave(M, dim=1)
     out[k:2 * k] = src * (1 - mask)
+    if SMOOTH > 0:
+        # (d) harmonic polynomials of degree <= 3 with random coefficients: what a
+        # subdomain sees near convergence on a large domain, where the MFP's slowly
+        # contracting iteration amplifies any systematic error of the subsolver
+        ns = int(n * SMOOTH)
+        x = pp[None, :, 0] - 0.5
+        y = pp[None, :, 1] - 0.5
+        basis = torch.stack([torch.ones_like(x[0]), x[0], y[0], x[0] ** 2 - y[0] ** 2, x[0] * y[0],
+                             x[0] ** 3 - 3 * x[0] * y[0] ** 2, 3 * x[0] ** 2 * y[0] - y[0] ** 3], 0)   # (7, 128)
+        c = torch.randn(ns, 7, device=device, generator=gen) * torch.tensor(
+            [0.5, 0.6, 0.6, 0.5, 0.5, 0.3, 0.3], device=device)
+        out[n - ns:] = c @ basis
     if not WIDE:
         return out
     # random offsets and scales (harmonic extension commutes with both)
@@ -110,6 +122,7 @@ def sample_boundaries(torch, n, device, gen):
 
 
 WIDE = False  # --wide: add random offsets / scales to the boundary mixture
+SMOOTH = 0.0  # --smooth f: fraction of the batch replaced by harmonic polynomials (degree <= 3)
 
 
 def main():
@@ -124,12 +137,14 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--out", default=os.path.join(ROOT, "weights", "sdnet_fit_d128.npy"))
     ap.add_argument("--wide", action="store_true")
+    ap.add_argument("--smooth", type=float, default=0.0)
     ap.add_argument("--normalized-loss", action="store_true")
     ap.add_argument("--init", default=None, help="start from these flat weights (MFCK order)")
     ap.add_argument("--eval", action="store_true", help="only evaluate --init")
     args = ap.parse_args()
-    global WIDE
+    global WIDE, SMOOTH
     WIDE = args.wide
+    SMOOTH = args.smooth
     dev = torch.device("cuda" if torch.cuda.is_available() else "cpu")
     torch.manual_seed(args.seed)
     gen = torch.Generator(device=dev)

@@ -58,16 +58,22 @@ def main():
     ap.add_argument("--chunk", type=int, default=50)
     ap.add_argument("--max", type=int, default=20000)
     ap.add_argument("--target", type=float, default=0.05)
+    ap.add_argument("--weights", default=os.path.join(ROOT, "weights", "sdnet_fit_d128.npy"))
+    ap.add_argument("--only", default="", help="comma list of subsolver names to run (default all)")
+    ap.add_argument("--grids", default="1x1,1x2,2x2,2x4")
     a = ap.parse_args()
     g = gp_boundary(a.n, a.n, 0)
     ref = dst_laplace(a.n, a.n, g.astype(np.float64))
     ref_dev = torch.from_numpy(ref.astype(np.float32)).cuda()
-    wfit = np.load(os.path.join(ROOT, "weights", "sdnet_fit_d128.npy"))
+    wfit = np.load(a.weights)
+    grids = [tuple(int(v) for v in x.split("x")) for x in a.grids.split(",")]
     out = []
     for name, sub, prec, w in [("exact fp32", mfp.EXACT_LAPLACE, mfp.FP32, None),
                                ("sdnet W-fit fp16", mfp.SDNET, mfp.FP16, wfit),
                                ("sdnet W-fit bf16", mfp.SDNET, mfp.BF16, wfit)]:
-        for grid in GRIDS:
+        if a.only and name not in a.only.split(","):
+            continue
+        for grid in grids:
             r = run(a.n, grid, sub, prec, w, g, ref_dev, a.chunk, a.max, a.target)
             r["subsolver"] = name
             print(json.dumps({k: v for k, v in r.items() if k != "mae_history"}), file=sys.stderr, flush=True)
