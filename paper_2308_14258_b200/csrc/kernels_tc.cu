@@ -828,7 +828,7 @@ static bool chain5() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("MFP_CHAIN5");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
 }
