@@ -180,9 +180,6 @@ void carve(mfp_ctx* c, void* base, size_t* total) {
   dn.bh = cv.take<float>((size_t)nh * kD);
   dn.QTc = cv.take<float>((size_t)kD * 64);
   dn.QTf = cv.take<float>((size_t)kD * kQF);
-  dn.Qc = cv.take<float>((size_t)64 * kD);
-  dn.Qf = cv.take<float>((size_t)kQF * kD);
-  dn.Wh_sw = cv.take<uint16_t>((size_t)nh * kWImg);
   dn.Wh_sw2 = cv.take<uint16_t>((size_t)nh * kWImg);
   dn.W1img = cv.take<uint16_t>((size_t)2 * kD * kNB);
   dn.HcT = cv.take<float>((size_t)kNB * 64);
@@ -704,14 +701,12 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
   if (cfg->subsolver == MFP_SDNET) {
     CK(cudaMemcpyAsync(c->params, params, n_params * sizeof(float), cudaMemcpyHostToDevice, s));
     for (int i = 0; i < 89; i++) c->dn.convw[i] = params[i];   // MFCK order: conv1 w, b, conv2 w, b
-    CK(cudaMemsetAsync((void*)c->dn.Wh_sw, 0, (size_t)net->n_hidden * kWImg * 2, s));
     CK(cudaMemsetAsync((void*)c->dn.Wh_sw2, 0, (size_t)net->n_hidden * kWImg * 2, s));
     PrepArgs a;
     a.P = c->params; a.n_hidden = net->n_hidden; a.f16 = cfg->precision == MFP_FP16 ? 1 : 0;
     a.oW1 = 89; a.oW2 = 89 + kD * kNB; a.oWh0 = a.oW2 + 2 * kD + kD;
     a.W1T = (float*)c->dn.W1T; a.WhT = (float*)c->dn.WhT; a.bh = (float*)c->dn.bh;
-    a.QTc = (float*)c->dn.QTc; a.QTf = (float*)c->dn.QTf; a.Qc = (float*)c->dn.Qc; a.Qf = (float*)c->dn.Qf;
-    a.Wsw = (uint16_t*)c->dn.Wh_sw;
+    a.QTc = (float*)c->dn.QTc; a.QTf = (float*)c->dn.QTf;
     a.Wsw2 = (uint16_t*)c->dn.Wh_sw2;
     a.W1img = (uint16_t*)c->dn.W1img;
     launch_prep(a, s);

@@ -44,7 +44,6 @@ __global__ void k_prep(PrepArgs a) {
     const float* Wl = a.P + a.oWh0 + (int64_t)l * (d * d + d);
     const float w = Wl[(int64_t)n * d + k];
     a.WhT[i] = w;                                    // [l][k][n]
-    uint8_t* img = reinterpret_cast<uint8_t*>(a.Wsw + (int64_t)l * kWImg);
     // CTA-pair image: half n/64 holds rows n%64 as a 64-row SW128 K-major
     // block (two 8 KB K-halves) followed by its 2 KB bias block
     uint8_t* img2 = reinterpret_cast<uint8_t*>(a.Wsw2 + (int64_t)l * kWImg) + (n >> 6) * (kWImg);
@@ -53,10 +52,8 @@ __global__ void k_prep(PrepArgs a) {
     // B operand row n = output feature, K-major; scaled by 1/2 (exact) because
     // the tensor-core epilogue feeds h' = 2 GELU(x) into the next layer
     if (a.f16) {
-      *reinterpret_cast<__half*>(img + sw128_offset(n, k)) = __float2half_rn(0.5f * w);
       *reinterpret_cast<__half*>(img2 + off2) = __float2half_rn(0.5f * w);
     } else {
-      *reinterpret_cast<__nv_bfloat16*>(img + sw128_offset(n, k)) = __float2bfloat16_rn(0.5f * w);
       *reinterpret_cast<__nv_bfloat16*>(img2 + off2) = __float2bfloat16_rn(0.5f * w);
     }
   }
@@ -68,21 +65,15 @@ __global__ void k_prep(PrepArgs a) {
     // (SWIZZLE_NONE K-major: 8-row x 16-byte core matrices, LBO 128 B, SBO 256 B);
     // the A operand carries a constant 1 in those two columns, so the MMA adds
     // b_hi + b_lo (accurate to ~2^-17 relative) to the fp32 accumulator.
-    uint8_t* blk = reinterpret_cast<uint8_t*>(a.Wsw + (int64_t)l * kWImg + kWImgW);
-    const uint32_t off = (uint32_t)((c >> 3) * 256 + (c & 7) * 16);
     const int rr = c & 63;
     uint8_t* blk2 = reinterpret_cast<uint8_t*>(a.Wsw2 + (int64_t)l * kWImg) + (c >> 6) * kWImg + 16384;
     const uint32_t off2 = (uint32_t)((rr >> 3) * 256 + (rr & 7) * 16);
     if (a.f16) {
       const __half hi = __float2half_rn(b), lo = __float2half_rn(b - __half2float(hi));
-      *reinterpret_cast<__half*>(blk + off) = hi;
-      *reinterpret_cast<__half*>(blk + off + 2) = lo;
       *reinterpret_cast<__half*>(blk2 + off2) = hi;
       *reinterpret_cast<__half*>(blk2 + off2 + 2) = lo;
     } else {
       const __nv_bfloat16 hi = __float2bfloat16_rn(b), lo = __float2bfloat16_rn(b - __bfloat162float(hi));
-      *reinterpret_cast<__nv_bfloat16*>(blk + off) = hi;
-      *reinterpret_cast<__nv_bfloat16*>(blk + off + 2) = lo;
       *reinterpret_cast<__nv_bfloat16*>(blk2 + off2) = hi;
       *reinterpret_cast<__nv_bfloat16*>(blk2 + off2 + 2) = lo;
     }
@@ -96,7 +87,6 @@ __global__ void k_prep(PrepArgs a) {
       query_xy(kQC, p, &x, &y);
       v = fmaf(a.P[a.oW2 + 2 * c], x, a.P[a.oW2 + 2 * c + 1] * y);
     }
-    a.Qc[i] = v;
     a.QTc[(int64_t)c * 64 + p] = v;
   }
   for (int64_t i = tid; i < (int64_t)kQF * d; i += nth) {
@@ -104,7 +94,6 @@ __global__ void k_prep(PrepArgs a) {
     float x, y;
     query_xy(kQF, p, &x, &y);
     float v = fmaf(a.P[a.oW2 + 2 * c], x, a.P[a.oW2 + 2 * c + 1] * y);
-    a.Qf[i] = v;
     a.QTf[(int64_t)c * kQF + p] = v;
   }
 }

@@ -97,11 +97,8 @@ struct DevNet {
   int gelu_tanh;
   int f16;               // tensor-core operands fp16 (1) or bf16 (0)
   // bf16 tables (tcgen05 path): weights pre-swizzled into the SW128 K-major image
-  const uint16_t* Wh_sw;  // [n_hidden][36 KB image]   (single-CTA chain)
   const uint16_t* Wh_sw2; // [n_hidden][2][18 KB half] (CTA-pair chain: rows 64h..64h+63)
   const uint16_t* W1img;  // [2][128*128] bf16 SW128 images of W1 = W1_hi + W1_lo (tensor-core embed)
-  const float* Qc;        // [64][d] row-major centre queries (tc path)
-  const float* Qf;        // [961][d] row-major interior queries
   // exact subsolver
   const float* HcT;      // [128 k][64]  (61 used)
   const float* HfT;      // [128 k][961]
@@ -179,8 +176,7 @@ struct PrepArgs {
   int f16;                 // tensor-core operand images in fp16 (1) or bf16 (0)
   int64_t oW1, oW2, oWh0;  // offsets; Wh_l at oWh0 + l*(d*d + d), bh_l right after
   float* W1T; float* WhT; float* bh;
-  float* QTc; float* QTf; float* Qc; float* Qf;
-  uint16_t* Wsw;           // [n_hidden][kWImg] 16-bit SW128 K-major images
+  float* QTc; float* QTf;
   uint16_t* Wsw2;          // [n_hidden][kWImg] CTA-pair half images
   uint16_t* W1img;         // [2][128*128] W1 hi / lo bf16 images
 };
