@@ -492,313 +492,6 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
 
 }  // namespace tc2
 
-// ---------------------------------------------------------------------------
-// Five tile contexts over four TMEM accumulators (tc5).  A tile needs a TMEM
-// accumulator only from its first MMA (hidden layer 1) until its head epilogue
-// has read the last one; its split layer (CUDA cores, into its A operand)
-// does not.  So five warpgroups, each with its own A operand, rotate over the
-// four 128-column accumulators: while four tiles hold accumulators the fifth
-// context already computes the next tile's split layer, and the MMA of that
-// tile issues as soon as an accumulator frees, instead of after the split
-// layer.  Tile t uses context t % 5 and accumulator t % 4.  Shared memory is
-// made to fit (5 x 32 KB A) by a 256-byte bias ones block read with SBO = 0
-// (every 8-row group aliases the same core matrices) and one staged z variant;
-// the TMEM allocation moves to the issuer warp (21 warps x 96 registers).
-namespace tc5 {
-using namespace tc;
-using tc2::cluster_rank;
-using tc2::cluster_sync;
-using tc2::commit2;
-using tc2::mbar_arrive_remote;
-using tc2::mma2;
-
-constexpr int kCtx = 5;                      // tile contexts (warpgroup + A operand) per CTA
-constexpr int kAcc = 4;                      // TMEM accumulators, 128 columns each
-constexpr int kEpi5 = 4 * kCtx;              // epilogue warps 0..19 (context = warp / 4)
-constexpr int kIssue5 = kEpi5;               // warp 20: TMEM allocation, MMA issue (even CTA)
-constexpr int kThreads5 = 32 * (kEpi5 + 1);  // 672
-constexpr int kHalf5 = kWImg;
-constexpr int kOnesB = 256;
-constexpr int kBars5 = kCtx + kAcc * kMaxHidden + kAcc;   // a_full[5], d_full[4][3], acc_free[4]
-
-struct Smem5 {
-  uint8_t* W;      // [nh][18 KB]
-  uint8_t* A;      // [5][32 KB]
-  uint8_t* ones;   // 256 B: K 0-7 core matrix with ones in K 0/1, K 8-15 zeros
-  float* zbuf;     // [5][4][128]: z + W2[:,0]/2
-  float* w2;       // [2][128]
-  float* wo;       // [128]
-  uint64_t* bars;
-  uint32_t* tmem_slot;
-};
-__device__ __forceinline__ Smem5 carve5(uint8_t* raw, int nh) {
-  Smem5 s;
-  s.W = raw;
-  s.A = raw + nh * kHalf5;
-  s.ones = s.A + kCtx * kTile;
-  s.zbuf = (float*)(s.ones + kOnesB);
-  s.w2 = s.zbuf + kCtx * kZRows * kD;
-  s.wo = s.w2 + 2 * kD;
-  s.bars = (uint64_t*)(s.wo + kD);
-  s.tmem_slot = (uint32_t*)(s.bars + kBars5);
-  return s;
-}
-size_t smem_bytes5(int n_hidden) {
-  return (size_t)n_hidden * kHalf5 + kCtx * kTile + kOnesB + 4 * ((size_t)kCtx * kZRows * kD + 3 * kD) +
-         8 * kBars5 + 16;
-}
-// SWIZZLE_NONE K-major descriptor with SBO = 0: all sixteen 8-row groups of the
-// 128-row bias A operand read the same two core matrices.
-__device__ __forceinline__ uint64_t ones_desc(uint32_t saddr) {
-  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)(128 >> 4) << 16;
-  d |= (uint64_t)1 << 46;
-  return d;
-}
-
-template <int GELU, int F16>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads5, 1)
-k_chain_tc5(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, Sink sink) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const int nh = net.n_hidden;
-  const Smem5 S = carve5(smem_raw, nh);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-  uint64_t* const a_full = S.bars;                       // [kCtx]
-  uint64_t* const d_full = S.bars + kCtx;                // [kAcc][kMaxHidden]
-  uint64_t* const acc_free = S.bars + kCtx + kAcc * kMaxHidden;   // [kAcc]
-
-  // ---- prologue
-  for (int l = 0; l < nh; l++) {
-    const uint4* src =
-        reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(net.Wh_sw2) + (size_t)l * 2 * kHalf5 + rank * kHalf5);
-    uint4* dst = reinterpret_cast<uint4*>(S.W + l * kHalf5);
-    for (int i = threadIdx.x; i < kHalf5 / 16; i += kThreads5) dst[i] = __ldg(src + i);
-  }
-  for (int i = threadIdx.x; i < kD; i += kThreads5) {
-    S.wo[i] = (GELU == 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
-    S.w2[i] = __ldg(net.W2 + 2 * i);
-    S.w2[kD + i] = __ldg(net.W2 + 2 * i + 1);
-  }
-  if (threadIdx.x < 16) {
-    const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
-    *reinterpret_cast<uint4*>(S.ones + threadIdx.x * 16) =
-        threadIdx.x < 8 ? make_uint4(one | (one << 16), 0u, 0u, 0u) : make_uint4(0u, 0u, 0u, 0u);
-  }
-  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < kCtx; k++) mbar_init(&a_full[k], 8);     // 4 warps x 2 CTAs
-    for (int i = 0; i < kAcc * kMaxHidden; i++) mbar_init(&d_full[i], 1);   // multicast commit
-    for (int a = 0; a < kAcc; a++) mbar_init(&acc_free[a], 8);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == kIssue5) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
-                 "r"(kTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-  }
-  fence_proxy_async();
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem = *S.tmem_slot;
-  pdl_launch_dependents();
-  pdl_wait();
-
-  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  const int64_t ntiles = (total_rows + 2 * kRows - 1) / (2 * kRows);
-  const int64_t nloc = ntiles > cid ? (ntiles - cid + ncl - 1) / ncl : 0;
-  const int64_t nsub = total_rows / q;
-
-  if (warp == kIssue5) {
-    // ---- MMA issue, in order: groups of four tiles (one per accumulator), layer
-    // by layer; a tile's first MMA also waits for its accumulator to be freed
-    // by the tile four before it
-    if (rank == 0 && lane == 0) {
-      const uint32_t ones_addr = smem_u32(S.ones);
-      for (int64_t j0 = 0; j0 < nloc; j0 += kAcc) {
-        for (int l = 0; l < nh; l++) {
-#pragma unroll
-          for (int s = 0; s < kAcc; s++) {
-            const int64_t t = j0 + s;
-            if (t >= nloc) continue;
-            const int k = (int)(t % kCtx);
-            if (l == 0 && t >= kAcc) mbar_wait(&acc_free[s], (uint32_t)(((t - kAcc) / kAcc) & 1));
-            mbar_wait(&a_full[k], (uint32_t)((nh * (t / kCtx) + l) & 1));
-            tc_fence_after();
-            const uint32_t d = tmem + (uint32_t)(s * kD);
-            const uint32_t a0 = smem_u32(S.A + k * kTile), b0 = smem_u32(S.W + l * kHalf5);
-#pragma unroll
-            for (int kk = 0; kk < kD / 16; kk++) {
-              const uint32_t offa = (uint32_t)((kk >> 2) * 16384 + (kk & 3) * 32);
-              const uint32_t offb = (uint32_t)((kk >> 2) * 8192 + (kk & 3) * 32);
-              mma2<F16>(d, sw128_desc(a0 + offa), sw128_desc(b0 + offb), kk > 0 ? 1u : 0u);
-            }
-            mma2<F16>(d, ones_desc(ones_addr), nosw_desc(b0 + 16384u), 1u);   // bias step
-            commit2(&d_full[s * kMaxHidden + l]);
-          }
-        }
-      }
-    }
-    __syncwarp();
-  } else {
-    // ---- epilogue warpgroup of context k; thread = one row of the tile
-    const int k = warp >> 2;
-    const int quad = warp & 3;
-    const int row = quad * 32 + lane;
-    const uint32_t a_row = smem_u32(S.A + k * kTile) + (uint32_t)row * 128u;
-    const int r7 = row & 7;
-    uint32_t a_sw[8];
-#pragma unroll
-    for (int j = 0; j < 8; j++) a_sw[j] = a_row + ((uint32_t)(j ^ r7) << 4);
-    float* zb = S.zbuf + k * kZRows * kD;
-    const float bo = __ldg(net.bo);
-    const int zi = 4 * row, zr_ = zi >> 7, zc = zi & 127;
-    auto row0_of = [&](int64_t t) -> int64_t { return (cid + t * ncl) * (2 * kRows) + rank * kRows; };
-    auto z_fetch = [&](int64_t t) -> float4 {
-      int64_t sidx = row0_of(t) / q + zr_;
-      if (sidx > nsub - 1) sidx = nsub - 1;
-      return __ldg(reinterpret_cast<const float4*>(z + sidx * kD + zc));
-    };
-    // z of the tile's <= 4 subdomains with W2[:,0]/2 folded in (x/m = 1/2 on the
-    // vertical centre line)
-    auto z_stage = [&](const float4 v) {
-      const float4 a = *reinterpret_cast<const float4*>(S.w2 + zc);
-      *reinterpret_cast<float4*>(zb + zi) =
-          make_float4(fmaf(0.5f, a.x, v.x), fmaf(0.5f, a.y, v.y), fmaf(0.5f, a.z, v.z), fmaf(0.5f, a.w, v.w));
-    };
-    auto arrive = [&](uint64_t* bar) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote(bar, 0u);
-    };
-    if (k < nloc) z_stage(z_fetch(k));
-    for (int64_t t = k; t < nloc; t += kCtx) {
-      const int s = (int)(t % kAcc);
-      const uint32_t par = (uint32_t)((t / kAcc) & 1);
-      const uint32_t t_row = tmem + (uint32_t)(s * kD) + ((uint32_t)(quad * 32) << 16);
-      const int64_t row0 = row0_of(t);
-      int64_t s_first = row0 / q;
-      if (s_first > nsub - 1) s_first = nsub - 1;
-      named_sync(1 + k, 128);   // this tile's staged z visible to the context's 4 warps
-      const bool have_next = t + kCtx < nloc;
-      float4 znext = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (have_next) znext = z_fetch(t + kCtx);
-      const int64_t grow = row0 + row;
-      const bool valid = grow < total_rows;
-      const int64_t gr = valid ? grow : total_rows - 1;
-      const int64_t sidx = gr / q;
-      const int p = (int)(gr - sidx * q);
-      float qx, qy;
-      query_xy(q, p, &qx, &qy);
-      int zo = (int)(sidx - s_first);
-      if (zo < 0 || zo >= kZRows) zo = 0;
-
-      // ---- split layer (Eq. 5): h' = 2 GELU((z + W2[:,0]/2) + W2[:,0] (x - 1/2) + W2[:,1] y);
-      // on the vertical centre line x - 1/2 = 0: one FMA per element pair
-      const bool vert = (q == kQC) && p < kM - 1;
-      const float* zs = zb + zo * kD;
-      const float qa = qx - 0.5f;
-#pragma unroll 1
-      for (int kh = 0; kh < 2; kh++) {
-#pragma unroll
-        for (int j16 = 0; j16 < 4; j16++) {
-          const int c0 = 64 * kh + 16 * j16;
-          float v[16];
-          const f2 QY = f2_make(qy, qy), QA = f2_make(qa, qa);
-#pragma unroll
-          for (int i = 0; i < 4; i++) {
-            const float4 zz = *reinterpret_cast<const float4*>(zs + c0 + 4 * i);
-            const float4 bb = *reinterpret_cast<const float4*>(S.w2 + kD + c0 + 4 * i);
-            f2 v01 = ffma2(f2_make(bb.x, bb.y), QY, f2_make(zz.x, zz.y));
-            f2 v23 = ffma2(f2_make(bb.z, bb.w), QY, f2_make(zz.z, zz.w));
-            if (!vert) {
-              const float4 aa = *reinterpret_cast<const float4*>(S.w2 + c0 + 4 * i);
-              v01 = ffma2(f2_make(aa.x, aa.y), QA, v01);
-              v23 = ffma2(f2_make(aa.z, aa.w), QA, v23);
-            }
-            f2_split(v01, v[4 * i], v[4 * i + 1]);
-            f2_split(v23, v[4 * i + 2], v[4 * i + 3]);
-          }
-          uint32_t w[8];
-          act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v), *reinterpret_cast<uint32_t(*)[4]>(w));
-          act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v + 8), *reinterpret_cast<uint32_t(*)[4]>(w + 4));
-          st_shared_v4(a_sw[2 * j16] + ((uint32_t)kh << 14), w[0], w[1], w[2], w[3]);
-          st_shared_v4(a_sw[2 * j16 + 1] + ((uint32_t)kh << 14), w[4], w[5], w[6], w[7]);
-        }
-      }
-      fence_proxy_async();
-      arrive(&a_full[k]);
-
-      // ---- hidden layers and head
-      f2 yacc = f2_make(0.f, 0.f);
-      for (int l = 0; l < nh; l++) {
-        // d_full[s][l] completes once per tile on accumulator s.  For the first
-        // layer the previous tile on s (t - 4, another context) may not have
-        // committed yet; a parity wait two phases ahead would alias, so first
-        // wait for that phase, then for this tile's.  (For l > 0 this tile's
-        // earlier commits imply tile t - 4 finished.)
-        if (l == 0 && t >= kAcc) mbar_wait(&d_full[s * kMaxHidden], par ^ 1u);
-        mbar_wait(&d_full[s * kMaxHidden + l], par);
-        tc_fence_after();
-        auto layer_epi = [&](auto last_tag) {
-          constexpr bool LAST = decltype(last_tag)::value;
-          auto work16 = [&](const uint32_t (&r)[16], int c16) {
-            if constexpr (!LAST) {
-#pragma unroll
-              for (int c8 = 0; c8 < 2; c8++) {
-                const int g = 2 * c16 + c8;
-                float v[8];
-#pragma unroll
-                for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[c8 * 8 + e]);
-                uint32_t w[4];
-                act8<GELU, F16>(v, w);
-                st_shared_v4(a_sw[g & 7] + ((uint32_t)(g >> 3) << 14), w[0], w[1], w[2], w[3]);
-              }
-            } else {
-              head32<GELU, 16>(r, S.wo + c16 * 16, yacc);
-            }
-          };
-          uint32_t ra[16], rb[16];
-          tmem_ld16(t_row, ra);
-          tmem_wait_ld_dep16(ra);
-#pragma unroll
-          for (int c16 = 0; c16 < kD / 16; c16 += 2) {
-            tmem_ld16(t_row + (uint32_t)((c16 + 1) * 16), rb);
-            work16(ra, c16);
-            tmem_wait_ld_dep16(rb);
-            if (c16 + 2 < kD / 16) tmem_ld16(t_row + (uint32_t)((c16 + 2) * 16), ra);
-            work16(rb, c16 + 1);
-            if (c16 + 2 < kD / 16) tmem_wait_ld_dep16(ra);
-          }
-        };
-        const bool last = (l == nh - 1);
-        if (last) layer_epi(std::true_type{});
-        else layer_epi(std::false_type{});
-        tc_fence_before();
-        if (!last) {
-          fence_proxy_async();
-          arrive(&a_full[k]);
-        }
-      }
-      arrive(&acc_free[s]);     // accumulator s read out: tile t + 4 may overwrite it
-      if (have_next) z_stage(znext);
-      float y0, y1;
-      f2_split(yacc, y0, y1);
-      if (valid) sink_store(sink, sidx, p, (y0 + y1) + bo);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();
-  if (warp == kIssue5) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
-  }
-}
-
-}  // namespace tc5
 
 
 bool chain_tc_available() { return true; }
@@ -817,20 +510,6 @@ void tc_kernel_attributes() {
   cudaFuncSetAttribute(tc2::k_chain_tc2<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
   cudaFuncSetAttribute(tc2::k_chain_tc2<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
   cudaFuncSetAttribute(tc2::k_chain_tc2<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
-  const int mx5 = (int)tc5::smem_bytes5(kMaxHidden);
-  cudaFuncSetAttribute(tc5::k_chain_tc5<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx5);
-  cudaFuncSetAttribute(tc5::k_chain_tc5<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx5);
-  cudaFuncSetAttribute(tc5::k_chain_tc5<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx5);
-  cudaFuncSetAttribute(tc5::k_chain_tc5<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx5);
-}
-
-static bool chain5() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MFP_CHAIN5");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
 }
 
 // Persistent grid: one CTA pair per TPC (74 clusters), or fewer for small batches.
@@ -842,17 +521,6 @@ void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const 
   const int64_t ptiles = (rows + 2 * tc::kRows - 1) / (2 * tc::kRows);
   const int64_t pairs = num_sms / 2;
   const int grid = 2 * (int)(ptiles < pairs ? ptiles : pairs);
-  if (chain5()) {
-    const size_t sm5 = tc5::smem_bytes5(net.n_hidden);
-#define MFP_TC5(G, F) launch_pdl(tc5::k_chain_tc5<G, F>, grid, tc5::kThreads5, sm5, s, z, rows, q, net, sink)
-    if (net.f16) {
-      if (net.gelu_tanh) MFP_TC5(1, 1); else MFP_TC5(0, 1);
-    } else {
-      if (net.gelu_tanh) MFP_TC5(1, 0); else MFP_TC5(0, 0);
-    }
-#undef MFP_TC5
-    return;
-  }
 #define MFP_TC2(G, F) launch_pdl(tc2::k_chain_tc2<G, F>, grid, tc2::kThreads2, sm, s, z, rows, q, net, sink)
   if (net.f16) {
     if (net.gelu_tanh) MFP_TC2(1, 1); else MFP_TC2(0, 1);
