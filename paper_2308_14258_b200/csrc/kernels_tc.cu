@@ -66,7 +66,28 @@ __device__ __forceinline__ uint32_t pack2_rn(float lo, float hi) {
 __device__ __forceinline__ f2 gelu2_mufu(f2 x) {
   float u0, u1;
   f2_split(fmul2(x, ffma2(fmul2(x, x), f2_make(kGF1, kGF1), f2_make(kGF0, kGF0))), u0, u1);
+#ifdef MFP_EXPERIMENT_FAKE_TANH   // timing experiment only (wrong results): clamp instead of MUFU tanh
+  return ffma2(x, f2_make(fminf(fmaxf(u0, -1.f), 1.f), fminf(fmaxf(u1, -1.f), 1.f)), x);
+#else
   return ffma2(x, f2_make(tanh_approx(u0), tanh_approx(u1)), x);
+#endif
+}
+
+// FMA-pipe form of h' = 2 GELU(x) for pairs feeding a 16-bit MMA (MFP_POLY_EVERY
+// builds): x (1 + S(x)), S(x) ~ x_c P(x_c^2), x_c = clamp(x, -3.4, 3.4), degree-5
+// minimax fit with S(3.4) = 1 (tools/fit_gelu_poly.py --n 5 --a 3.4): |dh'| <= 2.3e-3,
+// below the 16-bit rounding of h' wherever it is that large.  Moves one pair in
+// MFP_POLY_EVERY off the MUFU pipe (2 MUFU -> 3 extra FMA-pipe + 4 ALU ops).
+__device__ __forceinline__ f2 gelu2_poly(f2 x) {
+  float x0, x1;
+  f2_split(x, x0, x1);
+  const f2 xc = f2_make(fminf(fmaxf(x0, -3.4f), 3.4f), fminf(fmaxf(x1, -3.4f), 3.4f));
+  const f2 t = fmul2(xc, xc);
+  f2 P = ffma2(t, f2_make(2.003122427e-05f, 2.003122427e-05f), f2_make(-8.018445806e-04f, -8.018445806e-04f));
+  P = ffma2(P, t, f2_make(1.317339763e-02f, 1.317339763e-02f));
+  P = ffma2(P, t, f2_make(-1.187743098e-01f, -1.187743098e-01f));
+  P = ffma2(P, t, f2_make(7.877168655e-01f, 7.877168655e-01f));
+  return ffma2(x, fmul2(xc, P), x);
 }
 
 // Activation of the fp32 last layer, up to the factor the head weights carry:
@@ -108,6 +129,11 @@ __device__ __forceinline__ void act8(const float (&v)[8], uint32_t (&w)[4]) {
   for (int e = 0; e < 4; e++) {
     float h0, h1;
     if constexpr (GELU == 1) {
+#ifdef MFP_POLY_EVERY
+      if (e % MFP_POLY_EVERY == MFP_POLY_EVERY - 1)
+        f2_split(gelu2_poly(f2_make(v[2 * e], v[2 * e + 1])), h0, h1);
+      else
+#endif
       f2_split(gelu2_mufu(f2_make(v[2 * e], v[2 * e + 1])), h0, h1);
     } else {
       h0 = 2.f * gelu_erf(v[2 * e]);
