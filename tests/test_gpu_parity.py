@@ -192,6 +192,28 @@ def test_sdnet_batch_parity(lib, precision, qs, B):
     check_batch(out, ref, precision, S)
 
 
+@pytest.mark.parametrize("precision", [0, 1])
+def test_sdnet_batch_empty_and_chunked(lib, precision):
+    """B = 0 is a no-op; a batch larger than the context's z staging (4,096 rows on a
+    64^2 context) runs in chunks with a ragged tail — every chunk boundary row is
+    checked against the oracle, plus a random sample."""
+    import torch
+    from tests._refnet import torch_sdnet
+    m, w = make(lib, 64, 64, subsolver="sdnet", precision=precision, gelu=1 if precision else 0)
+    out0 = torch.full((1, 61), 7.0, device="cuda")
+    lib.mfp_sdnet_batch(m.ctx, torch.empty((1, 128), device="cuda"), 0, 0, out0)
+    assert float(out0.min()) == 7.0 == float(out0.max())
+    B = 3 * 4096 + 123
+    gb = random_boundaries(B, seed=17)
+    out = m.sdnet_batch(torch.from_numpy(gb).cuda(), 0).cpu().numpy()
+    rows = np.unique(np.concatenate([[0, 4095, 4096, 8191, 8192, 12287, 12288, B - 1],
+                                     np.random.default_rng(3).choice(B, 64, replace=False)]))
+    q = oracle.writeset(0, 0)[1]
+    ref = oracle.sdnet_forward(w.astype(np.float64), gb[rows].astype(np.float64), q)
+    _, S = torch_sdnet(w, gb[rows], q, return_scale=True)
+    check_batch(out[rows], ref, precision, S)
+
+
 @pytest.mark.parametrize("precision", [1, 2])
 @pytest.mark.parametrize("nx,ny,t,grid", [(64, 64, 20, (1, 1)), (512, 512, 4, (1, 1)), (128, 128, 6, (2, 2))])
 def test_sdnet_tensorcore_field_parity(lib, precision, nx, ny, t, grid):
