@@ -243,6 +243,20 @@ def sdnet_batch_sweep(m, torch, stream, sizes=(1024, 2048, 4096, 8192, 16384, 32
     return out
 
 
+def halo_line(rep, prof, world: int) -> dict:
+    """a7 against the NVLink roofline (north_star): bytes this rank sends per
+    exchange over the side-stream span of transport + unpack (CUDA events in
+    mfp_profile_iterations), vs the measured 770 GB/s per-direction peer copy of
+    B200_PROFILING.md.  Latency-bound by design: tens of KB per exchange."""
+    b = rep.halo_bytes_sent / max(rep.iterations, 1)
+    out = {"bytes_per_iter_rank0": b, "msgs_per_iter": rep.halo_msgs_per_iter}
+    if world > 1 and prof.ms_halo > 0:
+        gbs = b / (prof.ms_halo / 1000.0) / 1e9
+        out.update({"us_per_exchange": 1000.0 * prof.ms_halo, "gbs": gbs, "peak_gbs": 770.0,
+                    "frac": gbs / 770.0, "peak_source": "B200_PROFILING.md measured peer copy, per direction"})
+    return out
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
@@ -473,8 +487,7 @@ def main():
                 "points_iter_per_s": (NX + 1) * (NY + 1) * T * args.steps / (ms / 1000.0),
                 "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
                 "time_to_converge": ttc, "sdnet_batch_sweep": sweep, "boundary_io": bio, "clocks": clk.summary(),
-                "halo": {"bytes_per_iter_rank0": rep.halo_bytes_sent / max(rep.iterations, 1),
-                         "msgs_per_iter": rep.halo_msgs_per_iter}}
+                "halo": halo_line(rep, prof, world)}
         print(json.dumps(line), flush=True)
     m.close()
     if comm is not None:

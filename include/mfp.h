@@ -243,6 +243,14 @@ mfp_status mfp_gather_phase(mfp_ctx* ctx, int32_t rank, int32_t phase, float* gb
 mfp_status mfp_scatter_phase(mfp_ctx* ctx, int32_t rank, int32_t phase, const float* pred, int64_t B,
                              float* update_max);
 
+/* Communication-avoiding variant (the paper's open problem
+ * P:196 "reducing the communication frequency"): exchange halos after every s-th
+ * iteration only (and always after the last), so halo copies are up to s - 1
+ * iterations stale; s = 1 (default) is Algorithm 2.  s must divide
+ * check_every (CUDA-graph blocks replay one pattern).  Collective in the sense
+ * that every rank must use the same s.  Errors: INVALID. */
+mfp_status mfp_set_exchange_every(mfp_ctx* ctx, int32_t s);
+
 /* Run ONE phase (class 0..3 in G2 order) on the current lattice of every local
  * rank, without exchange (debug / sampled parity at full size). */
 mfp_status mfp_step_phase(mfp_ctx* ctx, int32_t phase);

@@ -174,7 +174,8 @@ class _Cfg(ctypes.Structure):
                 ("Py", ctypes.c_int), ("Px", ctypes.c_int), ("subsolver", ctypes.c_int),
                 ("check_every", ctypes.c_int), ("sequential", ctypes.c_int),
                 ("n_conv", ctypes.c_int), ("conv_k", ctypes.c_int * 8),
-                ("conv_ch", ctypes.c_int * 9), ("d", ctypes.c_int), ("n_hidden", ctypes.c_int)]
+                ("conv_ch", ctypes.c_int * 9), ("d", ctypes.c_int), ("n_hidden", ctypes.c_int),
+                ("exchange_every", ctypes.c_int)]
 
 
 @dataclass
@@ -188,12 +189,14 @@ class MfpConfig:
     check_every: int = 1
     sequential: bool = False
     net: NetShape = field(default_factory=NetShape)
+    exchange_every: int = 1    # communication-avoiding variant: halo refresh every s iterations
 
     def c(self) -> _Cfg:
         k, ch = self.net.arrays()
         return _Cfg(self.nx, self.ny, self.m, self.Py, self.Px, 1 if self.subsolver == "exact" else 0,
                     self.check_every, int(self.sequential), self.net.n_conv,
-                    (ctypes.c_int * 8)(*k), (ctypes.c_int * 9)(*ch), self.net.d, self.net.n_hidden)
+                    (ctypes.c_int * 8)(*k), (ctypes.c_int * 9)(*ch), self.net.d, self.net.n_hidden,
+                    self.exchange_every)
 
 
 @dataclass

@@ -402,6 +402,8 @@ typedef struct {
   int check_every; /* c                                                           */
   int sequential;  /* 1: baseline MFP, one subdomain at a time (A4)         */
   int n_conv, conv_k[ORC_MAXLAYERS], conv_ch[ORC_MAXLAYERS + 1], d, n_hidden;
+  int exchange_every; /* s: exchange after every s-th iteration and the last one
+                       * (communication-avoiding variant); 1 = Algorithm 2 */
 } orc_cfg;
 
 typedef struct {
@@ -544,8 +546,10 @@ int orc_mfp_run(const orc_cfg *cfg, const double *params, const double *g, int t
       }
     }
     /* communicate_new_boundaries: owners overwrite every halo copy of
-     * a line point, once per iteration. */
-    if (R > 1) {
+     * a line point, once per iteration — or, in the communication-
+     * avoiding variant, after every s-th iteration and the last. */
+    const int s_ex = c->exchange_every > 1 ? c->exchange_every : 1;
+    if (R > 1 && (it % s_ex == 0 || it == t)) {
       for (int r = 0; r < R; r++) {
         int ry = r / c->Px, rx = r % c->Px;
         int X0 = rx * Lx, X1 = X0 + Lx, Y0 = ry * Ly, Y1 = Y0 + Ly;

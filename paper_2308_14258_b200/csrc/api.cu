@@ -68,6 +68,7 @@ struct mfp_ctx {
   cudaEvent_t ev_packed = nullptr, ev_unpacked = nullptr;
   bool pending = false;                // an exchange is in flight on `side`
   bool use_graphs = false;             // replay blocks of c iterations as CUDA graphs
+  int exchange_every = 1;              // halo exchange after every s-th iteration (NEXT-4)
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // [0] plain block, [1] block ending in a check
   int glaunches[2] = {0, 0};
   std::vector<RankState> ranks;
@@ -354,7 +355,7 @@ mfp_status exchange_wait(mfp_ctx* c) {
 
 // One iteration: phase 0 (interior subdomains first while a pending exchange
 // is in flight, then the halo-touching ones), phases 1-3, then the exchange.
-mfp_status iterate(mfp_ctx* c) {
+mfp_status iterate(mfp_ctx* c, bool exchange = true) {
   mfp_status st;
   if (c->pending) {
     for (auto& rs : c->ranks) run_phase(c, rs, 0, 0, rs.plan.n0_interior);
@@ -365,7 +366,7 @@ mfp_status iterate(mfp_ctx* c) {
   }
   for (int ph = 1; ph < 4; ph++)
     for (auto& rs : c->ranks) run_phase(c, rs, ph);
-  return exchange_begin(c);
+  return exchange ? exchange_begin(c) : MFP_OK;
 }
 
 // delta_k (reading G5) -> host, max over ranks; returns nonfinite flag
@@ -414,7 +415,7 @@ mfp_status run_block(mfp_ctx* c, int kind) {
       if (kind == 1 && i == ce - 1)
         for (auto& rs : c->ranks)
           cudaMemcpyAsync(rs.snap, rs.lat, rs.plan.lat.cells * sizeof(float), cudaMemcpyDeviceToDevice, c->stream);
-      st = iterate(c);
+      st = iterate(c, (i + 1) % c->exchange_every == 0);
     }
     if (st == MFP_OK) st = exchange_wait(c);
     if (st == MFP_OK && kind == 1) st = enqueue_delta(c);
@@ -538,7 +539,7 @@ mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, floa
     if (check)
       for (auto& rs : c->ranks)
         CK(cudaMemcpyAsync(rs.snap, rs.lat, rs.plan.lat.cells * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
-    mfp_status st = iterate(c);
+    mfp_status st = iterate(c, it % c->exchange_every == 0 || it == t);
     if (st) return st;
     if (check) {
       // complete the exchange first: NCCL ops on one communicator must not be
@@ -856,6 +857,19 @@ mfp_status mfp_scatter_phase(mfp_ctx* c, int32_t rank, int32_t phase, const floa
   return MFP_OK;
 }
 
+mfp_status mfp_set_exchange_every(mfp_ctx* c, int32_t s) {
+  if (!c) return MFP_ERR_INVALID;
+  if (c->poisoned) return MFP_ERR_STATE;
+  if (s < 1 || c->cfg.check_every % s != 0)
+    return fail(c, MFP_ERR_INVALID, "exchange_every must be >= 1 and divide check_every");
+  if (s != c->exchange_every) {
+    for (auto& g : c->gexec)
+      if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    c->exchange_every = s;
+  }
+  return MFP_OK;
+}
+
 mfp_status mfp_step_phase(mfp_ctx* c, int32_t phase) {
   if (!c) return MFP_ERR_INVALID;
   if (c->poisoned) return MFP_ERR_STATE;
@@ -904,7 +918,7 @@ mfp_status mfp_profile_iterations(mfp_ctx* c, int32_t iters, mfp_profile* o) {
   cudaEvent_t a = ev(c), b = ev(c);
   CK(cudaEventRecord(a, c->stream));
   for (int it = 0; it < iters; it++) {
-    mfp_status st = iterate(c);
+    mfp_status st = iterate(c, (it + 1) % c->exchange_every == 0);
     if (st) { c->profiling = false; return st; }
   }
   {

@@ -101,6 +101,7 @@ _SIGS = {
     "mfp_cost_model": [_f64] * 8 + [_P(_f64)] * 3,
     "mfp_gather_phase": [_vp, _i32, _i32, _vp, _i64, _P(_i64), _P(_i32), _P(_i32)],
     "mfp_scatter_phase": [_vp, _i32, _i32, _vp, _i64, _P(ctypes.c_float)],
+    "mfp_set_exchange_every": [_vp, _i32],
     "mfp_nccl_get_unique_id": [_vp],
     "mfp_nccl_comm_init": [_i32, _vp, _i32, _P(_vp)],
     "mfp_nccl_comm_destroy": [_vp],
@@ -212,6 +213,10 @@ def mfp_scatter_phase(ctx, rank: int, phase: int, pred_dev, B: int, want_norm: b
     v = ctypes.c_float(0.0)
     _check(_lib.mfp_scatter_phase(ctx, rank, phase, _ptr(pred_dev), B, ctypes.byref(v) if want_norm else None), ctx)
     return v.value if want_norm else None
+
+
+def mfp_set_exchange_every(ctx, s: int) -> None:
+    _check(_lib.mfp_set_exchange_every(ctx, s), ctx)
 
 
 def mfp_step_phase(ctx, phase: int) -> None:

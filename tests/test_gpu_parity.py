@@ -90,6 +90,29 @@ def test_exact_distributed_parity(lib, grid, kx, ky, t):
         assert crossings_consistent(m.lines(r))
 
 
+@pytest.mark.parametrize("subsolver", ["exact", "sdnet"])
+@pytest.mark.parametrize("s_ex,t,ce", [(2, 10, 2), (4, 13, 4), (3, 11, 6)])
+def test_communication_avoiding_parity(lib, subsolver, s_ex, t, ce):
+    """mfp_set_exchange_every (NEXT-4): halos refreshed after every s-th
+    iteration and the last — graph-replayed blocks and the host-driven tail alike —
+    against the oracle's emulation of the same schedule (2x2 grid, fp32)."""
+    nx = ny = 8 * M
+    grid = (2, 2)
+    g = gp_boundary(nx, ny, 5)
+    m, w = make(lib, nx, ny, grid, subsolver=subsolver, check_every=ce)
+    lib.mfp_set_exchange_every(m.ctx, s_ex)
+    u, rep = m.solve(g, t, 0.0)
+    ref = oracle.mfp_run(oracle.MfpConfig(nx, ny, Py=2, Px=2, subsolver=subsolver, check_every=ce,
+                                          exchange_every=s_ex), g.astype(np.float64), t,
+                         params=None if w is None else w.astype(np.float64))
+    assert rel_err(gpu_lines(lib, m, nx, ny, grid), ref.lines, line_mask(nx, ny)) <= FP32_TOL
+    assert rel_err(u, ref.u) <= FP32_TOL
+    import paper_2308_14258_b200 as mfp
+    with pytest.raises(mfp.MfpError) as e:       # s must divide check_every
+        lib.mfp_set_exchange_every(m.ctx, ce + 1)
+    assert e.value.status == 1
+
+
 def test_exact_distributed_large(lib):
     """C3 (2049^2) on the 2x4 grid the 8-GPU bench uses: exchange overlap,
     D1 compute sets and final assembly at size, vs the oracle's emulation."""

@@ -182,6 +182,27 @@ def test_distributed_emulation_converges_to_same_solution(py, px):
     assert rp.iterations >= r1.iterations                          # staleness never helps here
 
 
+@pytest.mark.parametrize("s_ex", [2, 4])
+def test_communication_avoiding_same_limit(s_ex):
+    """The communication-avoiding variant (halos refreshed every s iterations)
+    is still a relaxed Schwarz iteration: same limit (the global discrete solution),
+    more iterations; s = 1 reproduces Algorithm 2 bit for bit."""
+    nx = ny = 4 * M
+    g = gp_boundary(nx, ny, 3).astype(np.float64)
+    ref = dst_laplace(nx, ny, g)
+    base = oracle.MfpConfig(nx, ny, Py=2, Px=2, subsolver="exact", check_every=4)
+    r1 = oracle.mfp_run(base, g, t=4000, tol=1e-13)
+    rs = oracle.mfp_run(oracle.MfpConfig(nx, ny, Py=2, Px=2, subsolver="exact", check_every=4,
+                                         exchange_every=s_ex), g, t=4000, tol=1e-13)
+    assert rs.iterations < 4000
+    assert np.max(np.abs(rs.u - ref)) < 1e-10
+    assert rs.iterations >= r1.iterations
+    r1b = oracle.mfp_run(oracle.MfpConfig(nx, ny, Py=2, Px=2, subsolver="exact", check_every=4,
+                                          exchange_every=1), g, t=30)
+    r1c = oracle.mfp_run(base, g, t=30)
+    assert np.array_equal(r1b.u, r1c.u)
+
+
 def test_distributed_p1_is_plain():
     nx, ny = 2 * M, 4 * M
     g = gp_boundary(nx, ny, 0).astype(np.float64)

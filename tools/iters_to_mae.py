@@ -28,10 +28,11 @@ from mfp_inputs import gp_boundary  # noqa: E402
 GRIDS = [(1, 1), (1, 2), (2, 2), (2, 4)]
 
 
-def run(n, grid, subsolver, precision, w, g, ref_dev, chunk, max_iters, target):
+def run(n, grid, subsolver, precision, w, g, ref_dev, chunk, max_iters, target, s_ex=1):
     cfg = mfp.make_config(n, n, grid, precision=precision, subsolver=subsolver, check_every=chunk)
     rank = 0 if grid == (1, 1) else mfp.ALL_RANKS
     m = mfp.Mfp(cfg, mfp.make_net(gelu=1 if precision != mfp.FP32 else 0), w, rank=rank)
+    mfp.mfp_set_exchange_every(m.ctx, s_ex)
     u = torch.empty((n + 1, n + 1), dtype=torch.float32, device="cuda")
     g_dev = torch.from_numpy(g.astype(np.float32)).cuda()
     done, mae, hist = 0, float("nan"), []
@@ -47,7 +48,7 @@ def run(n, grid, subsolver, precision, w, g, ref_dev, chunk, max_iters, target):
         if mae < target:
             break
     m.close()
-    return {"grid": f"{grid[0]}x{grid[1]}", "iterations": done if mae < target else None, "mae": mae,
+    return {"grid": f"{grid[0]}x{grid[1]}", "exchange_every": s_ex, "iterations": done if mae < target else None, "mae": mae,
             "reached": mae < target, "wall_s": time.perf_counter() - t0,
             "mae_history": hist[:: max(1, len(hist) // 20)]}
 
@@ -61,6 +62,7 @@ def main():
     ap.add_argument("--weights", default=os.path.join(ROOT, "weights", "sdnet_fit_d128.npy"))
     ap.add_argument("--only", default="", help="comma list of subsolver names to run (default all)")
     ap.add_argument("--grids", default="1x1,1x2,2x2,2x4")
+    ap.add_argument("--exchange-every", default="1", help="comma list of s (NEXT-4); each must divide --chunk")
     a = ap.parse_args()
     g = gp_boundary(a.n, a.n, 0)
     ref = dst_laplace(a.n, a.n, g.astype(np.float64))
@@ -74,10 +76,13 @@ def main():
         if a.only and name not in a.only.split(","):
             continue
         for grid in grids:
-            r = run(a.n, grid, sub, prec, w, g, ref_dev, a.chunk, a.max, a.target)
-            r["subsolver"] = name
-            print(json.dumps({k: v for k, v in r.items() if k != "mae_history"}), file=sys.stderr, flush=True)
-            out.append(r)
+            for s_ex in [int(v) for v in a.exchange_every.split(",")]:
+                if s_ex > 1 and grid == (1, 1):
+                    continue
+                r = run(a.n, grid, sub, prec, w, g, ref_dev, a.chunk, a.max, a.target, s_ex)
+                r["subsolver"] = name
+                print(json.dumps({k: v for k, v in r.items() if k != "mae_history"}), file=sys.stderr, flush=True)
+                out.append(r)
     print(json.dumps({"experiment": "iterations to MAE < %g vs the discrete solution (P:179)" % a.target,
                       "domain": f"{a.n + 1}^2 (GP boundary k=0)", "rows": out}))
 
