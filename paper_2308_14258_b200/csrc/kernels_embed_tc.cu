@@ -93,7 +93,7 @@ __device__ __forceinline__ void conv_stack2(const f2 (&g4)[4], int lane, const D
 template <int GELU>
 __global__ void __launch_bounds__(kThreadsE, 1)
 k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ anchors,
-           const float* __restrict__ gb, int64_t B, DevNet net, float* __restrict__ z) {
+           const float* __restrict__ gb, int64_t B, int rows, DevNet net, float* __restrict__ z) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sWhi = smem_raw;
   uint8_t* sWlo = sWhi + kImg;
@@ -135,24 +135,31 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
   const int i0 = 4 * lane;
   const uint32_t a_hi = smem_u32(sAhi), a_lo = smem_u32(sAlo);
   uint32_t phase = 0u;
-  for (int64_t base = (int64_t)blockIdx.x * kRowsE; base < B; base += (int64_t)gridDim.x * kRowsE) {
-    // ---- gather + conv stack, 8 subdomains per warp (gathers issued up front)
+  // `rows` (32, 64, 96 or 128) subdomains per round: small batches (a rank's share
+  // on 8 GPUs) spread over more CTAs with fewer subdomains per warp, so the
+  // serial conv work per warp shrinks with the batch; rows >= `rows` of the
+  // 128-row MMA are don't-care (rows are independent in the MMA, never stored)
+  const int pw = rows >> 4;   // subdomains per warp (even)
+  for (int64_t base = (int64_t)blockIdx.x * rows; base < B; base += (int64_t)gridDim.x * rows) {
+    // ---- gather + conv stack, pw subdomains per warp (gathers issued up front)
     float4 gpre[kPerWarp];
 #pragma unroll
     for (int j = 0; j < kPerWarp; j++) {
-      int64_t s = base + warp * kPerWarp + j;
+      if (j >= pw) break;
+      int64_t s = base + warp * pw + j;
       if (s > B - 1) s = B - 1;
       gpre[j] = gb ? __ldg(reinterpret_cast<const float4*>(gb + s * kNB + i0)) : gather4(lat, L, __ldg(anchors + s), lane);
     }
 #pragma unroll
     for (int jp = 0; jp < kPerWarp; jp += 2) {
+      if (jp >= pw) break;
       const f2 g4[4] = {f2_make(gpre[jp].x, gpre[jp + 1].x), f2_make(gpre[jp].y, gpre[jp + 1].y),
                         f2_make(gpre[jp].z, gpre[jp + 1].z), f2_make(gpre[jp].w, gpre[jp + 1].w)};
       f2 e2[4];
       conv_stack2<GELU>(g4, lane, net, e2);
 #pragma unroll
       for (int h = 0; h < 2; h++) {
-      const int row = warp * kPerWarp + jp + h;
+      const int row = warp * pw + jp + h;
       float e[4];
 #pragma unroll
       for (int p = 0; p < 4; p++) {
@@ -198,7 +205,7 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
       tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(cb * 32), r);
       tmem_wait_ld();
       const int64_t s = base + quad * 32 + lane;
-      if (s < B) {
+      if (quad * 32 + lane < rows && s < B) {
         float4* dst = reinterpret_cast<float4*>(z + s * kD + cb * 32);
         const float* bb = sB1 + cb * 32;
 #pragma unroll
@@ -235,13 +242,18 @@ void embed_tc_kernel_attributes() {
 void launch_embed_tc(const float* lat, const LatticeGeom& L, const uint32_t* anchors, const float* gb,
                      int64_t B, const DevNet& net, float* z, cudaStream_t s) {
   if (B <= 0) return;
-  int64_t blocks = (B + emb::kRowsE - 1) / emb::kRowsE;
+  // rows per CTA round: the smallest multiple of 32 that covers B over the SMs
+  int64_t per = (B + 147) / 148;
+  int rows = (int)((per + 31) / 32) * 32;
+  if (rows > emb::kRowsE) rows = emb::kRowsE;
+  if (rows < 32) rows = 32;
+  int64_t blocks = (B + rows - 1) / rows;
   if (blocks > 148) blocks = 148;
   const size_t sm = emb::smem_bytes();
   if (net.gelu_tanh)
-    launch_pdl(emb::k_embed_tc<1>, (int)blocks, emb::kThreadsE, sm, s, lat, L, anchors, gb, B, net, z);
+    launch_pdl(emb::k_embed_tc<1>, (int)blocks, emb::kThreadsE, sm, s, lat, L, anchors, gb, B, rows, net, z);
   else
-    launch_pdl(emb::k_embed_tc<0>, (int)blocks, emb::kThreadsE, sm, s, lat, L, anchors, gb, B, net, z);
+    launch_pdl(emb::k_embed_tc<0>, (int)blocks, emb::kThreadsE, sm, s, lat, L, anchors, gb, B, rows, net, z);
 }
 
 }  // namespace mfp
