@@ -9,7 +9,14 @@ iterations (tol = 0, parity mode), i.e. every row of SURVEY §8(a): init (a0),
 T x [4 x (gather a1, embed a2, split expansion a3, hidden GEMM chain a4, head
 a5, scatter a6), halo exchange a7, delta a8 every 16 iterations], final phase
 (a9).  N = 1: the whole domain on one B200.  N > 1 (torchrun): the same domain
-on a Py x Px processor grid (1x2, 2x2, 2x4), NCCL halo exchange — strong scaling.
+on a Py x Px processor grid (1x2, 2x2, 2x4), NCCL halo exchange — strong scaling
+(default).  --scaling weak: a 1024 x 2048-point block per GPU instead (1024x2048,
+2048x2048, 2048x4096, 4096x4096 at N = 1, 2, 4, 8).
+
+Extra legs on rank 0 after the timed region: e2e, the chain's roofline (CUDA events
+on its stream), time-to-converge (W-rand SDNet, exact subsolver vs DST-I, fitted
+SDNet vs the paper's MAE-0.05 rule), and at N = 1 the C3 batch sweep, the
+boundary-IO HBM roofline past L2 and the fp64 oracle on the host cores.
 
 value = UNIQUE predictions (T x 65,025) x K / max-over-ranks device time of the
 K timed steps (CUDA events on the solve stream, L2 flushed between steps, outside
@@ -47,6 +54,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--precision", default="bf16", choices=["bf16", "fp16", "fp32"])
     p.add_argument("--no-converge", action="store_true")
+    p.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                   help="strong: C5 (4097^2) at every N (default); weak: a 1024x2048 block per GPU")
     p.add_argument("--no-extras", action="store_true",
                    help="skip the legs after the timed region (e2e, sweep, boundary IO, CPU baseline): "
                         "used for the ncu launch list of the step")
@@ -128,10 +137,24 @@ def cpu_oracle_rate(target_s: float = 12.0):
     return n / dt, n, dt, oracle.num_threads()
 
 
-def bench_config(T: int, grid, tensor: bool) -> dict:
-    return {"workload": "C5: 4097x4097 points, m=32 (65,025 predictions/iteration), "
-                        f"{T} MFP iterations + final phase per step",
-            "nx": NX, "ny": NY, "m": 32, "iters_per_step": T, "grid": list(grid),
+def preds_per_iter(nx: int, ny: int) -> int:
+    return (2 * (nx // 32) - 1) * (2 * (ny // 32) - 1)
+
+
+def domain(world: int, scaling: str):
+    """strong: the C5 domain on every N; weak: a 1024 x 2048-point block per GPU
+    (1024x2048, 2048x2048, 2048x4096, 4096x4096)."""
+    if scaling == "strong":
+        return NX, NY
+    py, px = GRIDS[world]
+    return 1024 * px, 2048 * py
+
+
+def bench_config(T: int, grid, tensor: bool, nx: int = NX, ny: int = NY, scaling: str = "strong") -> dict:
+    wl = ("C5: 4097x4097 points, m=32 (65,025 predictions/iteration)" if (nx, ny) == (NX, NY) else
+          f"C5 weak scaling: {nx + 1}x{ny + 1} points, m=32 ({preds_per_iter(nx, ny):,} predictions/iteration)")
+    return {"workload": wl + f", {T} MFP iterations + final phase per step",
+            "nx": nx, "ny": ny, "m": 32, "iters_per_step": T, "grid": list(grid), "scaling": scaling,
             "subsolver": "sdnet d=128 L_h=3 (W-rand)", "gelu": "tanh" if tensor else "erf",
             "l2": "flushed between steps (512 MB write, outside the events)",
             "parallelism": f"domain {grid[0]}x{grid[1]}"}
@@ -153,9 +176,10 @@ def run_reference(args):
     v = tot_n / tot_t
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "predictions/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_t / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (GP boundary, W-rand SDNet weights)",
-            "config": bench_config(args.iters, GRIDS.get(args.gpus, (1, 1)), args.precision != "fp32"),
+            "config": bench_config(args.iters, GRIDS.get(args.gpus, (1, 1)), args.precision != "fp32",
+                                   *domain(args.gpus if args.gpus in GRIDS else 1, args.scaling), args.scaling),
             "cpu_baseline": {"value": v, "unit": "predictions/s", "cores": thr, "kind": "oracle",
                              "sample": f"{n_last} C5 subdomain SDNet predictions per step from the initial "
                                        "lattice (fp64 oracle, exact-erf GELU; a bounded sample of one "
@@ -295,16 +319,18 @@ def main():
         return float(t.item())
 
     grid = GRIDS[world]
+    nx, ny = domain(world, args.scaling)
+    ppi = preds_per_iter(nx, ny)
     prec = {"bf16": mfp.BF16, "fp16": mfp.FP16, "fp32": mfp.FP32}[args.precision]
     tensor = prec != mfp.FP32
-    cfg = mfp.make_config(NX, NY, grid, precision=prec, subsolver=mfp.SDNET, check_every=16)
+    cfg = mfp.make_config(nx, ny, grid, precision=prec, subsolver=mfp.SDNET, check_every=16)
     net = mfp.make_net(gelu=1 if tensor else 0)
     w = random_weights(0)
     stream = torch.cuda.Stream(device=dev)
     m = mfp.Mfp(cfg, net, w, rank=rank, nccl_comm=comm, stream=stream)
-    g_host = gp_boundary(NX, NY, 0)
+    g_host = gp_boundary(nx, ny, 0)
     g_dev = torch.from_numpy(g_host).to(dev)
-    u_dev = torch.empty((NY + 1, NX + 1), dtype=torch.float32, device=dev)
+    u_dev = torch.empty((ny + 1, nx + 1), dtype=torch.float32, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     T = args.iters
 
@@ -333,14 +359,14 @@ def main():
     torch.cuda.synchronize()
     ms = sum(a.elapsed_time(b) for a, b in ev)
     ms = max_over_ranks(ms)
-    preds = PRED_PER_ITER * T * args.steps
+    preds = ppi * T * args.steps
     value = preds / (ms / 1000.0)
 
     # e2e through the public host API: H2D of g + D2H of u inside the timed
     # region, from / into pinned host buffers
     if args.no_extras:
         if rank == 0:
-            print(json.dumps({"metric": METRIC, "value": PRED_PER_ITER * T * args.steps / (ms / 1000.0),
+            print(json.dumps({"metric": METRIC, "value": ppi * T * args.steps / (ms / 1000.0),
                               "unit": "predictions/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                               "ms_per_step": ms / args.steps, "note": "--no-extras (launch-list run)"}), flush=True)
         m.close()
@@ -349,7 +375,7 @@ def main():
         if world > 1:
             dist.destroy_process_group()
         return
-    u_pin = torch.empty((NY + 1, NX + 1) if rank == 0 else (1, 1), dtype=torch.float32).pin_memory()
+    u_pin = torch.empty((ny + 1, nx + 1) if rank == 0 else (1, 1), dtype=torch.float32).pin_memory()
     g_pin = torch.from_numpy(g_host).pin_memory()
     u_host, g_host = u_pin.numpy(), g_pin.numpy()
     for _ in range(1):
@@ -363,7 +389,7 @@ def main():
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     barrier()
     e2e = {"value": preds / e2e_s, "unit": "predictions/s", "h2d_bytes_per_step": g_host.nbytes,
-           "d2h_bytes_per_step": (NX + 1) * (NY + 1) * 4 if rank == 0 else 0}
+           "d2h_bytes_per_step": (nx + 1) * (ny + 1) * 4 if rank == 0 else 0}
 
     # roofline of the dominant kernel (the tcgen05 chain), events on its stream
     prof = m.profile(8)
@@ -411,7 +437,7 @@ def main():
                "note": "W-rand SDNet weights: the fixed point is not physically meaningful (SURVEY exp-5)"}
         # the same MFP with the exact discrete-Laplace subsolver: a provable fixed
         # point (the global 5-point solution), so time-to-converge is meaningful
-        cfg_x = mfp.make_config(NX, NY, grid, precision=mfp.FP32, subsolver=mfp.EXACT_LAPLACE, check_every=16)
+        cfg_x = mfp.make_config(nx, ny, grid, precision=mfp.FP32, subsolver=mfp.EXACT_LAPLACE, check_every=16)
         mx = mfp.Mfp(cfg_x, net, None, rank=rank, nccl_comm=comm, stream=stream)
         tol_x = 1e-6 * float(np.max(np.abs(g_host)))
         barrier()
@@ -429,7 +455,7 @@ def main():
             try:
                 sys.path.insert(0, os.path.join(ROOT, "tests"))
                 from _refsolve import dst_laplace
-                ref = dst_laplace(NX, NY, g_host.astype(np.float64))
+                ref = dst_laplace(nx, ny, g_host.astype(np.float64))
                 ref_dev = torch.from_numpy(ref.astype(np.float32)).to(dev)
                 ttc_x["max_err_vs_discrete_solution"] = float(np.max(np.abs(u_dev.cpu().numpy() - ref)))
                 ttc_x["mae_vs_discrete_solution"] = float(np.mean(np.abs(u_dev.cpu().numpy() - ref)))
@@ -482,9 +508,9 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "predictions/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-                "config": bench_config(T, grid, tensor),
-                "points_iter_per_s": (NX + 1) * (NY + 1) * T * args.steps / (ms / 1000.0),
+                "scaling": args.scaling, "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+                "config": bench_config(T, grid, tensor, nx, ny, args.scaling),
+                "points_iter_per_s": (nx + 1) * (ny + 1) * T * args.steps / (ms / 1000.0),
                 "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
                 "time_to_converge": ttc, "sdnet_batch_sweep": sweep, "boundary_io": bio, "clocks": clk.summary(),
                 "halo": halo_line(rep, prof, world)}
