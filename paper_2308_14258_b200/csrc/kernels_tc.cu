@@ -318,32 +318,11 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
     if (rank == 0 && lane == 0) {
       uint32_t pa[kSlots2] = {0u, 0u, 0u, 0u};
       const uint32_t ones_addr = smem_u32(S.ones);
-#ifdef MFP_SKEW
-      // Skewed round robin: slot s's k-th MMA (tile s + 4 (k / nh), layer k % nh)
-      // is issued in round k + s * MFP_SKEW, so consecutive slots sit MFP_SKEW
-      // layers apart and their MMA waits fall at different times instead of in
-      // lock step.  Each slot's MMAs stay in its own order: no cross-slot waits.
-      int64_t kmax[kSlots2];
-      int64_t rmax = 0;
-      for (int s = 0; s < kSlots2; s++) {
-        kmax[s] = nloc > s ? (int64_t)nh * ((nloc - s + kSlots2 - 1) / kSlots2) : 0;
-        if (kmax[s] > 0 && kmax[s] - 1 + s * MFP_SKEW > rmax) rmax = kmax[s] - 1 + s * MFP_SKEW;
-      }
-      for (int64_t r = 0; r <= rmax; r++) {
-#pragma unroll
-        for (int s = 0; s < kSlots2; s++) {
-          const int64_t kk = r - (int64_t)s * MFP_SKEW;
-          if (kk < 0 || kk >= kmax[s]) continue;
-          const int64_t j0 = s + kSlots2 * (kk / nh) - s;   // so that j0 + s is the tile
-          const int l = (int)(kk % nh);
-          {
-#else
       for (int64_t j0 = 0; j0 < nloc; j0 += kSlots2) {
         for (int l = 0; l < nh; l++) {
 #pragma unroll
           for (int s = 0; s < kSlots2; s++) {
             if (j0 + s >= nloc) continue;
-#endif
             mbar_wait(&S.bars[s], pa[s]);   // both CTAs' A operands of layer l written
             MFP_TR(kIssueWarp, j0 + s, l, 0);
             pa[s] ^= 1u;
