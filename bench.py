@@ -433,6 +433,7 @@ def main():
             e1.record(stream)
         torch.cuda.synchronize()
         ttc = {"ms": max_over_ranks(e0.elapsed_time(e1)), "iterations": rc.iterations,
+               "ms_without_final_phase": max_over_ranks(rc.ms_total - rc.ms_final),
                "converged": bool(rc.converged), "tol": tol, "last_delta": rc.last_delta,
                "note": "W-rand SDNet weights: the fixed point is not physically meaningful (SURVEY exp-5)"}
         # the same MFP with the exact discrete-Laplace subsolver: a provable fixed
@@ -448,6 +449,7 @@ def main():
             e1.record(stream)
         torch.cuda.synchronize()
         ttc_x = {"ms": max_over_ranks(e0.elapsed_time(e1)), "iterations": rx.iterations,
+                 "ms_without_final_phase": max_over_ranks(rx.ms_total - rx.ms_final),
                  "converged": bool(rx.converged), "tol": tol_x, "last_delta": rx.last_delta,
                  "subsolver": "exact discrete-Laplace (fp32)"}
         ref_dev = None
