@@ -66,6 +66,8 @@ struct mfp_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;         // halo exchange (overlaps interior phase 0)
   cudaEvent_t ev_packed = nullptr, ev_unpacked = nullptr;
+  float* pipe_host = nullptr;          // mfp_solve, one rank: D2H of the field overlapped with the final phase
+  cudaEvent_t ev_band[4] = {nullptr, nullptr, nullptr, nullptr};
   bool pending = false;                // an exchange is in flight on `side`
   bool use_graphs = false;             // replay blocks of c iterations as CUDA graphs
   int exchange_every = 1;              // halo exchange after every s-th iteration (NEXT-4)
@@ -438,7 +440,41 @@ mfp_status run_block(mfp_ctx* c, int kind) {
 }
 
 // Final phase into the device field u (row-major, ld = nx+1).
+// Single-rank SDNet final phase for mfp_solve with a HOST field: the atomic
+// subdomains run in 4 row bands, and each band's rows are copied to the host on
+// the side stream as soon as its chain kernel finishes, so the 67 MB D2H of C5
+// overlaps the remaining bands instead of following the whole phase.  Same
+// kernels, same per-row arithmetic as the one-shot path (bit-identical field).
+mfp_status final_phase_banded(mfp_ctx* c, float* u) {
+  RankState& rs = c->ranks[0];
+  const RankPlan& p = rs.plan;
+  const int W = c->cfg.nx + 1;
+  launch_final_lines(rs.lat, p.lat, 0, 0, p.bw, p.bh, u, W, c->stream);
+  c->launches++;
+  const int Kx = c->cfg.nx / kM, Ky = c->cfg.ny / kM;
+  const int nb = Ky < 4 ? Ky : 4;
+  const int per = (Ky + nb - 1) / nb;
+  for (int k = 0; k < nb; k++) {
+    const int r0 = k * per, r1 = std::min(Ky, (k + 1) * per);
+    if (r0 >= r1) break;
+    const int64_t s0 = (int64_t)r0 * Kx, nbk = (int64_t)(r1 - r0) * Kx;
+    embed(c, rs.lat, p.lat, rs.final_lat_anchor + s0, nullptr, nbk, rs.z);
+    c->launches++;
+    Sink sk{};
+    sk.mode = 1; sk.q = kQF; sk.anchors = rs.final_anchor + s0; sk.field = u; sk.ld = W;
+    chain(c, rs.z, nbk, kQF, sk);
+    if (!c->ev_band[k]) CK(cudaEventCreateWithFlags(&c->ev_band[k], cudaEventDisableTiming));
+    CK(cudaEventRecord(c->ev_band[k], c->stream));
+    CK(cudaStreamWaitEvent(c->side, c->ev_band[k], 0));
+    const int y0 = r0 * kM, y1 = (r1 == Ky) ? c->cfg.ny : r1 * kM - 1;   // line rows y = 32 r belong to the band above
+    CK(cudaMemcpyAsync(c->pipe_host + (int64_t)y0 * W, u + (int64_t)y0 * W, (size_t)(y1 - y0 + 1) * W * sizeof(float),
+                       cudaMemcpyDeviceToHost, c->side));
+  }
+  return MFP_OK;
+}
+
 mfp_status final_phase(mfp_ctx* c, float* u) {
+  if (c->pipe_host && c->R == 1 && c->cfg.subsolver == MFP_SDNET) return final_phase_banded(c, u);
   const int W = c->cfg.nx + 1;
   for (auto& rs : c->ranks) {
     const RankPlan& p = rs.plan;
@@ -721,6 +757,9 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
 }
 
 void mfp_destroy(mfp_ctx* c) {
+  if (c)
+    for (auto& e : c->ev_band)
+      if (e) cudaEventDestroy(e);
   if (!c) return;
   for (auto e : c->evpool) cudaEventDestroy(e);
   if (c->hdelta) cudaFreeHost(c->hdelta);
@@ -760,7 +799,14 @@ mfp_status mfp_solve(mfp_ctx* c, const float* g, int32_t max_iters, float tol, f
   }
   const bool root = (c->rank == 0 || c->rank == MFP_ALL_RANKS);
   float* u = u_out ? (root ? c->full : c->ranks[0].block) : nullptr;
+  const bool banded = u_out && root && c->R == 1 && c->cfg.subsolver == MFP_SDNET;
+  c->pipe_host = banded ? u_out : nullptr;
   mfp_status st = solve_impl(c, gd, max_iters, tol, u, u_out != nullptr, rep);
+  c->pipe_host = nullptr;
+  if (banded) {
+    CK(cudaStreamSynchronize(c->side));   // the band copies (also on error paths: no copy left in flight)
+    return st;
+  }
   if (st != MFP_OK && st != MFP_NOT_CONVERGED) return st;
   if (root && u_out) {
     const size_t nu = (size_t)(c->cfg.nx + 1) * (c->cfg.ny + 1);
