@@ -709,6 +709,7 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
   // graphs need a capturable (non-legacy) stream; MFP_NO_GRAPHS=1 disables them
   c->use_graphs = c->stream != nullptr && !(getenv("MFP_NO_GRAPHS") && getenv("MFP_NO_GRAPHS")[0] == '1');
   sdnet_kernel_attributes();
+  exact_kernel_attributes();
   tc_kernel_attributes();
   embed_tc_kernel_attributes();
   CK(cudaEventCreateWithFlags(&c->ev_packed, cudaEventDisableTiming));

@@ -145,6 +145,7 @@ void launch_gather_embed(const float* lat, const LatticeGeom& L, const uint32_t*
                          const float* gb, int64_t B, const DevNet& net, float* z,
                          cudaStream_t s);
 // exact subsolver phase (gather + H_c + scatter) for lattice anchors
+void exact_kernel_attributes();
 void launch_exact_phase(float* lat, const LatticeGeom& L, const uint32_t* anchors, int64_t B,
                         const float* HcT, cudaStream_t s);
 // exact subsolver for the final phase / batches: gb rows or lattice anchors -> sink
