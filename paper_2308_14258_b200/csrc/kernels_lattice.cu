@@ -3,8 +3,14 @@
 // pack/unpack (N7, a7), final-phase line copy (a9).  HBM-bound or latency-bound
 // work: coalesced line segments, grids sized in multiples of the SM count.
 #include "device_common.cuh"
+#include "tc_common.cuh"   // f2 packed fp32x2 helpers
 
 namespace mfp {
+
+using tcx::f2;
+using tcx::f2_make;
+using tcx::f2_split;
+using tcx::ffma2;
 
 // ---------------------------------------------------------------- a0: init
 // g (2(nx+ny), reading G6) onto the boundary lines of the local lattice; the
@@ -41,63 +47,72 @@ void launch_init_lattice(float* lat, const LatticeGeom& L, int nx, int ny, const
 // takes 8 subdomains at a time (their perimeters staged in smem by 16-byte
 // gathers), lane l owns outputs p = l and l + 32, and every H_c^T element it
 // loads from smem feeds 8 FMAs (one per subdomain) — 0.25 shared loads per FMA
-// instead of 1.  Persistent blocks (2 per SM) load H_c^T (32 KB) once.  Each
-// output keeps the plain k-ascending FMA chain, so results are unchanged.
-constexpr int kExactWarps = 8;
+// instead of 1, packed: one FFMA2 updates a lane's two outputs.  Persistent blocks
+// (one per SM, 16 warps) load H_c^T (32 KB) once.  Each output keeps the plain k-ascending
+// FMA chain (FFMA2 rounds per lane like FFMA), so results are unchanged.
+constexpr int kExactWarps = 16;
 constexpr int kExactSub = 8;   // subdomains per warp per round
 
 __global__ void __launch_bounds__(kExactWarps * 32)
 k_exact_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ anchors,
               int64_t B, const float* __restrict__ HcT) {
   extern __shared__ __align__(16) float ex_smem[];
-  float* sH = ex_smem;                                   // H_c^T [k][p], p padded to 64
+  // H_c^T interleaved per lane: sH[k][lane] = (H^T[k][lane], H^T[k][lane + 32]), so one
+  // 8-byte load gives a lane both of its outputs' coefficients and one packed FFMA2
+  // updates both outputs (p = lane, lane + 32) of a subdomain
+  float2* sH = reinterpret_cast<float2*>(ex_smem);
   float* sg = ex_smem + kNB * 64;                        // [warp][sub][k]
-  for (int i = threadIdx.x; i < kNB * 64 / 4; i += blockDim.x)
-    reinterpret_cast<float4*>(sH)[i] = __ldg(reinterpret_cast<const float4*>(HcT) + i);
+  for (int i = threadIdx.x; i < kNB * 32; i += blockDim.x) {
+    const int k = i >> 5, l = i & 31;
+    sH[i] = make_float2(__ldg(HcT + k * 64 + l), __ldg(HcT + k * 64 + 32 + l));
+  }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* g = sg + warp * kExactSub * kNB;
   const int64_t step = (int64_t)gridDim.x * kExactWarps * kExactSub;
   for (int64_t s0 = ((int64_t)blockIdx.x * kExactWarps + warp) * kExactSub; s0 < B; s0 += step) {
     uint32_t pk[kExactSub];
+    float4 gv[kExactSub];
 #pragma unroll
-    for (int j = 0; j < kExactSub; j++) {
-      const int64_t sj = s0 + j < B ? s0 + j : B - 1;
-      pk[j] = __ldg(anchors + sj);
-      reinterpret_cast<float4*>(g + j * kNB)[lane] = gather4(lat, L, pk[j], lane);
-    }
+    for (int j = 0; j < kExactSub; j++) pk[j] = __ldg(anchors + (s0 + j < B ? s0 + j : B - 1));
+#pragma unroll
+    for (int j = 0; j < kExactSub; j++) gv[j] = gather4(lat, L, pk[j], lane);   // 8 gathers in flight
+#pragma unroll
+    for (int j = 0; j < kExactSub; j++) reinterpret_cast<float4*>(g + j * kNB)[lane] = gv[j];
     __syncwarp();
-    float y0[kExactSub], y1[kExactSub];
+    f2 y[kExactSub];
 #pragma unroll
-    for (int j = 0; j < kExactSub; j++) y0[j] = y1[j] = 0.f;
+    for (int j = 0; j < kExactSub; j++) y[j] = f2_make(0.f, 0.f);
 #pragma unroll 2
     for (int k = 0; k < kNB; k += 4) {
-      float h0[4], h1[4];
+      f2 h[4];
 #pragma unroll
       for (int t = 0; t < 4; t++) {
-        h0[t] = sH[(k + t) * 64 + lane];
-        h1[t] = sH[(k + t) * 64 + 32 + lane];
+        const float2 hv = sH[(k + t) * 32 + lane];
+        h[t] = f2_make(hv.x, hv.y);
       }
 #pragma unroll
       for (int j = 0; j < kExactSub; j++) {
         const float4 gk = *reinterpret_cast<const float4*>(g + j * kNB + k);
-        y0[j] = fmaf(h0[0], gk.x, y0[j]); y1[j] = fmaf(h1[0], gk.x, y1[j]);
-        y0[j] = fmaf(h0[1], gk.y, y0[j]); y1[j] = fmaf(h1[1], gk.y, y1[j]);
-        y0[j] = fmaf(h0[2], gk.z, y0[j]); y1[j] = fmaf(h1[2], gk.z, y1[j]);
-        y0[j] = fmaf(h0[3], gk.w, y0[j]); y1[j] = fmaf(h1[3], gk.w, y1[j]);
+        y[j] = ffma2(h[0], f2_make(gk.x, gk.x), y[j]);
+        y[j] = ffma2(h[1], f2_make(gk.y, gk.y), y[j]);
+        y[j] = ffma2(h[2], f2_make(gk.z, gk.z), y[j]);
+        y[j] = ffma2(h[3], f2_make(gk.w, gk.w), y[j]);
       }
     }
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < kExactSub; j++) {
       if (s0 + j >= B) continue;
+      float y0, y1;
+      f2_split(y[j], y0, y1);
       int a, b;
       unpack_anchor(pk[j], a, b);
       int64_t dup;
       const int64_t c0 = centre_cell(a, b, lane, L.strideH, L.strideV, L.offV, &dup);
-      lat[c0] = y0[j];
-      if (dup >= 0) lat[dup] = y0[j];
-      if (lane + 32 < kQC) lat[centre_cell(a, b, lane + 32, L.strideH, L.strideV, L.offV, &dup)] = y1[j];
+      lat[c0] = y0;
+      if (dup >= 0) lat[dup] = y0;
+      if (lane + 32 < kQC) lat[centre_cell(a, b, lane + 32, L.strideH, L.strideV, L.offV, &dup)] = y1;
     }
   }
 }
@@ -107,7 +122,7 @@ void launch_exact_phase(float* lat, const LatticeGeom& L, const uint32_t* anchor
   if (B <= 0) return;
   const int per_block = kExactWarps * kExactSub;
   int64_t blocks = (B + per_block - 1) / per_block;
-  if (blocks > 148 * 2) blocks = 148 * 2;
+  if (blocks > 148) blocks = 148;
   const size_t smem = sizeof(float) * ((size_t)kNB * 64 + (size_t)kExactWarps * kExactSub * kNB);
   k_exact_phase<<<(int)blocks, kExactWarps * 32, smem, s>>>(lat, L, anchors, B, HcT);
 }
