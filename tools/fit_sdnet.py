@@ -101,6 +101,12 @@ def sample_boundaries(torch, n, device, gen):
     mask = (torch.rand(k, 4, device=device, generator=gen) < 0.35).float()
     mask = mask.repeat_interleave(M, dim=1)
     out[k:2 * k] = src * (1 - mask)
+    if BANK is not None:
+        # (e) boundaries the MFP iteration itself feeds the subsolver
+        # (tools/collect_mfp_boundaries.py): zero-interior starts to near convergence
+        nk = int(n * BANK_FRAC)
+        idx = torch.randint(0, BANK.shape[0], (nk,), device=device, generator=gen)
+        out[:nk] = BANK[idx]
     if SMOOTH > 0:
         # (d) harmonic polynomials of degree <= 3 with random coefficients: what a
         # subdomain sees near convergence on a large domain, where the MFP's slowly
@@ -123,6 +129,8 @@ def sample_boundaries(torch, n, device, gen):
 
 WIDE = False  # --wide: add random offsets / scales to the boundary mixture
 SMOOTH = 0.0  # --smooth f: fraction of the batch replaced by harmonic polynomials (degree <= 3)
+BANK = None   # --bank file: boundary vectors collected from MFP runs; BANK_FRAC of each batch
+BANK_FRAC = 0.5
 
 
 def main():
@@ -138,15 +146,20 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "weights", "sdnet_fit_d128.npy"))
     ap.add_argument("--wide", action="store_true")
     ap.add_argument("--smooth", type=float, default=0.0)
+    ap.add_argument("--bank", default=None)
+    ap.add_argument("--bank-frac", type=float, default=0.5)
     ap.add_argument("--normalized-loss", action="store_true")
     ap.add_argument("--init", default=None, help="start from these flat weights (MFCK order)")
     ap.add_argument("--eval", action="store_true", help="only evaluate --init")
     args = ap.parse_args()
-    global WIDE, SMOOTH
+    global WIDE, SMOOTH, BANK, BANK_FRAC
     WIDE = args.wide
     SMOOTH = args.smooth
+    BANK_FRAC = args.bank_frac
     dev = torch.device("cuda" if torch.cuda.is_available() else "cpu")
     torch.manual_seed(args.seed)
+    if args.bank:
+        BANK = torch.tensor(np.load(args.bank), dtype=torch.float32, device=dev)
     gen = torch.Generator(device=dev)
     gen.manual_seed(args.seed)
 
