@@ -408,7 +408,7 @@ def main():
         traffic = json.load(open(tfile)).get("chain_tc_dram_bytes_per_launch")
     roofline = {"bound": "tensor" if tensor else "alu", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                "kernel": "k_chain_tc (hidden GEMM chain a4 + epilogues a3/a5/a6)" if tensor else "k_chain_fp32",
+                "kernel": "k_chain_tc2 (hidden GEMM chain a4 + epilogues a3/a5/a6)" if tensor else "k_chain_fp32",
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"
                 if tensor else "derived fp32 SIMT peak (DESIGN.md §7)",
                 "chain_ms_per_launch": chain_ms, "chain_share_of_iteration":
