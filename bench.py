@@ -484,7 +484,7 @@ def main():
                 u_f = torch.empty((fy + 1, fx + 1), dtype=torch.float32, device=dev)
                 g_arg = torch.from_numpy(gf).to(dev)
                 chunk, done, dev_ms, mae, reached = 64, 0, 0.0, float("nan"), False
-                while done < 30016:
+                while done < 20032:
                     barrier()
                     with torch.cuda.stream(stream):
                         e0.record(stream)
