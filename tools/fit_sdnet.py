@@ -129,6 +129,7 @@ def sample_boundaries(torch, n, device, gen):
 
 WIDE = False  # --wide: add random offsets / scales to the boundary mixture
 SMOOTH = 0.0  # --smooth f: fraction of the batch replaced by harmonic polynomials (degree <= 3)
+QAT = None    # --qat bf16|fp16: train through the chain's 16-bit operand rounding
 BANK = None   # --bank file: boundary vectors collected from MFP runs; BANK_FRAC of each batch
 BANK_FRAC = 0.5
 
@@ -147,15 +148,18 @@ def main():
     ap.add_argument("--wide", action="store_true")
     ap.add_argument("--smooth", type=float, default=0.0)
     ap.add_argument("--bank", default=None)
+    ap.add_argument("--qat", default=None, choices=[None, "bf16", "fp16"])
     ap.add_argument("--bank-frac", type=float, default=0.5)
     ap.add_argument("--normalized-loss", action="store_true")
     ap.add_argument("--init", default=None, help="start from these flat weights (MFCK order)")
     ap.add_argument("--eval", action="store_true", help="only evaluate --init")
     args = ap.parse_args()
-    global WIDE, SMOOTH, BANK, BANK_FRAC
+    global WIDE, SMOOTH, BANK, BANK_FRAC, QAT
     WIDE = args.wide
     SMOOTH = args.smooth
     BANK_FRAC = args.bank_frac
+    if args.qat:
+        QAT = torch.bfloat16 if args.qat == "bf16" else torch.float16
     dev = torch.device("cuda" if torch.cuda.is_available() else "cpu")
     torch.manual_seed(args.seed)
     if args.bank:
@@ -185,7 +189,14 @@ def main():
             z = s.W1(x.flatten(1))
             h = F.gelu(z[:, None, :] + s.W2(X)[None])
             for lin in s.hid:
-                h = F.gelu(lin(h))
+                if QAT is not None:
+                    # the tensor-core chain's operands: activations h' and weights rounded
+                    # to 16 bit (RN), fp32 accumulate; straight-through gradients
+                    hq = h + (h.to(QAT).float() - h).detach()
+                    wq = lin.weight + (lin.weight.to(QAT).float() - lin.weight).detach()
+                    h = F.gelu(F.linear(hq, wq, lin.bias))
+                else:
+                    h = F.gelu(lin(h))
             return s.head(h)[..., 0]
 
         def load_flat(s, v):

@@ -1,0 +1,6 @@
+# quantization-aware fine-tune (bf16 operands) of the MFP-distribution fit
+mkdir -p gpurun_out/fit
+python paper_2308_14258_b200/build.py > gpurun_out/build.log 2>&1
+timeout 600 python tools/collect_mfp_boundaries.py --out /tmp/mfp_bank.npy 2>&1 | tail -1
+timeout 1500 python tools/fit_sdnet.py --init weights/sdnet_fit_d128_mfp.npy --steps 40000 --lr 1.5e-4 --batch 2048 --bank /tmp/mfp_bank.npy --bank-frac 0.5 --smooth 0.25 --qat bf16 --seed 5 --out gpurun_out/fit/w_qat.npy > gpurun_out/fit/w_qat.log 2>&1; tail -1 gpurun_out/fit/w_qat.log | cut -c1-300
+timeout 900 python tools/iters_to_mae.py --weights gpurun_out/fit/w_qat.npy --only "sdnet W-fit fp16,sdnet W-fit bf16" --grids 1x1 --max 10000 --chunk 100 2>&1 >/dev/null | cut -c1-200
