@@ -1,6 +1,7 @@
-"""The paper's accuracy criterion with fitted weights (NEXT-1): the fp16 MFP with
-the SDNet fitted on MFP-iteration boundaries (weights/sdnet_fit_d128_mfp.npy,
-tools/collect_mfp_boundaries.py + tools/fit_sdnet.py --bank) reaches MAE < 0.05
+"""The paper's accuracy criterion with fitted weights (NEXT-1): the bf16 MFP with
+the SDNet fitted on MFP-iteration boundaries through the chain's bf16 operand
+rounding (weights/sdnet_fit_d128_mfp.npy, tools/collect_mfp_boundaries.py +
+tools/fit_sdnet.py --bank --qat bf16) reaches MAE < 0.05
 against the discrete solution (P:179's stop rule) on a GP-boundary domain, and the
 same weights through the fp32 SIMT path agree with the fp64 oracle (fixed K)."""
 import os
@@ -26,12 +27,12 @@ def lib():
 
 
 @pytest.mark.skipif(not os.path.exists(W), reason="weights/sdnet_fit_d128_mfp.npy not generated")
-def test_fp16_mfp_reaches_paper_mae(lib):
+def test_bf16_mfp_reaches_paper_mae(lib):
     n = 1024
     w = np.load(W)
     g = gp_boundary(n, n, 0)
     ref = dst_laplace(n, n, g.astype(np.float64))
-    cfg = lib.make_config(n, n, precision=lib.FP16, subsolver=lib.SDNET, check_every=50)
+    cfg = lib.make_config(n, n, precision=lib.BF16, subsolver=lib.SDNET, check_every=50)
     m = lib.Mfp(cfg, lib.make_net(gelu=1), w)
     u, _ = m.solve(g, 50, 0.0)
     for _ in range(60):
