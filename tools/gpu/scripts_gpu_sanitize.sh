@@ -1,0 +1,10 @@
+#!/bin/bash
+# compute-sanitizer over the GPU parity tests (graphs off so every kernel is a plain launch)
+python paper_2308_14258_b200/build.py > /dev/null 2>&1
+export MFP_NO_GRAPHS=1
+timeout 1500 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_parity.py -q -x \
+  -k "batch_parity or phase_placement or exact_fixed_k_parity or full_size_sampled" 2>&1 | tail -4
+timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_boundary_io.py -q -x -k "not 1024" 2>&1 | tail -4
+for t in racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $t --print-limit 10 python -m pytest tests/test_gpu_parity.py -q -x -k "batch_parity and 333" 2>&1 | tail -3
+done
