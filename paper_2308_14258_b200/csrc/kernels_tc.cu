@@ -518,350 +518,6 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
 
 }  // namespace tc2
 
-// ---------------------------------------------------------------------------
-// Half tiles, ping-pong (tc4, MFP_CHAIN_HALF=1).  M = 128 pair MMAs (64 rows per
-// CTA): the accumulator of a half tile takes 64 TMEM columns (D column n < 64 in
-// lanes 0-63, n >= 64 in lanes 64-127 — the "2x2" datapath layout of 2-SM M = 128),
-// so eight slots fit the 512 columns.  Each epilogue warpgroup owns two slots and
-// alternates between them layer by layer: while the tensor core computes one
-// half tile's next layer, the warps run the other's epilogue — the MMA round
-// trip hides behind useful work instead of an idle wait.  A thread handles one
-// row and one 64-column half (its TMEM lane quadrant): warps q = 0, 1 rows 0-63 of
-// columns 0-63, q = 2, 3 the same rows of columns 64-127; the head's two partial
-// dot products of a row meet in shared memory.
-namespace tc4 {
-using namespace tc;
-using tc2::cluster_rank;
-using tc2::cluster_sync;
-using tc2::commit2;
-using tc2::mbar_arrive_remote;
-
-constexpr int kS4 = 8;                        // half-tile slots (TMEM 8 x 64 columns)
-constexpr int kRows4 = 64;                    // rows per CTA per half tile
-constexpr int kTile4 = kRows4 * kD * 2;       // 16 KB A operand
-constexpr int kZR4 = 3;                       // subdomains a 64-row half tile can touch (q >= 61)
-constexpr int kEpi4 = 16;
-constexpr int kAlloc4 = kEpi4, kIssue4 = kEpi4 + 1;
-constexpr int kThreads4 = 32 * (kEpi4 + 2);   // 576
-constexpr int kHalf4 = kWImg;
-
-template <int F16>
-constexpr uint32_t idesc4() {   // kind::f16, D fp32, M = 128 (pair), N = 128
-  return (1u << 4) | ((F16 ? 0u : 1u) << 7) | ((F16 ? 0u : 1u) << 10) | ((uint32_t)(kD >> 3) << 17) |
-         ((uint32_t)(128 >> 4) << 24);
-}
-template <int F16>
-__device__ __forceinline__ void mma4(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc4<F16>()), "r"(accum)
-      : "memory");
-}
-
-struct Smem4 {
-  uint8_t* W;      // [nh][18 KB]
-  uint8_t* A;      // [8][16 KB]
-  uint8_t* ones;   // 4 KB (rows 0-63 used)
-  float* zbuf;     // [8 slots][2][3][128]: z + W2[:,0]/2, z + W2[:,1]/2
-  float* ypart;    // [8 slots][64]: head partial of the upper column half
-  float* w2;       // [2][128]
-  float* wo;       // [128]
-  uint64_t* bars;  // a_full[8] (even CTA), d_full[8]
-  uint32_t* tmem_slot;
-};
-__device__ __forceinline__ Smem4 carve4(uint8_t* raw, int nh) {
-  Smem4 s;
-  s.W = raw;
-  s.A = raw + nh * kHalf4;
-  s.ones = s.A + kS4 * kTile4;
-  s.zbuf = (float*)(s.ones + kOnes);
-  s.ypart = s.zbuf + kS4 * 2 * kZR4 * kD;
-  s.w2 = s.ypart + kS4 * kRows4;
-  s.wo = s.w2 + 2 * kD;
-  s.bars = (uint64_t*)(s.wo + kD);
-  s.tmem_slot = (uint32_t*)(s.bars + 2 * kS4);
-  return s;
-}
-size_t smem_bytes4(int n_hidden) {
-  return (size_t)n_hidden * kHalf4 + kS4 * kTile4 + kOnes +
-         4 * ((size_t)kS4 * 2 * kZR4 * kD + kS4 * kRows4 + 3 * kD) + 16 * kS4 + 16;
-}
-
-template <int GELU, int F16>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads4, 1)
-k_chain_tc4(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, Sink sink) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const int nh = net.n_hidden;
-  const Smem4 S = carve4(smem_raw, nh);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-  uint64_t* const a_full = S.bars;
-  uint64_t* const d_full = S.bars + kS4;
-
-  for (int l = 0; l < nh; l++) {
-    const uint4* src =
-        reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(net.Wh_sw2) + (size_t)l * 2 * kHalf4 + rank * kHalf4);
-    uint4* dst = reinterpret_cast<uint4*>(S.W + l * kHalf4);
-    for (int i = threadIdx.x; i < kHalf4 / 16; i += kThreads4) dst[i] = __ldg(src + i);
-  }
-  for (int i = threadIdx.x; i < kD; i += kThreads4) {
-    S.wo[i] = (GELU == 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
-    S.w2[i] = __ldg(net.W2 + 2 * i);
-    S.w2[kD + i] = __ldg(net.W2 + 2 * i + 1);
-  }
-  if (threadIdx.x < kRows) {
-    const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
-    const int r = threadIdx.x;
-    *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + (r & 7) * 16) = make_uint4(one | (one << 16), 0u, 0u, 0u);
-    *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + 128 + (r & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
-  }
-  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kS4; s++) {
-      mbar_init(&a_full[s], 8);
-      mbar_init(&d_full[s], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == kAlloc4) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
-                 "r"(kTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-  }
-  fence_proxy_async();
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem = *S.tmem_slot;
-  pdl_launch_dependents();
-  pdl_wait();
-
-  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  const int64_t ntiles = (total_rows + 2 * kRows4 - 1) / (2 * kRows4);
-  const int64_t nloc = ntiles > cid ? (ntiles - cid + ncl - 1) / ncl : 0;
-  const int64_t nsub = total_rows / q;
-
-  if (warp == kIssue4) {
-    if (rank == 0 && lane == 0) {
-      uint32_t pa[kS4] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-      const uint32_t ones_addr = smem_u32(S.ones);
-      for (int64_t j0 = 0; j0 < nloc; j0 += kS4) {
-        for (int l = 0; l < nh; l++) {
-#pragma unroll
-          for (int s = 0; s < kS4; s++) {
-            if (j0 + s >= nloc) continue;
-            mbar_wait(&a_full[s], pa[s]);
-            pa[s] ^= 1u;
-            tc_fence_after();
-            const uint32_t d = tmem + (uint32_t)(s * 64);
-            const uint32_t a0 = smem_u32(S.A + s * kTile4), b0 = smem_u32(S.W + l * kHalf4);
-#pragma unroll
-            for (int k = 0; k < kD / 16; k++) {
-              const uint32_t off = (uint32_t)((k >> 2) * 8192 + (k & 3) * 32);
-              mma4<F16>(d, sw128_desc(a0 + off), sw128_desc(b0 + off), k > 0 ? 1u : 0u);
-            }
-            mma4<F16>(d, nosw_desc(ones_addr), nosw_desc(b0 + 16384u), 1u);   // bias step
-            commit2(&d_full[s]);
-          }
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp < kEpi4) {
-    const int k = warp >> 2;          // warpgroup: slots k (A) and k + 4 (B)
-    const int quad = warp & 3;
-    const int hh = quad >> 1;         // column half
-    const int row = (quad & 1) * 32 + lane;
-    const int tid = quad * 32 + lane; // 0..127 within the warpgroup
-    const int r7 = row & 7;
-    uint32_t a_sw[8];                 // this row's swizzled chunks in K-half hh of slot k's A
-    {
-      const uint32_t a_row = smem_u32(S.A + k * kTile4) + (uint32_t)hh * 8192u + (uint32_t)row * 128u;
-#pragma unroll
-      for (int j = 0; j < 8; j++) a_sw[j] = a_row + ((uint32_t)(j ^ r7) << 4);
-    }
-    constexpr uint32_t kBOff = 4u * kTile4;            // slot k + 4's A, as an immediate offset
-    const uint32_t t_rowA = tmem + (uint32_t)(k * 64) + ((uint32_t)(quad * 32) << 16);
-    const float bo = __ldg(net.bo);
-    auto row0_of = [&](int64_t j) -> int64_t { return (cid + j * ncl) * (2 * kRows4) + rank * kRows4; };
-    // z staging of a half tile: threads 0..95 move one float4 of its <= 3 subdomains
-    auto z_fetch = [&](int64_t j) -> float4 {
-      int64_t sidx = row0_of(j) / q + (tid >> 5);
-      if (sidx > nsub - 1) sidx = nsub - 1;
-      return __ldg(reinterpret_cast<const float4*>(z + sidx * kD + 4 * (tid & 31)));
-    };
-    auto z_stage = [&](int slot, const float4 v) {
-      if (tid >= 96) return;
-      const int zc = 4 * (tid & 31), zi = (tid >> 5) * kD + zc;
-      float* zb = S.zbuf + slot * 2 * kZR4 * kD;
-      const float4 a = *reinterpret_cast<const float4*>(S.w2 + zc);
-      const float4 b = *reinterpret_cast<const float4*>(S.w2 + kD + zc);
-      *reinterpret_cast<float4*>(zb + zi) =
-          make_float4(fmaf(0.5f, a.x, v.x), fmaf(0.5f, a.y, v.y), fmaf(0.5f, a.z, v.z), fmaf(0.5f, a.w, v.w));
-      *reinterpret_cast<float4*>(zb + kZR4 * kD + zi) =
-          make_float4(fmaf(0.5f, b.x, v.x), fmaf(0.5f, b.y, v.y), fmaf(0.5f, b.z, v.z), fmaf(0.5f, b.w, v.w));
-    };
-    auto arrive = [&](int slot) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote(&a_full[slot], 0u);
-    };
-    // one half tile's row bookkeeping
-    struct Rw { int64_t sidx; int p; bool valid; float qx, qy; int zo; };
-    auto row_info = [&](int64_t j) -> Rw {
-      Rw w;
-      const int64_t row0 = row0_of(j);
-      int64_t s_first = row0 / q;
-      if (s_first > nsub - 1) s_first = nsub - 1;
-      const int64_t grow = row0 + row;
-      w.valid = grow < total_rows;
-      const int64_t gr = w.valid ? grow : total_rows - 1;
-      w.sidx = gr / q;
-      w.p = (int)(gr - w.sidx * q);
-      query_xy(q, w.p, &w.qx, &w.qy);
-      w.zo = (int)(w.sidx - s_first);
-      if (w.zo < 0 || w.zo >= kZR4) w.zo = 0;
-      return w;
-    };
-    // split layer of one half tile into its A operand (this thread's column half)
-    auto split = [&](int slot, const Rw& w, uint32_t aoff) {
-      const bool centre = (q == kQC);
-      const bool vert = w.p < kM - 1;
-      const float* zb = S.zbuf + slot * 2 * kZR4 * kD;
-      const float* zs = zb + ((centre && !vert) ? kZR4 * kD : 0) + w.zo * kD;
-      const float* w1s = S.w2 + ((centre && vert) ? kD : 0);
-      const float q1 = centre ? (vert ? w.qy : w.qx) : w.qx - 0.5f;
-      const f2 Q1 = f2_make(q1, q1), QY = f2_make(w.qy, w.qy);
-#pragma unroll
-      for (int j16 = 0; j16 < 4; j16++) {
-        const int c0 = 64 * hh + 16 * j16;
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-          const float4 zz = *reinterpret_cast<const float4*>(zs + c0 + 4 * i);
-          const float4 aa = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
-          f2 v01 = ffma2(f2_make(aa.x, aa.y), Q1, f2_make(zz.x, zz.y));
-          f2 v23 = ffma2(f2_make(aa.z, aa.w), Q1, f2_make(zz.z, zz.w));
-          if (!centre) {
-            const float4 bb = *reinterpret_cast<const float4*>(S.w2 + kD + c0 + 4 * i);
-            v01 = ffma2(f2_make(bb.x, bb.y), QY, v01);
-            v23 = ffma2(f2_make(bb.z, bb.w), QY, v23);
-          }
-          f2_split(v01, v[4 * i], v[4 * i + 1]);
-          f2_split(v23, v[4 * i + 2], v[4 * i + 3]);
-        }
-        uint32_t wv[8];
-        act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v), *reinterpret_cast<uint32_t(*)[4]>(wv));
-        act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v + 8), *reinterpret_cast<uint32_t(*)[4]>(wv + 4));
-        st_shared_v4(a_sw[2 * j16] + aoff, wv[0], wv[1], wv[2], wv[3]);
-        st_shared_v4(a_sw[2 * j16 + 1] + aoff, wv[4], wv[5], wv[6], wv[7]);
-      }
-      fence_proxy_async();
-    };
-    // one layer's epilogue of one half tile (4 16-column chunks of this thread's half)
-    auto layer = [&](uint32_t t_row, uint32_t aoff, bool last, f2& yacc) {
-      auto run = [&](auto last_tag) {
-        constexpr bool LAST = decltype(last_tag)::value;
-        auto work16 = [&](const uint32_t (&r)[16], int c16) {
-          if constexpr (!LAST) {
-#pragma unroll
-            for (int c8 = 0; c8 < 2; c8++) {
-              const int g = 2 * c16 + c8;
-              float v[8];
-#pragma unroll
-              for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[c8 * 8 + e]);
-              uint32_t wv[4];
-              act8<GELU, F16>(v, wv);
-              st_shared_v4(a_sw[g] + aoff, wv[0], wv[1], wv[2], wv[3]);
-            }
-          } else {
-            head32<GELU, 16>(r, S.wo + 64 * hh + c16 * 16, yacc);
-          }
-        };
-        uint32_t ra[16], rb[16];
-        tmem_ld16(t_row, ra);
-        tmem_wait_ld_dep16(ra);
-#pragma unroll
-        for (int c16 = 0; c16 < 4; c16 += 2) {
-          tmem_ld16(t_row + (uint32_t)((c16 + 1) * 16), rb);
-          work16(ra, c16);
-          tmem_wait_ld_dep16(rb);
-          if (c16 + 2 < 4) tmem_ld16(t_row + (uint32_t)((c16 + 2) * 16), ra);
-          work16(rb, c16 + 1);
-          if (c16 + 2 < 4) tmem_wait_ld_dep16(ra);
-        }
-      };
-      if (last) run(std::true_type{});
-      else run(std::false_type{});
-      tc_fence_before();
-      if (!last) fence_proxy_async();
-    };
-
-    if (k < nloc) z_stage(k, z_fetch(k));
-    if (k + 4 < nloc) z_stage(k + 4, z_fetch(k + 4));
-    uint32_t pdA = 0u, pdB = 0u;
-    for (int64_t jA = k; jA < nloc; jA += kS4) {
-      const int64_t jB = jA + 4;
-      const bool hasB = jB < nloc;
-      named_sync(1 + k, 128);   // staged z of both half tiles visible
-      const bool nA = jA + kS4 < nloc, nB = jB + kS4 < nloc;
-      float4 zA = make_float4(0.f, 0.f, 0.f, 0.f), zB = zA;
-      if (nA) zA = z_fetch(jA + kS4);
-      if (nB) zB = z_fetch(jB + kS4);
-      const Rw wA = row_info(jA);
-      const Rw wB = row_info(hasB ? jB : jA);
-      split(k, wA, 0u);
-      arrive(k);
-      if (hasB) {
-        split(k + 4, wB, kBOff);
-        arrive(k + 4);
-      }
-      f2 yA = f2_make(0.f, 0.f), yB = f2_make(0.f, 0.f);
-      for (int l = 0; l < nh; l++) {
-        const bool last = (l == nh - 1);
-        mbar_wait(&d_full[k], pdA);
-        pdA ^= 1u;
-        tc_fence_after();
-        layer(t_rowA, 0u, last, yA);
-        if (!last) arrive(k);
-        if (hasB) {
-          mbar_wait(&d_full[k + 4], pdB);
-          pdB ^= 1u;
-          tc_fence_after();
-          layer(t_rowA + 4u * 64u, kBOff, last, yB);
-          if (!last) arrive(k + 4);
-        }
-      }
-      // head: the two column halves of a row meet in shared memory
-      float ya0, ya1, yb0, yb1;
-      f2_split(yA, ya0, ya1);
-      f2_split(yB, yb0, yb1);
-      if (hh == 1) {
-        S.ypart[k * kRows4 + row] = ya0 + ya1;
-        if (hasB) S.ypart[(k + 4) * kRows4 + row] = yb0 + yb1;
-      }
-      named_sync(1 + k, 128);
-      if (hh == 0) {
-        if (wA.valid) sink_store(sink, wA.sidx, wA.p, (ya0 + ya1) + S.ypart[k * kRows4 + row] + bo);
-        if (hasB && wB.valid) sink_store(sink, wB.sidx, wB.p, (yb0 + yb1) + S.ypart[(k + 4) * kRows4 + row] + bo);
-      }
-      if (nA) z_stage(k, zA);
-      if (nB) z_stage(k + 4, zB);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();
-  if (warp == kAlloc4) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
-  }
-}
-
-}  // namespace tc4
-
 
 
 bool chain_tc_available() { return true; }
@@ -880,20 +536,6 @@ void tc_kernel_attributes() {
   cudaFuncSetAttribute(tc2::k_chain_tc2<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
   cudaFuncSetAttribute(tc2::k_chain_tc2<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
   cudaFuncSetAttribute(tc2::k_chain_tc2<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
-  const int mx4 = (int)tc4::smem_bytes4(kMaxHidden);
-  cudaFuncSetAttribute(tc4::k_chain_tc4<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx4);
-  cudaFuncSetAttribute(tc4::k_chain_tc4<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx4);
-  cudaFuncSetAttribute(tc4::k_chain_tc4<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx4);
-  cudaFuncSetAttribute(tc4::k_chain_tc4<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx4);
-}
-
-static bool chain_half() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MFP_CHAIN_HALF");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
 }
 
 // Persistent grid: one CTA pair per TPC (74 clusters), or fewer for small batches.
@@ -901,20 +543,6 @@ void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const 
                      cudaStream_t s) {
   if (B <= 0) return;
   const int64_t rows = B * q;
-  if (chain_half()) {
-    const size_t sm4 = tc4::smem_bytes4(net.n_hidden);
-    const int64_t pt4 = (rows + 2 * tc4::kRows4 - 1) / (2 * tc4::kRows4);
-    const int64_t pairs4 = num_sms / 2;
-    const int grid4 = 2 * (int)(pt4 < pairs4 ? pt4 : pairs4);
-#define MFP_TC4(G, F) launch_pdl(tc4::k_chain_tc4<G, F>, grid4, tc4::kThreads4, sm4, s, z, rows, q, net, sink)
-    if (net.f16) {
-      if (net.gelu_tanh) MFP_TC4(1, 1); else MFP_TC4(0, 1);
-    } else {
-      if (net.gelu_tanh) MFP_TC4(1, 0); else MFP_TC4(0, 0);
-    }
-#undef MFP_TC4
-    return;
-  }
   const size_t sm = tc2::smem_bytes2(net.n_hidden);
   const int64_t ptiles = (rows + 2 * tc::kRows - 1) / (2 * tc::kRows);
   const int64_t pairs = num_sms / 2;
