@@ -139,6 +139,36 @@ def test_sdnet_tensorcore_distributed_2x4(lib, precision):
     assert rel_err(u, ref.u) <= BF16_TOL
 
 
+def test_exact_distributed_c4_full_size(lib):
+    """C4 (4097^2) on the 2x4 grid the 8-GPU bench uses, every rank on this device
+    (MFP_ALL_RANKS): two iterations against the oracle's D1 emulation (line lattice
+    and final field), at full size."""
+    nx = ny = 4096
+    grid = (2, 4)
+    g = gp_boundary(nx, ny, 0)
+    m, _ = make(lib, nx, ny, grid)
+    u, rep = m.solve(g, 2, 0.0)
+    ref = oracle.mfp_run(oracle.MfpConfig(nx, ny, Py=2, Px=4, subsolver="exact"), g.astype(np.float64), 2)
+    assert rel_err(gpu_lines(lib, m, nx, ny, grid), ref.lines, line_mask(nx, ny)) <= FP32_TOL
+    assert rel_err(u, ref.u) <= FP32_TOL
+
+
+def test_exact_distributed_c5_converges_to_dst(lib):
+    """SURVEY §8(d) "C5 8-GPU parity": the exact-subsolver MFP on the 2x4 grid at
+    4097^2, run to convergence (delta <= 1e-6 max|g|), lands on the global discrete
+    solution (DST-I) as the single-rank solve does (bench: max err 2.7e-3, fp32)."""
+    from tests._refsolve import dst_laplace
+    nx = ny = 4096
+    g = gp_boundary(nx, ny, 0)
+    m, _ = make(lib, nx, ny, (2, 4), check_every=16)
+    tol = 1e-6 * float(np.max(np.abs(g)))
+    u, rep = m.solve(g, 60000, tol)
+    assert rep.converged
+    ref = dst_laplace(nx, ny, g.astype(np.float64))
+    assert np.max(np.abs(u - ref)) < 5e-3
+    assert np.mean(np.abs(u - ref)) < 2e-3
+
+
 def test_exact_converges_to_discrete_solution(lib):
     """C2 to convergence against the scipy DST-I global discrete solution."""
     from tests._refsolve import dst_laplace
