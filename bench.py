@@ -528,7 +528,12 @@ def main():
                 "config": bench_config(T, grid, tensor, nx, ny, args.scaling),
                 "points_iter_per_s": (nx + 1) * (ny + 1) * T * args.steps / (ms / 1000.0),
                 "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
-                "time_to_converge": ttc, "sdnet_batch_sweep": sweep, "boundary_io": bio, "clocks": clk.summary(),
+                "time_to_converge": ttc, "sdnet_batch_sweep": sweep, "boundary_io": bio,
+                "paper_context": {"note": "the paper's own numbers, other hardware (context, not a baseline; "
+                                          "BASELINE.md)",
+                                  "mfp_2049_time_to_mae_0.05_s": 880.0, "mfp_2049_iterations_to_mae_0.05": 3200,
+                                  "hardware": "1 x A30, mpi4py (P:179, P:187)",
+                                  "derived_predictions_per_s": 58.7e3}, "clocks": clk.summary(),
                 "halo": halo_line(rep, prof, world)}
         print(json.dumps(line), flush=True)
     m.close()
