@@ -536,8 +536,15 @@ mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, floa
                       mfp_report* rep) {
   if (c->poisoned) return MFP_ERR_STATE;
   if (t < 1 || !(tol >= 0.f)) return fail(c, MFP_ERR_INVALID, "max_iters >= 1 and tol >= 0 required");
-  cudaEvent_t e0, e1, e2;
-  CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1)); CK(cudaEventCreate(&e2));
+  struct Events {   // destroyed on every return path
+    cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
+    ~Events() {
+      for (auto x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } ev3;
+  CK(cudaEventCreate(&ev3.e[0])); CK(cudaEventCreate(&ev3.e[1])); CK(cudaEventCreate(&ev3.e[2]));
+  cudaEvent_t e0 = ev3.e[0], e1 = ev3.e[1], e2 = ev3.e[2];
   c->launches = 0;
   CK(cudaEventRecord(e0, c->stream));
   if (g_dev) {
@@ -626,7 +633,6 @@ mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, floa
     rep->halo_msgs_per_iter = msgs;
     rep->gpu_launches = c->launches;
   }
-  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
   if (tol > 0.f && !converged) return MFP_NOT_CONVERGED;
   return MFP_OK;
 }
