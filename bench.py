@@ -468,7 +468,10 @@ def main():
         # through the chain's bf16 operand rounding (weights/sdnet_fit_d128_mfp.npy,
         # DESIGN.md §9), bf16 operands, on the paper's strong-scaling domain (2049^2,
         # P:179) and on the bench domain
-        wfit = os.path.join(ROOT, "weights", "sdnet_fit_d128_mfp.npy")
+        # (precision-specific: the fit trains through its own operand rounding)
+        fit_prec = mfp.FP16 if prec == mfp.FP16 else mfp.BF16
+        wfit = os.path.join(ROOT, "weights", "sdnet_fit_d128_mfp_fp16.npy" if fit_prec == mfp.FP16
+                            else "sdnet_fit_d128_mfp.npy")
         if os.path.exists(wfit) and tensor:
             w_fit = np.load(wfit)
             for name, (fx, fy) in (("paper_2049", (2048, 2048)), ("bench_domain", (nx, ny))):
@@ -479,7 +482,7 @@ def main():
                     sys.path.insert(0, os.path.join(ROOT, "tests"))
                     from _refsolve import dst_laplace
                     ref_f = torch.from_numpy(dst_laplace(fx, fy, gf.astype(np.float64)).astype(np.float32)).to(dev)
-                cfg_f = mfp.make_config(fx, fy, grid, precision=mfp.BF16, subsolver=mfp.SDNET, check_every=16)
+                cfg_f = mfp.make_config(fx, fy, grid, precision=fit_prec, subsolver=mfp.SDNET, check_every=16)
                 mf = mfp.Mfp(cfg_f, mfp.make_net(gelu=1), w_fit, rank=rank, nccl_comm=comm, stream=stream)
                 u_f = torch.empty((fy + 1, fx + 1), dtype=torch.float32, device=dev)
                 g_arg = torch.from_numpy(gf).to(dev)
@@ -505,7 +508,8 @@ def main():
                         reached = True
                         break
                 ttc[f"sdnet_w_fit_mae_0.05_{name}"] = {
-                    "domain": f"{fx + 1}x{fy + 1}", "precision": "bf16", "iterations": done, "reached": reached,
+                    "domain": f"{fx + 1}x{fy + 1}", "precision": "fp16" if fit_prec == mfp.FP16 else "bf16",
+                    "weights": os.path.basename(wfit), "iterations": done, "reached": reached,
                     "mae": mae, "ms": dev_ms,
                     "note": f"device time of {done // chunk} resumed solves of {chunk} iterations, each including "
                             "the final phase (the MAE needs the field); stop rule of P:179 (paper: 3,200 "
