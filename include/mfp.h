@@ -251,6 +251,30 @@ mfp_status mfp_scatter_phase(mfp_ctx* ctx, int32_t rank, int32_t phase, const fl
  * that every rank must use the same s.  Errors: INVALID. */
 mfp_status mfp_set_exchange_every(mfp_ctx* ctx, int32_t s);
 
+/* Device-initiated halo transport (the paper names
+ * direct GPU-GPU transfers via NVSHMEM as the way past its MPI exchange).
+ * communicate_new_boundaries then runs as two kernels and no NCCL call:
+ * the pack snapshots the owned send cells into one of two parity buffers of the
+ * rank's peer-memory region and publishes an epoch flag; the pull kernel waits
+ * for each stencil peer's flag, loads the peer's segment straight from the
+ * peer's region (NVLink P2P) into this rank's halo cells and signals
+ * "consumed" back.  The convergence allreduce and the final gather stay NCCL.
+ *
+ * mfp_p2p_export (one process per GPU, R > 1): allocates this rank's region
+ *   (cudaMalloc, owned by the context, freed by mfp_destroy) and writes its
+ *   64-byte cudaIpcMemHandle_t to handle_out (HOST).  The caller all-gathers the
+ *   handles (e.g. torch.distributed over any backend).
+ * mfp_p2p_open: handles (HOST) = R handles of 64 B in rank order for one
+ *   process per GPU (every rank must have exported), or NULL for MFP_ALL_RANKS
+ *   (every rank's region on this device, no IPC).  Switches the context to the
+ *   peer transport for the rest of its life; collective (every rank calls it at
+ *   the same iteration boundary, no solve in flight).  Before mfp_destroy the
+ *   ranks must synchronise (a peer may still read this rank's region).
+ * Errors: INVALID (wrong mode, NULL/non-NULL handles, already open, exchange
+ *   in flight), CUDA (allocation, IPC). */
+mfp_status mfp_p2p_export(mfp_ctx* ctx, void* handle_out);
+mfp_status mfp_p2p_open(mfp_ctx* ctx, const void* handles);
+
 /* Run ONE phase (class 0..3 in G2 order) on the current lattice of every local
  * rank, without exchange (debug / sampled parity at full size). */
 mfp_status mfp_step_phase(mfp_ctx* ctx, int32_t phase);

@@ -53,6 +53,9 @@ struct RankState {
   std::vector<int64_t> send_off, recv_off;
   int64_t nsend = 0, nrecv = 0;
   float* block = nullptr;  // owned block field (NCCL transport with R > 1)
+  char* p2p = nullptr;         // NEXT-2 peer-memory region (own cudaMalloc, IPC-exportable)
+  P2PPeer* p2p_tab = nullptr;  // device table of the stencil peers' regions
+  int p2p_np = 0;
 };
 
 }  // namespace
@@ -71,6 +74,8 @@ struct mfp_ctx {
   bool pending = false;                // an exchange is in flight on `side`
   bool use_graphs = false;             // replay blocks of c iterations as CUDA graphs
   int exchange_every = 1;              // halo exchange after every s-th iteration (NEXT-4)
+  bool p2p = false;                    // halo transport: peer-memory kernels (NEXT-2) instead of NCCL / copies
+  std::vector<void*> p2p_opened;       // IPC-mapped peer regions (multi-process)
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // [0] plain block, [1] block ending in a check
   int glaunches[2] = {0, 0};
   std::vector<RankState> ranks;
@@ -298,8 +303,48 @@ void run_phase(mfp_ctx* c, RankState& rs, int ph, int64_t b0 = 0, int64_t b1 = -
 // of the owned cells), then the transport — grouped ncclSend/ncclRecv, or
 // device copies for MFP_ALL_RANKS — and the unpack run on the side stream;
 // exchange_wait makes the main stream wait for the unpack.
+P2PSelf p2p_self(const RankState& rs) {
+  P2PSelf s{};
+  s.rank = rs.plan.rank;
+  s.flags = (unsigned long long*)rs.p2p;
+  s.epoch = (unsigned long long*)(rs.p2p + kP2PEpochOff);
+  s.counter = (unsigned int*)(rs.p2p + kP2PCounterOff);
+  s.sendbuf[0] = (float*)(rs.p2p + kP2PHeader);
+  s.sendbuf[1] = (float*)(rs.p2p + kP2PHeader + p2p_parity_bytes(rs.nsend));
+  return s;
+}
+
+// NEXT-2 transport (kernels_p2p.cu): pack + publish on the main stream, then
+// the fused pull + unpack on the side stream; no NCCL call, no host wait.
+mfp_status exchange_begin_p2p(mfp_ctx* c) {
+  for (auto& rs : c->ranks) {
+    launch_pack_p2p(rs.lat, rs.send_idx, rs.nsend, p2p_self(rs), rs.p2p_np, rs.p2p_tab, c->stream);
+    c->launches++;
+  }
+  CK(cudaEventRecord(c->ev_packed, c->stream));
+  CK(cudaStreamWaitEvent(c->side, c->ev_packed, 0));
+  cudaEvent_t h0 = nullptr;
+  if (c->profiling) {
+    h0 = ev(c);
+    cudaEventRecord(h0, c->side);
+  }
+  for (auto& rs : c->ranks) {
+    launch_pull_p2p(rs.lat, rs.recv_idx, rs.nrecv, p2p_self(rs), rs.p2p_np, rs.p2p_tab, c->side);
+    c->launches++;
+  }
+  CK(cudaEventRecord(c->ev_unpacked, c->side));
+  if (c->profiling) {
+    cudaEvent_t h1 = ev(c);
+    cudaEventRecord(h1, c->side);
+    c->spans.push_back({h0, h1, kKindHalo, 0});
+  }
+  c->pending = true;
+  return MFP_OK;
+}
+
 mfp_status exchange_begin(mfp_ctx* c) {
   if (c->R == 1) return MFP_OK;
+  if (c->p2p) return exchange_begin_p2p(c);
   for (auto& rs : c->ranks) {
     launch_pack(rs.lat, rs.send_idx, rs.nsend, rs.sendbuf, c->stream);
     c->launches++;
@@ -778,6 +823,12 @@ void mfp_destroy(mfp_ctx* c) {
     if (g) cudaGraphExecDestroy(g);
   if (c->ev_packed) cudaEventDestroy(c->ev_packed);
   if (c->ev_unpacked) cudaEventDestroy(c->ev_unpacked);
+  if (c->p2p) cudaStreamSynchronize(c->stream);
+  for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
+  for (auto& rs : c->ranks) {
+    if (rs.p2p) cudaFree(rs.p2p);
+    if (rs.p2p_tab) cudaFree(rs.p2p_tab);
+  }
   delete c;
 }
 
@@ -920,6 +971,92 @@ mfp_status mfp_set_exchange_every(mfp_ctx* c, int32_t s) {
       if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     c->exchange_every = s;
   }
+  return MFP_OK;
+}
+
+namespace {
+mfp_status p2p_alloc_own(mfp_ctx* c) {
+  for (auto& rs : c->ranks)
+    if (!rs.p2p) {
+      const size_t bytes = p2p_region_bytes(rs.nsend);
+      CK(cudaMalloc((void**)&rs.p2p, bytes));
+      CK(cudaMemset(rs.p2p, 0, bytes));
+    }
+  CK(cudaDeviceSynchronize());
+  return MFP_OK;
+}
+}  // namespace
+
+mfp_status mfp_p2p_export(mfp_ctx* c, void* handle_out) {
+  if (!c || !handle_out) return MFP_ERR_INVALID;
+  if (c->poisoned) return MFP_ERR_STATE;
+  if (c->rank == MFP_ALL_RANKS || c->R == 1)
+    return fail(c, MFP_ERR_INVALID, "p2p_export: only for one-process-per-GPU contexts with R > 1");
+  mfp_status st = p2p_alloc_own(c);
+  if (st) return st;
+  CK(cudaIpcGetMemHandle((cudaIpcMemHandle_t*)handle_out, c->ranks[0].p2p));
+  return MFP_OK;
+}
+
+mfp_status mfp_p2p_open(mfp_ctx* c, const void* handles) {
+  if (!c) return MFP_ERR_INVALID;
+  if (c->poisoned) return MFP_ERR_STATE;
+  if (c->R == 1) return fail(c, MFP_ERR_INVALID, "p2p_open: a 1x1 grid has no halo");
+  if (c->R > kP2PMaxRanks) return fail(c, MFP_ERR_INVALID, "p2p_open: more than 256 ranks");
+  if (c->p2p) return fail(c, MFP_ERR_INVALID, "p2p_open: already open");
+  if (c->pending) return fail(c, MFP_ERR_INVALID, "p2p_open: an exchange is in flight");
+  const bool all = (c->rank == MFP_ALL_RANKS);
+  if (all != (handles == nullptr))
+    return fail(c, MFP_ERR_INVALID, "p2p_open: handles must be NULL exactly for MFP_ALL_RANKS");
+  if (!all && !c->ranks[0].p2p) return fail(c, MFP_ERR_INVALID, "p2p_open: call mfp_p2p_export first");
+  mfp_status st = p2p_alloc_own(c);
+  if (st) return st;
+  GlobalPlan gp;
+  std::string err;
+  if ((st = build_plan(&c->cfg, MFP_ALL_RANKS, &gp, &err))) return fail(c, st, err);
+  std::vector<char*> base(c->R, nullptr);
+  if (all) {
+    for (auto& rs : c->ranks) base[rs.plan.rank] = rs.p2p;
+  } else {
+    base[c->rank] = c->ranks[0].p2p;
+    for (const auto& pp : c->ranks[0].plan.peers) {
+      if (base[pp.rank]) continue;
+      void* p = nullptr;
+      cudaIpcMemHandle_t h;
+      memcpy(&h, (const char*)handles + (size_t)pp.rank * sizeof(cudaIpcMemHandle_t), sizeof(h));
+      CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      c->p2p_opened.push_back(p);
+      base[pp.rank] = (char*)p;
+    }
+  }
+  for (auto& rs : c->ranks) {
+    std::vector<P2PPeer> tab;
+    for (size_t i = 0; i < rs.plan.peers.size(); i++) {
+      const int q = rs.plan.peers[i].rank;
+      const RankPlan& qp = gp.ranks[q];
+      int64_t off = 0, nq = 0, len = -1;
+      for (const auto& x : qp.peers) {
+        if (x.rank == rs.plan.rank) { len = (int64_t)x.send_idx.size(); off = nq; }
+        nq += (int64_t)x.send_idx.size();
+      }
+      if (len != (int64_t)rs.plan.peers[i].recv_idx.size())
+        return fail(c, MFP_ERR_INVALID, "p2p_open: send/recv segment mismatch");
+      P2PPeer e{};
+      e.rank = q;
+      e.flags = (unsigned long long*)base[q];
+      e.sendbuf[0] = (const float*)(base[q] + kP2PHeader);
+      e.sendbuf[1] = (const float*)(base[q] + kP2PHeader + p2p_parity_bytes(nq));
+      e.send_off = off;
+      e.recv_off = rs.recv_off[i];
+      tab.push_back(e);
+    }
+    rs.p2p_np = (int)tab.size();
+    CK(cudaMalloc((void**)&rs.p2p_tab, std::max<size_t>(1, tab.size()) * sizeof(P2PPeer)));
+    if (!tab.empty()) CK(cudaMemcpy(rs.p2p_tab, tab.data(), tab.size() * sizeof(P2PPeer), cudaMemcpyHostToDevice));
+  }
+  for (auto& g : c->gexec)
+    if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+  c->p2p = true;
   return MFP_OK;
 }
 

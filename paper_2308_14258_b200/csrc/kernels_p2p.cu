@@ -1,0 +1,102 @@
+// NEXT-2: device-initiated halo exchange over peer memory (the
+// paper points at NVSHMEM for direct GPU-GPU transfers).  Replaces the
+// grouped ncclSend/ncclRecv + unpack of communicate_new_boundaries with
+// two kernels and no host-side collective:
+//   k_pack_p2p  (main stream): waits until every peer has consumed the send
+//               buffer of the same parity two exchanges ago, snapshots the
+//               owned send cells into sendbuf[e & 1] ("new boundaries"),
+//               and the last block publishes packed = e (release, system scope);
+//   k_pull_p2p  (side stream): waits for each peer's packed >= e, loads the
+//               peer's sendbuf[e & 1] segment addressed to this rank straight
+//               over NVLink (or from the same device when every rank lives in
+//               one process) into the halo cells of this rank's lattice (the
+//               unpack is fused), and the last block publishes consumed[me] = e
+//               on every peer and advances this rank's epoch.
+// The epoch lives in device memory, so both kernels replay unchanged inside
+// the CUDA graphs of §8.  Deadlock freedom: pack(e) waits only
+// on peers' pull(e - 2), pull(e) only on peers' pack(e); neither depends on a
+// later kernel of the waiting rank.
+#include "mfp_internal.h"
+
+namespace mfp {
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Thread 0 of the block spins until *flag >= want; the block then proceeds.
+__device__ __forceinline__ void block_wait_ge(const unsigned long long* flag, unsigned long long want) {
+  if (threadIdx.x == 0)
+    while (ld_acquire_sys(flag) < want) __nanosleep(64);
+  __syncthreads();
+}
+
+// Returns true in exactly one thread of the last block to finish (classic
+// threadfence reduction); the counter is re-armed for the next launch.
+__device__ __forceinline__ bool last_block(unsigned int* counter) {
+  __shared__ bool am_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(counter, 1u);
+    am_last = (t == gridDim.x - 1);
+    if (am_last) *counter = 0;
+  }
+  __syncthreads();
+  return am_last && threadIdx.x == 0;
+}
+
+__global__ void k_pack_p2p(const float* __restrict__ lat, const int32_t* __restrict__ idx, int64_t n,
+                           P2PSelf self, int npeers, const P2PPeer* __restrict__ peers) {
+  const unsigned long long e = *self.epoch + 1;
+  // sendbuf[e & 1] was last read by the peers' pull(e - 2)
+  if (e > 2)
+    for (int i = 0; i < npeers; i++) block_wait_ge(self.flags + kP2PConsumed + peers[i].rank, e - 2);
+  float* buf = self.sendbuf[e & 1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = lat[__ldg(idx + i)];
+  if (last_block(self.counter + 0)) {
+    __threadfence_system();
+    st_release_sys(self.flags + kP2PPacked, e);
+  }
+}
+
+__global__ void k_pull_p2p(float* __restrict__ lat, const int32_t* __restrict__ idx, int64_t n,
+                           P2PSelf self, int npeers, const P2PPeer* __restrict__ peers) {
+  const unsigned long long e = *self.epoch + 1;
+  for (int i = 0; i < npeers; i++) block_wait_ge(peers[i].flags + kP2PPacked, e);
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    int i = 0;
+    while (i + 1 < npeers && j >= peers[i + 1].recv_off) i++;
+    const P2PPeer& p = peers[i];
+    // plain (weak) load is ordered after the acquire above by the block barrier
+    lat[__ldg(idx + j)] = p.sendbuf[e & 1][p.send_off + (j - p.recv_off)];
+  }
+  if (last_block(self.counter + 1)) {
+    __threadfence_system();
+    for (int i = 0; i < npeers; i++) st_release_sys(peers[i].flags + kP2PConsumed + self.rank, e);
+    *self.epoch = e;
+  }
+}
+
+static int grid_p2p(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b > 148) b = 148;  // one block per SM at most: every block spins on the flags
+  return b < 1 ? 1 : (int)b;
+}
+
+void launch_pack_p2p(const float* lat, const int32_t* idx, int64_t n, const P2PSelf& self, int npeers,
+                     const P2PPeer* peers, cudaStream_t s) {
+  k_pack_p2p<<<grid_p2p(n), 256, 0, s>>>(lat, idx, n, self, npeers, peers);
+}
+void launch_pull_p2p(float* lat, const int32_t* idx, int64_t n, const P2PSelf& self, int npeers,
+                     const P2PPeer* peers, cudaStream_t s) {
+  k_pull_p2p<<<grid_p2p(n), 256, 0, s>>>(lat, idx, n, self, npeers, peers);
+}
+
+}  // namespace mfp

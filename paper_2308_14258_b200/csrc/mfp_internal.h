@@ -168,6 +168,37 @@ void launch_delta(const float* lat, const float* snap, const int64_t* segs, int 
                   unsigned int* out /* [0]=max bits, [1]=nonfinite flag */, cudaStream_t s);
 void launch_pack(const float* lat, const int32_t* idx, int64_t n, float* buf, cudaStream_t s);
 void launch_unpack(float* lat, const int32_t* idx, int64_t n, const float* buf, cudaStream_t s);
+// NEXT-2 peer-memory halo transport (kernels_p2p.cu).  A rank's P2P region
+// (one cudaMalloc, IPC-exportable): u64 flags[kP2PFlags] at 0 (packed epoch at
+// kP2PPacked, consumed epoch of consumer rank r at kP2PConsumed + r), the u64
+// epoch at kP2PEpochOff, two u32 block counters at kP2PCounterOff, then
+// sendbuf[0] at kP2PHeader and sendbuf[1] at kP2PHeader + p2p_parity_bytes(nsend).
+constexpr int kP2PMaxRanks = 256;
+constexpr int kP2PPacked = 0;
+constexpr int kP2PConsumed = 8;
+constexpr size_t kP2PEpochOff = (size_t)(kP2PConsumed + kP2PMaxRanks) * 8;
+constexpr size_t kP2PCounterOff = kP2PEpochOff + 64;
+constexpr size_t kP2PHeader = 4096;
+inline size_t p2p_parity_bytes(int64_t nsend) { return ((size_t)(nsend > 0 ? nsend : 1) * 4 + 255) / 256 * 256; }
+inline size_t p2p_region_bytes(int64_t nsend) { return kP2PHeader + 2 * p2p_parity_bytes(nsend); }
+struct P2PSelf {
+  int rank;
+  unsigned long long* flags;  // own region
+  unsigned long long* epoch;
+  unsigned int* counter;      // [2]
+  float* sendbuf[2];
+};
+struct P2PPeer {               // device table, one entry per stencil peer, recv_off ascending
+  int rank;
+  unsigned long long* flags;  // the peer's region (peer memory)
+  const float* sendbuf[2];    // the peer's send buffers
+  int64_t send_off;           // this rank's segment inside the peer's send buffer
+  int64_t recv_off;           // the segment's start in this rank's recv list
+};
+void launch_pack_p2p(const float* lat, const int32_t* idx, int64_t n, const P2PSelf& self, int npeers,
+                     const P2PPeer* peers, cudaStream_t s);
+void launch_pull_p2p(float* lat, const int32_t* idx, int64_t n, const P2PSelf& self, int npeers,
+                     const P2PPeer* peers, cudaStream_t s);
 void launch_final_lines(const float* lat, const LatticeGeom& L, int X0, int Y0, int bw, int bh,
                         float* field, int ld, cudaStream_t s);
 // one-time preparation (kernels_prep.cu)

@@ -102,6 +102,8 @@ _SIGS = {
     "mfp_gather_phase": [_vp, _i32, _i32, _vp, _i64, _P(_i64), _P(_i32), _P(_i32)],
     "mfp_scatter_phase": [_vp, _i32, _i32, _vp, _i64, _P(ctypes.c_float)],
     "mfp_set_exchange_every": [_vp, _i32],
+    "mfp_p2p_export": [_vp, _vp],
+    "mfp_p2p_open": [_vp, _vp],
     "mfp_nccl_get_unique_id": [_vp],
     "mfp_nccl_comm_init": [_i32, _vp, _i32, _P(_vp)],
     "mfp_nccl_comm_destroy": [_vp],
@@ -217,6 +219,20 @@ def mfp_scatter_phase(ctx, rank: int, phase: int, pred_dev, B: int, want_norm: b
 
 def mfp_set_exchange_every(ctx, s: int) -> None:
     _check(_lib.mfp_set_exchange_every(ctx, s), ctx)
+
+
+def mfp_p2p_export(ctx) -> bytes:
+    """NEXT-2: this rank's 64-byte IPC handle of its peer-memory halo region."""
+    h = ctypes.create_string_buffer(64)
+    _check(_lib.mfp_p2p_export(ctx, h), ctx)
+    return h.raw
+
+
+def mfp_p2p_open(ctx, handles=None) -> None:
+    """NEXT-2: switch to the peer-memory halo transport.  handles: the R
+    exported handles in rank order (one process per GPU), None for ALL_RANKS."""
+    buf = None if handles is None else ctypes.create_string_buffer(b"".join(handles), 64 * len(handles))
+    _check(_lib.mfp_p2p_open(ctx, buf), ctx)
 
 
 def mfp_step_phase(ctx, phase: int) -> None:
