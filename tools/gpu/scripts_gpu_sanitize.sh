@@ -8,3 +8,8 @@ timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest 
 for t in racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $t --print-limit 10 python -m pytest tests/test_gpu_parity.py -q -x -k "batch_parity and 333" 2>&1 | tail -3
 done
+# NEXT-2 peer-memory transport (spin-waits on epoch flags, last-block publication)
+for t in memcheck synccheck racecheck; do
+  MFP_NO_GRAPHS=1 timeout 900 compute-sanitizer --tool $t --print-limit 10 python -m pytest tests/test_gpu_p2p.py -q -x \
+    -k "grid0 or grid3 or errors" 2>&1 | tail -3
+done
