@@ -29,10 +29,14 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Thread 0 of the block spins until *flag >= want; the block then proceeds.
-__device__ __forceinline__ void block_wait_ge(const unsigned long long* flag, unsigned long long want) {
-  if (threadIdx.x == 0)
-    while (ld_acquire_sys(flag) < want) __nanosleep(64);
+// Thread i < npeers spins until flag(i) >= want (all peers polled in parallel,
+// one system-scope round trip instead of npeers); the block then proceeds.
+template <class F>
+__device__ __forceinline__ void block_wait_peers(int npeers, F flag, unsigned long long want) {
+  if (threadIdx.x < npeers) {
+    const unsigned long long* f = flag(threadIdx.x);
+    while (ld_acquire_sys(f) < want) __nanosleep(64);
+  }
   __syncthreads();
 }
 
@@ -56,7 +60,7 @@ __global__ void k_pack_p2p(const float* __restrict__ lat, const int32_t* __restr
   const unsigned long long e = *self.epoch + 1;
   // sendbuf[e & 1] was last read by the peers' pull(e - 2)
   if (e > 2)
-    for (int i = 0; i < npeers; i++) block_wait_ge(self.flags + kP2PConsumed + peers[i].rank, e - 2);
+    block_wait_peers(npeers, [&](int i) { return self.flags + kP2PConsumed + peers[i].rank; }, e - 2);
   float* buf = self.sendbuf[e & 1];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     buf[i] = lat[__ldg(idx + i)];
@@ -69,7 +73,7 @@ __global__ void k_pack_p2p(const float* __restrict__ lat, const int32_t* __restr
 __global__ void k_pull_p2p(float* __restrict__ lat, const int32_t* __restrict__ idx, int64_t n,
                            P2PSelf self, int npeers, const P2PPeer* __restrict__ peers) {
   const unsigned long long e = *self.epoch + 1;
-  for (int i = 0; i < npeers; i++) block_wait_ge(peers[i].flags + kP2PPacked, e);
+  block_wait_peers(npeers, [&](int i) { return (const unsigned long long*)peers[i].flags + kP2PPacked; }, e);
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     int i = 0;
     while (i + 1 < npeers && j >= peers[i + 1].recv_off) i++;
