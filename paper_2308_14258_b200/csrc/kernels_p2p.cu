@@ -5,7 +5,7 @@
 //   k_pack_p2p  (main stream): waits until every peer has consumed the send
 //               buffer of the same parity two exchanges ago, snapshots the
 //               owned send cells into sendbuf[e & 1] ("new boundaries"),
-//               and the last block publishes packed = e (release, system scope);
+//               and the last block publishes packed = e (fence.sc.sys + relaxed store);
 //   k_pull_p2p  (side stream): waits for each peer's packed >= e, loads the
 //               peer's sendbuf[e & 1] segment addressed to this rank straight
 //               over NVLink (or from the same device when every rank lives in
@@ -25,8 +25,11 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// Relaxed system-scope store; preceded by one __threadfence_system() (fence.sc.sys)
+// it forms the release pattern, so a block publishing to 8 peers pays one system
+// membar instead of the one st.release.sys emits per store (MEMBAR.ALL.SYS each).
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // Thread i < npeers spins until flag(i) >= want (all peers polled in parallel,
@@ -66,7 +69,7 @@ __global__ void k_pack_p2p(const float* __restrict__ lat, const int32_t* __restr
     buf[i] = lat[__ldg(idx + i)];
   if (last_block(self.counter + 0)) {
     __threadfence_system();
-    st_release_sys(self.flags + kP2PPacked, e);
+    st_relaxed_sys(self.flags + kP2PPacked, e);
   }
 }
 
@@ -83,7 +86,7 @@ __global__ void k_pull_p2p(float* __restrict__ lat, const int32_t* __restrict__ 
   }
   if (last_block(self.counter + 1)) {
     __threadfence_system();
-    for (int i = 0; i < npeers; i++) st_release_sys(peers[i].flags + kP2PConsumed + self.rank, e);
+    for (int i = 0; i < npeers; i++) st_relaxed_sys(peers[i].flags + kP2PConsumed + self.rank, e);
     *self.epoch = e;
   }
 }
