@@ -2,20 +2,23 @@
 // paper points at NVSHMEM for direct GPU-GPU transfers).  Replaces the
 // grouped ncclSend/ncclRecv + unpack of communicate_new_boundaries with
 // two kernels and no host-side collective:
-//   k_pack_p2p  (main stream): waits until every peer has consumed the send
-//               buffer of the same parity two exchanges ago, snapshots the
-//               owned send cells into sendbuf[e & 1] ("new boundaries"),
+//   k_pack_p2p  (main stream): snapshots the owned send cells into
+//               sendbuf[e & 1] ("new boundaries"; the previous pull made
+//               sure every peer has consumed that buffer's exchange e - 2),
 //               and the last block publishes packed = e (fence.sc.sys + relaxed store);
 //   k_pull_p2p  (side stream): waits for each peer's packed >= e, loads the
 //               peer's sendbuf[e & 1] segment addressed to this rank straight
 //               over NVLink (or from the same device when every rank lives in
 //               one process) into the halo cells of this rank's lattice (the
 //               unpack is fused), and the last block publishes consumed[me] = e
-//               on every peer and advances this rank's epoch.
+//               on every peer, waits until every peer has consumed exchange
+//               e - 1 (so pack(e + 1) may overwrite that parity buffer; the host
+//               orders every pack after the previous pull, exchange_wait) and
+//               advances this rank's epoch.
 // The epoch lives in device memory, so both kernels replay unchanged inside
-// the CUDA graphs of §8.  Deadlock freedom: pack(e) waits only
-// on peers' pull(e - 2), pull(e) only on peers' pack(e); neither depends on a
-// later kernel of the waiting rank.
+// the CUDA graphs of §8.  Deadlock freedom: pull(e) waits on
+// peers' pack(e) and pull(e - 1), pack never waits; neither depends on a later
+// kernel of the waiting rank.
 #include "mfp_internal.h"
 
 namespace mfp {
@@ -60,10 +63,9 @@ __device__ __forceinline__ bool last_block(unsigned int* counter) {
 
 __global__ void k_pack_p2p(const float* __restrict__ lat, const int32_t* __restrict__ idx, int64_t n,
                            P2PSelf self, int npeers, const P2PPeer* __restrict__ peers) {
+  // sendbuf[e & 1] was last read by the peers' pull(e - 2); this rank's pull(e - 1)
+  // saw them consume it, and the host orders pack(e) after pull(e - 1)
   const unsigned long long e = *self.epoch + 1;
-  // sendbuf[e & 1] was last read by the peers' pull(e - 2)
-  if (e > 2)
-    block_wait_peers(npeers, [&](int i) { return self.flags + kP2PConsumed + peers[i].rank; }, e - 2);
   float* buf = self.sendbuf[e & 1];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     buf[i] = lat[__ldg(idx + i)];
@@ -87,6 +89,9 @@ __global__ void k_pull_p2p(float* __restrict__ lat, const int32_t* __restrict__ 
   if (last_block(self.counter + 1)) {
     __threadfence_system();
     for (int i = 0; i < npeers; i++) st_relaxed_sys(peers[i].flags + kP2PConsumed + self.rank, e);
+    // free sendbuf[(e + 1) & 1] for pack(e + 1): the peers' pull(e - 1) has read it
+    for (int i = 0; i < npeers; i++)
+      while (ld_acquire_sys(self.flags + kP2PConsumed + peers[i].rank) + 1 < e) __nanosleep(64);
     *self.epoch = e;
   }
 }
