@@ -7,8 +7,9 @@ One STEP = one complete mfp_solve of the C5 workload (4097 x 4097 grid points,
 m = 32, 65,025 subdomain predictions per iteration = 4 phases) for T fixed
 iterations (tol = 0, parity mode), i.e. every row of SURVEY §8(a): init (a0),
 T x [4 x (gather a1, embed a2, split expansion a3, hidden GEMM chain a4, head
-a5, scatter a6), halo exchange a7, delta a8 every 16 iterations], final phase
-(a9).  N = 1: the whole domain on one B200.  N > 1 (torchrun): the same domain
+a5, scatter a6), halo exchange a7], delta a8 after every 16th iteration (the
+library evaluates delta every check_every = 16 iterations also in the fixed-
+iteration parity mode; tol = 0 only disables the stop), final phase (a9).  N = 1: the whole domain on one B200.  N > 1 (torchrun): the same domain
 on a Py x Px processor grid (1x2, 2x2, 2x4), NCCL halo exchange — strong scaling
 (default).  --scaling weak: a 1024 x 2048-point block per GPU instead (1024x2048,
 2048x2048, 2048x4096, 4096x4096 at N = 1, 2, 4, 8).
@@ -138,6 +139,57 @@ def cpu_oracle_rate(target_s: float = 12.0):
     oracle.predict_from_field(cfg, U, anc[:n], 0, w)
     dt = time.perf_counter() - t0
     return n / dt, n, dt, oracle.num_threads()
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def set_oracle_threads(n: int) -> None:
+    """OpenMP thread count of the oracle's parallel regions (libgomp ICV of this thread)."""
+    import ctypes
+    ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+
+
+def cpu_baseline_leg() -> dict:
+    """The oracle as it stands on the box's host cores (BASELINE.md "CPU baseline
+    plan"), bounded to ~25 s: (1) the metric's unit on a C5 sample with every
+    core, 5 runs -> median / min / max; (2) the same with 1 thread, 3 runs;
+    (3) exact-subsolver MFP solves to delta <= 1e-6 max|g| (c = 16) at C1 (65^2)
+    and C2 (513^2), wall time and iterations."""
+    import oracle
+    from mfp_inputs import gp_boundary
+    allc = oracle.num_threads()
+    runs = [cpu_oracle_rate(target_s=2.0) for _ in range(5)]
+    rates = [r[0] for r in runs]
+    set_oracle_threads(1)
+    try:
+        one = [cpu_oracle_rate(target_s=1.0) for _ in range(3)]
+    finally:
+        set_oracle_threads(allc)
+    conv = {}
+    for name, n in (("C1_65x65", 64), ("C2_513x513", 512)):
+        g = gp_boundary(n, n, 0).astype(np.float64)
+        tol = 1e-6 * float(np.max(np.abs(g)))
+        t0 = time.perf_counter()
+        r = oracle.mfp_run(oracle.MfpConfig(n, n, subsolver="exact", check_every=16), g, 200000, tol=tol)
+        conv[name] = {"seconds": time.perf_counter() - t0, "iterations": r.iterations, "tol": tol,
+                      "subsolver": "exact discrete Laplace (fp64)", "threads": allc}
+    return {"value": float(statistics.median(rates)), "unit": "predictions/s", "cores": allc, "kind": "oracle",
+            "min": float(min(rates)), "max": float(max(rates)), "runs": len(rates),
+            "sample": f"{runs[0][1]} C5 subdomain SDNet predictions from the initial lattice per run (fp64 "
+                      f"oracle, exact-erf GELU, ~2 s per run); median of {len(rates)} runs",
+            "cpu_model": cpu_model(),
+            "one_thread": {"value": float(statistics.median([r[0] for r in one])), "unit": "predictions/s",
+                           "min": float(min(r[0] for r in one)), "max": float(max(r[0] for r in one)),
+                           "runs": len(one), "sample": f"{one[0][1]} C5 predictions per run"},
+            "oracle_time_to_converge": conv}
 
 
 def preds_per_iter(nx: int, ny: int) -> int:
@@ -284,6 +336,21 @@ def halo_line(rep, prof, world: int) -> dict:
     return out
 
 
+def nccl_summary(path):
+    """Transport lines of rank 0's NCCL INFO log (P2P / NVLS / SHM / NET)."""
+    if not path or not os.path.exists(path):
+        return None
+    kinds = {}
+    nvls = False
+    for line in open(path, errors="replace"):
+        if " via " in line:
+            k = line.split(" via ", 1)[1].split()[0]
+            kinds[k] = kinds.get(k, 0) + 1
+        if "NVLS" in line:
+            nvls = True
+    return {"log": os.path.relpath(path, ROOT), "channels_via": kinds, "nvls_mentioned": nvls}
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
@@ -303,7 +370,14 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
+    nccl_log = None
     if world > 1:
+        # NCCL's INFO log (which transport / NVLS each channel uses) to a file, not
+        # stdout: the evidence that the halo really crossed NVLink is kept
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        nccl_log = os.path.join(ROOT, "gpurun_out", f"nccl_debug_rank{rank}.log")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", nccl_log)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
         obj = [mfp.mfp_nccl_get_unique_id() if rank == 0 else None]
@@ -369,6 +443,24 @@ def main():
     ms = max_over_ranks(ms)
     preds = ppi * T * args.steps
     value = preds / (ms / 1000.0)
+
+    # self-check of the distributed run: rank 0 re-solves the same grid with every
+    # rank emulated on its own GPU (MFP_ALL_RANKS: same plans, kernels and per-rank
+    # batches; device copies instead of NCCL) and compares the final fields
+    parity = None
+    if world > 1:
+        if rank == 0:
+            me = mfp.Mfp(cfg, net, w, rank=mfp.ALL_RANKS, stream=stream)
+            u_e = torch.empty_like(u_dev)
+            me.solve_device(g_dev, T, 0.0, u_e)
+            torch.cuda.synchronize()
+            diff = float((u_e - u_dev).abs().max())
+            parity = {"vs": "MFP_ALL_RANKS emulation of the same grid on rank 0's GPU, same T",
+                      "max_abs_diff": diff, "bit_identical": bool(torch.equal(u_e, u_dev)),
+                      "max_abs_u": float(u_dev.abs().max())}
+            me.close()
+            del u_e
+        barrier()
 
     # e2e through the public host API: H2D of g + D2H of u inside the timed
     # region, from / into pinned host buffers
@@ -530,9 +622,7 @@ def main():
         bio = boundary_io_bench(mfp, torch, peaks)
     cpu = None
     if rank == 0 and world == 1:
-        rate, n, dt, thr = cpu_oracle_rate()
-        cpu = {"value": rate, "unit": "predictions/s", "cores": thr, "kind": "oracle",
-               "sample": f"{n} C5 subdomain SDNet predictions from the initial lattice (fp64 oracle, {dt:.1f} s)"}
+        cpu = cpu_baseline_leg()
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "predictions/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -546,7 +636,8 @@ def main():
                                   "mfp_2049_time_to_mae_0.05_s": 880.0, "mfp_2049_iterations_to_mae_0.05": 3200,
                                   "hardware": "1 x A30, mpi4py (P:179, P:187)",
                                   "derived_predictions_per_s": 58.7e3}, "clocks": clk.summary(),
-                "halo": halo_line(rep, prof, world)}
+                "halo": halo_line(rep, prof, world), "parity_vs_emulation": parity,
+                "nccl_transport": nccl_summary(nccl_log)}
         print(json.dumps(line), flush=True)
     m.close()
     if comm is not None:

@@ -196,8 +196,12 @@ const char* mfp_last_error(const mfp_ctx* ctx);  /* never NULL */
 /* Algorithm 2.  g: HOST, 2(nx+ny) fp32 values walked counter-clockwise
  * from (0,0) (bottom x=0..nx-1, right y=0..ny-1, top x=nx..1, left y=ny..1;
  * reading G6).  g == NULL resumes from the current lattice (no init).
- * max_iters = t >= 1.  tol = eps >= 0; tol == 0 runs exactly max_iters
- * iterations (parity mode).  u_out: HOST (ny+1)*(nx+1) fp32, required on rank 0
+ * max_iters = t >= 1.  tol = eps >= 0.  delta_k (reading G5: max over owned
+ * interior line points of |U_k - U_{k-1}|, allreduce-MAX over ranks) is
+ * evaluated every check_every iterations and after the last one; the solve
+ * stops at the first such k with delta_k <= tol.  tol == 0 runs exactly
+ * max_iters iterations (parity mode; delta is still evaluated and reported in
+ * rep->last_delta).  u_out: HOST (ny+1)*(nx+1) fp32, required on rank 0
  * (and for MFP_ALL_RANKS), ignored elsewhere; may be NULL to skip the final
  * phase.  rep nullable.  Collective over the communicator.
  * Returns OK, NOT_CONVERGED (u written), NONFINITE, CUDA, NCCL, STATE. */
@@ -264,16 +268,18 @@ mfp_status mfp_set_exchange_every(mfp_ctx* ctx, int32_t s);
  *   (cudaMalloc, owned by the context, freed by mfp_destroy) and writes its
  *   64-byte cudaIpcMemHandle_t to handle_out (HOST).  The caller all-gathers the
  *   handles (e.g. torch.distributed over any backend).
- * mfp_p2p_open: handles (HOST) = R handles of 64 B in rank order for one
- *   process per GPU (every rank must have exported), or NULL for MFP_ALL_RANKS
- *   (every rank's region on this device, no IPC).  Switches the context to the
- *   peer transport for the rest of its life; collective (every rank calls it at
- *   the same iteration boundary, no solve in flight).  Before mfp_destroy the
- *   ranks must synchronise (a peer may still read this rank's region).
- * Errors: INVALID (wrong mode, NULL/non-NULL handles, already open, exchange
- *   in flight), CUDA (allocation, IPC). */
+ * mfp_p2p_open: handles (HOST) = n_handles = R handles of 64 B in rank order
+ *   for one process per GPU (every rank must have exported), or NULL with
+ *   n_handles = 0 for MFP_ALL_RANKS (every rank's region on this device, no
+ *   IPC).  Switches the context to the peer transport for the rest of its
+ *   life; collective (every rank calls it at the same iteration boundary, no
+ *   solve in flight).  On any error nothing stays opened (a retry starts
+ *   clean).  mfp_destroy waits (<= 30 s) until every stencil peer has consumed
+ *   this rank's last exchange before it frees the region.
+ * Errors: INVALID (wrong mode, NULL/non-NULL handles, n_handles != R, already
+ *   open, exchange in flight), CUDA (allocation, IPC). */
 mfp_status mfp_p2p_export(mfp_ctx* ctx, void* handle_out);
-mfp_status mfp_p2p_open(mfp_ctx* ctx, const void* handles);
+mfp_status mfp_p2p_open(mfp_ctx* ctx, const void* handles, int32_t n_handles);
 
 /* Run ONE phase (class 0..3 in G2 order) on the current lattice of every local
  * rank, without exchange (debug / sampled parity at full size). */

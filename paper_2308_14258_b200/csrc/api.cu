@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <time.h>
+
 #include "mfp_internal.h"
 
 
@@ -88,7 +90,7 @@ struct mfp_ctx {
   unsigned int* hdelta = nullptr;  // pinned
   unsigned int* iomax = nullptr;   // scatter block maxima (a6 standalone)
   unsigned int* ioout = nullptr;   // [2] reduced update norm + non-finite flag
-  int num_sms = 148;
+  int num_sms = 0;   // set from the device in mfp_init
   int launches = 0;
   bool poisoned = false;
   std::string err;
@@ -103,6 +105,18 @@ struct mfp_ctx {
 namespace {
 
 }  // namespace
+
+int mfp::num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 148;
+  }
+  return cache[dev];
+}
 
 bool mfp::pdl_enabled() {
   static int v = -1;
@@ -139,6 +153,81 @@ mfp_status fail(mfp_ctx* c, mfp_status st, const std::string& msg) {
       return fail(c, MFP_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));    \
     }                                                                                      \
   } while (0)
+
+// Host wait on `stream` that also watches the NCCL communicator: a peer that
+// died or errored never completes its side of a collective, which would leave
+// this rank blocked in cudaStreamSynchronize forever.  Polls the stream and
+// ncclCommGetAsyncError; on an async error or after MFP_NCCL_TIMEOUT_S seconds
+// (default 600) the communicator is aborted and the context poisoned
+// (NCCL errors are sticky; SPEC's watchdog analog).
+double nccl_timeout_s() {
+  static double v = -1.0;
+  if (v < 0.0) {
+    const char* e = getenv("MFP_NCCL_TIMEOUT_S");
+    v = (e && atof(e) > 0.0) ? atof(e) : 600.0;
+  }
+  return v;
+}
+
+mfp_status wait_stream(mfp_ctx* c, cudaStream_t st) {
+  if (!c->comm) {
+    CK(cudaStreamSynchronize(st));
+    return MFP_OK;
+  }
+  struct timespec t0, now;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
+  for (unsigned spin = 0;; spin++) {
+    const cudaError_t q = cudaStreamQuery(st);
+    if (q == cudaSuccess) return MFP_OK;
+    if (q != cudaErrorNotReady) return fail(c, MFP_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(q));
+    ncclResult_t ar = ncclSuccess;
+    ncclCommGetAsyncError(c->comm, &ar);
+    clock_gettime(CLOCK_MONOTONIC, &now);
+    const double el = (double)(now.tv_sec - t0.tv_sec) + 1e-9 * (double)(now.tv_nsec - t0.tv_nsec);
+    if (ar != ncclSuccess && ar != ncclInProgress) {
+      ncclCommAbort(c->comm);
+      c->comm = nullptr;
+      return fail(c, MFP_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(ar));
+    }
+    if (el > nccl_timeout_s()) {
+      ncclCommAbort(c->comm);
+      c->comm = nullptr;
+      return fail(c, MFP_ERR_NCCL, "NCCL watchdog: collective did not complete within MFP_NCCL_TIMEOUT_S");
+    }
+    if (spin > 64) {   // short spin first (sub-ms checks), then back off
+      struct timespec ts = {0, 50000};
+      nanosleep(&ts, nullptr);
+    }
+  }
+}
+
+// Collective agreement over the communicator (no-op without one): every rank
+// contributes {digest, ~digest, flag}; after an allreduce-MAX, a rank sees
+// max(d) == d and max(~d) == ~d only if every rank holds the same digest, and
+// max(flag) != 0 if any rank raised its flag.  Returns MFP_OK / INVALID
+// (digests differ) / `flag_status` (some rank flagged) on EVERY rank alike.
+mfp_status agree(mfp_ctx* c, uint64_t digest, uint64_t flag, mfp_status flag_status, const char* what) {
+  if (!c->comm) return flag ? fail(c, flag_status, what) : MFP_OK;
+  uint64_t h[3] = {digest, ~digest, flag ? 1ull : 0ull};
+  uint64_t* d = nullptr;
+  CK(cudaMalloc((void**)&d, sizeof(h)));
+  struct Free { uint64_t* p; ~Free() { cudaFree(p); } } fr{d};
+  CK(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+  NK(ncclAllReduce(d, d, 3, ncclUint64, ncclMax, c->comm, c->stream));
+  uint64_t r[3];
+  CK(cudaMemcpyAsync(r, d, sizeof(r), cudaMemcpyDeviceToHost, c->stream));
+  if (mfp_status st = wait_stream(c, c->stream)) return st;
+  if (r[2]) return fail(c, flag_status, std::string(what) + " (on at least one rank)");
+  if (r[0] != digest || r[1] != ~digest)
+    return fail(c, MFP_ERR_INVALID, "configuration / weights differ across ranks (collective digest mismatch)");
+  return MFP_OK;
+}
+
+uint64_t fnv1a(uint64_t h, const void* p, size_t n) {
+  const unsigned char* b = (const unsigned char*)p;
+  for (size_t i = 0; i < n; i++) { h ^= b[i]; h *= 1099511628211ull; }
+  return h;
+}
 
 mfp_status check_net(const mfp_sdnet_desc* n, std::string* err) {
   if (!n) { *err = "net is NULL"; return MFP_ERR_INVALID; }
@@ -194,7 +283,7 @@ void carve(mfp_ctx* c, void* base, size_t* total) {
   dn.HfT = cv.take<float>((size_t)kNB * kQF);
   c->gstage = cv.take<float>((size_t)2 * (c->cfg.nx + c->cfg.ny));
   c->delta = cv.take<unsigned int>(4);
-  c->iomax = cv.take<unsigned int>(148 * 8);   // >= scatter_grid(B) for any B
+  c->iomax = cv.take<unsigned int>(kMaxSMs * 8);   // >= scatter_grid(B) for any B
   c->ioout = cv.take<unsigned int>(2);
   const bool need_full = (c->rank == MFP_ALL_RANKS || c->rank == 0);
   c->full = need_full ? cv.take<float>((size_t)(c->cfg.nx + 1) * (c->cfg.ny + 1)) : nullptr;
@@ -434,7 +523,7 @@ mfp_status enqueue_delta(mfp_ctx* c) {
 
 // Host side of the check: wait for the pinned copy and decode it.
 mfp_status read_delta(mfp_ctx* c, float* delta, bool* nonfinite) {
-  CK(cudaStreamSynchronize(c->stream));
+  if (mfp_status st = wait_stream(c, c->stream)) return st;
   uint32_t bits = c->hdelta[0];
   float d;
   memcpy(&d, &bits, 4);
@@ -607,8 +696,10 @@ mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, floa
     // in flight) replays one captured CUDA graph: c x (4 phases + exchange),
     // plus the snapshot / delta / allreduce of the check iteration.
     if (c->use_graphs && it % ce == 0 && t - it >= ce && !c->pending) {
+      // every block ends in a check (delta every c iterations, reading G5),
+      // also in parity mode (tol == 0), where only the stop is disabled
       const int end = it + ce;
-      const bool check = (tol > 0.f) || end == t;
+      const bool check = true;
       mfp_status st = run_block(c, check ? 1 : 0);
       if (st) return st;
       it = end;
@@ -621,7 +712,7 @@ mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, floa
       continue;
     }
     it++;
-    const bool check = (tol > 0.f && it % ce == 0) || it == t;
+    const bool check = (it % ce == 0) || it == t;
     // snapshot for delta (only owned cells are compared; halo cells being
     // unpacked concurrently on the side stream are never read back)
     if (check)
@@ -650,7 +741,7 @@ mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, floa
     if (st) return st;
   }
   CK(cudaEventRecord(e2, c->stream));
-  CK(cudaEventSynchronize(e2));
+  if (mfp_status st = wait_stream(c, c->stream)) return st;
   CK(cudaGetLastError());
   if (rep) {
     memset(rep, 0, sizeof(*rep));
@@ -674,12 +765,39 @@ mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, floa
       for (auto& pp : rs.plan.peers) m += !pp.send_idx.empty();
       msgs = std::max(msgs, m);
     }
-    rep->halo_bytes_sent = bytes * it;
+    // exchanges issued: after every s-th iteration and after the last one
+    // (s | c, so a convergence stop also lands on an exchange): ceil(it / s)
+    const int64_t s_ex = c->exchange_every;
+    rep->halo_bytes_sent = bytes * ((it + s_ex - 1) / s_ex);
     rep->halo_msgs_per_iter = msgs;
     rep->gpu_launches = c->launches;
   }
   if (tol > 0.f && !converged) return MFP_NOT_CONVERGED;
   return MFP_OK;
+}
+
+}  // namespace
+
+namespace {
+// Before a rank frees its IPC-exported region (mfp_destroy), every stencil peer
+// must have finished its last pull from it: peer r stores consumed[r] = e into
+// THIS rank's region after reading exchange e (kernels_p2p.cu).  Poll those
+// flags until they reach this rank's epoch (bounded: 30 s, then give up).
+void p2p_quiesce(mfp_ctx* c) {
+  RankState& rs = c->ranks[0];
+  if (!rs.p2p) return;
+  unsigned long long epoch = 0;
+  if (cudaMemcpy(&epoch, rs.p2p + kP2PEpochOff, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  std::vector<unsigned long long> flags(kP2PConsumed + kP2PMaxRanks);
+  for (int spin = 0; spin < 300000; spin++) {
+    if (cudaMemcpy(flags.data(), rs.p2p, flags.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    bool done = true;
+    for (const auto& pp : rs.plan.peers)
+      if (flags[kP2PConsumed + pp.rank] < epoch) done = false;
+    if (done) return;
+    struct timespec ts = {0, 100000};
+    nanosleep(&ts, nullptr);
+  }
 }
 
 }  // namespace
@@ -737,11 +855,28 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
   if (cfg->subsolver == MFP_SDNET) {
     if (!params) return fail(c, MFP_ERR_INVALID, "params required for the SDNet subsolver");
     if (n_params != param_count_of(net)) return fail(c, MFP_ERR_INVALID, "n_params mismatch (S:387 order)");
+    // (identical weights on every rank are enforced by the collective digest
+    // below, so a non-finite parameter is seen by every rank alike)
     for (size_t i = 0; i < n_params; i++)
       if (!std::isfinite(params[i])) return fail(c, MFP_ERR_NONFINITE, "non-finite parameter");
   }
   if (cfg->precision != MFP_FP32 && cfg->subsolver == MFP_SDNET && !chain_tc_available())
     return fail(c, MFP_ERR_INVALID, "tcgen05 chain not built into this library");
+  // collective validation: every rank of the communicator must
+  // hold the same config, SDNet shape and weights; a rank whose local checks
+  // failed makes every rank fail instead of leaving its peers blocked in the
+  // first collective
+  if (c->comm) {
+    int nr = 0;
+    NK(ncclCommCount(c->comm, &nr));
+    if (nr != c->R) return fail(c, MFP_ERR_INVALID, "communicator size != grid_rows * grid_cols");
+    uint64_t dg = 1469598103934665603ull;
+    dg = fnv1a(dg, cfg, sizeof(*cfg));
+    dg = fnv1a(dg, net, sizeof(*net));
+    dg = fnv1a(dg, &n_params, sizeof(n_params));
+    if (params) dg = fnv1a(dg, params, n_params * sizeof(float));
+    if (mfp_status st2 = agree(c, dg, 0, MFP_OK, "")) return st2;
+  }
   int dev = 0;
   cudaDeviceProp prop;
   CK(cudaGetDevice(&dev));
@@ -823,7 +958,10 @@ void mfp_destroy(mfp_ctx* c) {
     if (g) cudaGraphExecDestroy(g);
   if (c->ev_packed) cudaEventDestroy(c->ev_packed);
   if (c->ev_unpacked) cudaEventDestroy(c->ev_unpacked);
-  if (c->p2p) cudaStreamSynchronize(c->stream);
+  if (c->p2p) {
+    cudaStreamSynchronize(c->stream);
+    if (c->rank != MFP_ALL_RANKS) p2p_quiesce(c);
+  }
   for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
   for (auto& rs : c->ranks) {
     if (rs.p2p) cudaFree(rs.p2p);
@@ -850,8 +988,12 @@ mfp_status mfp_solve(mfp_ctx* c, const float* g, int32_t max_iters, float tol, f
   const size_t ng = 2 * (size_t)(c->cfg.nx + c->cfg.ny);
   const float* gd = nullptr;
   if (g) {
+    bool bad = false;
     for (size_t i = 0; i < ng; i++)
-      if (!std::isfinite(g[i])) return fail(c, MFP_ERR_NONFINITE, "non-finite boundary value");
+      if (!std::isfinite(g[i])) bad = true;
+    // collective: every rank returns NONFINITE together, none is left
+    // waiting in the first exchange of a solve its peers abandoned
+    if (mfp_status st = agree(c, 0, bad ? 1 : 0, MFP_ERR_NONFINITE, "non-finite boundary value (S:121)")) return st;
     CK(cudaMemcpyAsync(c->gstage, g, ng * sizeof(float), cudaMemcpyHostToDevice, c->stream));
     gd = c->gstage;
   }
@@ -998,7 +1140,7 @@ mfp_status mfp_p2p_export(mfp_ctx* c, void* handle_out) {
   return MFP_OK;
 }
 
-mfp_status mfp_p2p_open(mfp_ctx* c, const void* handles) {
+mfp_status mfp_p2p_open(mfp_ctx* c, const void* handles, int32_t n_handles) {
   if (!c) return MFP_ERR_INVALID;
   if (c->poisoned) return MFP_ERR_STATE;
   if (c->R == 1) return fail(c, MFP_ERR_INVALID, "p2p_open: a 1x1 grid has no halo");
@@ -1008,6 +1150,8 @@ mfp_status mfp_p2p_open(mfp_ctx* c, const void* handles) {
   const bool all = (c->rank == MFP_ALL_RANKS);
   if (all != (handles == nullptr))
     return fail(c, MFP_ERR_INVALID, "p2p_open: handles must be NULL exactly for MFP_ALL_RANKS");
+  if (n_handles != (all ? 0 : c->R))
+    return fail(c, MFP_ERR_INVALID, "p2p_open: n_handles must be R (0 for MFP_ALL_RANKS)");
   if (!all && !c->ranks[0].p2p) return fail(c, MFP_ERR_INVALID, "p2p_open: call mfp_p2p_export first");
   mfp_status st = p2p_alloc_own(c);
   if (st) return st;
@@ -1018,17 +1162,30 @@ mfp_status mfp_p2p_open(mfp_ctx* c, const void* handles) {
   if (all) {
     for (auto& rs : c->ranks) base[rs.plan.rank] = rs.p2p;
   } else {
+    // `handles` holds R 64-byte handles in rank order (the caller checks the count)
     base[c->rank] = c->ranks[0].p2p;
     for (const auto& pp : c->ranks[0].plan.peers) {
       if (base[pp.rank]) continue;
       void* p = nullptr;
       cudaIpcMemHandle_t h;
       memcpy(&h, (const char*)handles + (size_t)pp.rank * sizeof(cudaIpcMemHandle_t), sizeof(h));
-      CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {   // roll back: a later retry starts from a clean state
+        for (void* q : c->p2p_opened) cudaIpcCloseMemHandle(q);
+        c->p2p_opened.clear();
+        return fail(c, MFP_ERR_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+      }
       c->p2p_opened.push_back(p);
       base[pp.rank] = (char*)p;
     }
   }
+  auto rollback = [&](mfp_status st, const std::string& msg) {
+    for (auto& rs : c->ranks)
+      if (rs.p2p_tab) { cudaFree(rs.p2p_tab); rs.p2p_tab = nullptr; rs.p2p_np = 0; }
+    for (void* q : c->p2p_opened) cudaIpcCloseMemHandle(q);
+    c->p2p_opened.clear();
+    return fail(c, st, msg);
+  };
   for (auto& rs : c->ranks) {
     std::vector<P2PPeer> tab;
     for (size_t i = 0; i < rs.plan.peers.size(); i++) {
@@ -1040,7 +1197,7 @@ mfp_status mfp_p2p_open(mfp_ctx* c, const void* handles) {
         nq += (int64_t)x.send_idx.size();
       }
       if (len != (int64_t)rs.plan.peers[i].recv_idx.size())
-        return fail(c, MFP_ERR_INVALID, "p2p_open: send/recv segment mismatch");
+        return rollback(MFP_ERR_INVALID, "p2p_open: send/recv segment mismatch");
       P2PPeer e{};
       e.rank = q;
       e.flags = (unsigned long long*)base[q];
@@ -1051,8 +1208,10 @@ mfp_status mfp_p2p_open(mfp_ctx* c, const void* handles) {
       tab.push_back(e);
     }
     rs.p2p_np = (int)tab.size();
-    CK(cudaMalloc((void**)&rs.p2p_tab, std::max<size_t>(1, tab.size()) * sizeof(P2PPeer)));
-    if (!tab.empty()) CK(cudaMemcpy(rs.p2p_tab, tab.data(), tab.size() * sizeof(P2PPeer), cudaMemcpyHostToDevice));
+    cudaError_t e = cudaMalloc((void**)&rs.p2p_tab, std::max<size_t>(1, tab.size()) * sizeof(P2PPeer));
+    if (e == cudaSuccess && !tab.empty())
+      e = cudaMemcpy(rs.p2p_tab, tab.data(), tab.size() * sizeof(P2PPeer), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return rollback(MFP_ERR_CUDA, std::string("p2p_open: ") + cudaGetErrorString(e));
   }
   for (auto& g : c->gexec)
     if (g) { cudaGraphExecDestroy(g); g = nullptr; }

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(1024) k_reduce_max(const unsigned int* __restr
 // Grid: a multiple of the SM count (8 warps per block, 8 blocks per SM).
 static int io_blocks(int64_t units, int per_block) {
   int64_t b = (units + per_block - 1) / per_block;
-  const int64_t cap = 148 * 8;
+  const int64_t cap = (int64_t)(num_sms() < kMaxSMs ? num_sms() : kMaxSMs) * 8;
   if (b > cap) b = cap;
   return b < 1 ? 1 : (int)b;
 }

@@ -243,12 +243,13 @@ void launch_embed_tc(const float* lat, const LatticeGeom& L, const uint32_t* anc
                      int64_t B, const DevNet& net, float* z, cudaStream_t s) {
   if (B <= 0) return;
   // rows per CTA round: the smallest multiple of 32 that covers B over the SMs
-  int64_t per = (B + 147) / 148;
+  const int sms = num_sms();
+  int64_t per = (B + sms - 1) / sms;
   int rows = (int)((per + 31) / 32) * 32;
   if (rows > emb::kRowsE) rows = emb::kRowsE;
   if (rows < 32) rows = 32;
   int64_t blocks = (B + rows - 1) / rows;
-  if (blocks > 148) blocks = 148;
+  if (blocks > sms) blocks = sms;
   const size_t sm = emb::smem_bytes();
   if (net.gelu_tanh)
     launch_pdl(emb::k_embed_tc<1>, (int)blocks, emb::kThreadsE, sm, s, lat, L, anchors, gb, B, rows, net, z);

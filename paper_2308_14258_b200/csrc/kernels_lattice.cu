@@ -36,7 +36,7 @@ void launch_init_lattice(float* lat, const LatticeGeom& L, int nx, int ny, const
   cudaMemsetAsync(lat, 0, sizeof(float) * L.cells, s);
   int n = 2 * (nx + ny);
   int blocks = (n + 255) / 256;
-  if (blocks > 148 * 4) blocks = 148 * 4;
+  if (blocks > num_sms() * 4) blocks = num_sms() * 4;
   k_init_boundary<<<blocks, 256, 0, s>>>(lat, L, nx, ny, g);
 }
 
@@ -122,7 +122,7 @@ void launch_exact_phase(float* lat, const LatticeGeom& L, const uint32_t* anchor
   if (B <= 0) return;
   const int per_block = kExactWarps * kExactSub;
   int64_t blocks = (B + per_block - 1) / per_block;
-  if (blocks > 148) blocks = 148;
+  if (blocks > num_sms()) blocks = num_sms();
   const size_t smem = sizeof(float) * ((size_t)kNB * 64 + (size_t)kExactWarps * kExactSub * kNB);
   k_exact_phase<<<(int)blocks, kExactWarps * 32, smem, s>>>(lat, L, anchors, B, HcT);
 }
@@ -178,7 +178,7 @@ void launch_exact_general(const float* lat, const LatticeGeom& L, const uint32_t
                           cudaStream_t s) {
   if (B <= 0) return;
   int64_t blocks = (B + kExactGroup - 1) / kExactGroup;
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks > num_sms() * 8) blocks = num_sms() * 8;
   k_exact_general<<<(int)blocks, 256, 0, s>>>(lat, L, lat_anchors, gb, B, q, HT, sink);
 }
 
@@ -217,7 +217,7 @@ void launch_delta(const float* lat, const float* snap, const int64_t* segs, int 
                   unsigned int* out, cudaStream_t s) {
   // out is zeroed by the caller once per check (max accumulates over local ranks)
   if (nseg <= 0) return;
-  int blocks = nseg < 148 * 4 ? nseg : 148 * 4;
+  int blocks = nseg < num_sms() * 4 ? nseg : num_sms() * 4;
   k_delta<<<blocks, 256, 0, s>>>(lat, snap, segs, nseg, out);
 }
 
@@ -235,7 +235,7 @@ __global__ void k_unpack(float* __restrict__ lat, const int32_t* __restrict__ id
 
 static int grid_for(int64_t n) {
   int64_t b = (n + 255) / 256;
-  if (b > 148 * 4) b = 148 * 4;
+  if (b > num_sms() * 4) b = num_sms() * 4;
   return b < 1 ? 1 : (int)b;
 }
 
@@ -266,7 +266,7 @@ __global__ void k_final_lines(const float* __restrict__ lat, LatticeGeom L, int 
 
 void launch_final_lines(const float* lat, const LatticeGeom& L, int X0, int Y0, int bw, int bh,
                         float* field, int ld, cudaStream_t s) {
-  k_final_lines<<<148 * 4, 256, 0, s>>>(lat, L, X0, Y0, bw, bh, field, ld);
+  k_final_lines<<<num_sms() * 4, 256, 0, s>>>(lat, L, X0, Y0, bw, bh, field, ld);
 }
 
 }  // namespace mfp

@@ -98,7 +98,11 @@ __global__ void k_pull_p2p(float* __restrict__ lat, const int32_t* __restrict__ 
 
 static int grid_p2p(int64_t n) {
   int64_t b = (n + 255) / 256;
-  if (b > 148) b = 148;  // one block per SM at most: every block spins on the flags
+  // every pull block polls the <= 8 peer flags (one thread per peer, nanosleep
+  // back-off) before copying; capping the grid at the SM count bounds that
+  // spinning.  Blocks may still co-reside on an SM (nothing reserves one SM per
+  // block) and share it with the main stream's persistent chain kernel.
+  if (b > num_sms()) b = num_sms();
   return b < 1 ? 1 : (int)b;
 }
 

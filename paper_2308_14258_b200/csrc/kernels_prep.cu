@@ -98,7 +98,7 @@ __global__ void k_prep(PrepArgs a) {
   }
 }
 
-void launch_prep(const PrepArgs& a, cudaStream_t s) { k_prep<<<148 * 2, 256, 0, s>>>(a); }
+void launch_prep(const PrepArgs& a, cudaStream_t s) { k_prep<<<num_sms() * 2, 256, 0, s>>>(a); }
 
 // Harmonic-extension matrix H^T [k][q] for the 5-point Dirichlet problem on the
 // (m+1)^2 patch: separation of variables with the DST-I basis,
@@ -139,7 +139,7 @@ __global__ void k_harmonic(int q, int ld, float* __restrict__ HT) {
 }
 
 void launch_harmonic(int q, float* HT, cudaStream_t s) {
-  k_harmonic<<<148, 256, 0, s>>>(q, q == kQC ? 64 : q, HT);
+  k_harmonic<<<num_sms(), 256, 0, s>>>(q, q == kQC ? 64 : q, HT);
 }
 
 }  // namespace mfp

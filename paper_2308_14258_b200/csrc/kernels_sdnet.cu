@@ -111,7 +111,7 @@ void launch_gather_embed(const float* lat, const LatticeGeom& L, const uint32_t*
                          const float* gb, int64_t B, const DevNet& net, float* z, cudaStream_t s) {
   if (B <= 0) return;
   int64_t blocks = (B + kEmbSub - 1) / kEmbSub;
-  if (blocks > 2 * 148) blocks = 2 * 148;   // two resident blocks per SM
+  if (blocks > 2 * num_sms()) blocks = 2 * num_sms();   // two resident blocks per SM
   if (net.gelu_tanh)
     k_gather_embed<1><<<(int)blocks, kEmbWarps * 32, kEmbSmem, s>>>(lat, L, anchors, gb, B, net, z);
   else
@@ -216,7 +216,7 @@ void launch_chain_fp32(const float* z, int64_t B, int q, const DevNet& net, cons
   const size_t sm = simt_smem(net.n_hidden);
   const int64_t rows = B * q;
   int64_t tiles = (rows + kSimtRows - 1) / kSimtRows;
-  int blocks = (int)(tiles < 148 ? tiles : 148);
+  int blocks = (int)(tiles < num_sms() ? tiles : num_sms());
   const float* QT = q == kQC ? net.QTc : net.QTf;
   const int qpad = q == kQC ? 64 : kQF;
   k_chain_fp32<<<blocks, 256, sm, s>>>(z, rows, q, qpad, QT, net, sink);

@@ -28,6 +28,7 @@
 //     ahead; the last layer's epilogue stays fp32 (GELU + head dot
 //     y = wo.h + bo; the head cancels strongly) followed by the
 //     fused scatter onto the lattice (a6) or the final-phase field (a9).
+#include <cstdlib>
 #include <type_traits>
 
 #include <cuda_bf16.h>
@@ -545,7 +546,11 @@ void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const 
   const int64_t rows = B * q;
   const size_t sm = tc2::smem_bytes2(net.n_hidden);
   const int64_t ptiles = (rows + 2 * tc::kRows - 1) / (2 * tc::kRows);
-  const int64_t pairs = num_sms / 2;
+  int64_t pairs = num_sms / 2;
+  // MFP_MAX_PAIRS=n (sanitizer runs only): cap the persistent grid so a small
+  // batch still cycles every tile slot through many rounds
+  static const int max_pairs = getenv("MFP_MAX_PAIRS") ? atoi(getenv("MFP_MAX_PAIRS")) : 0;
+  if (max_pairs > 0 && pairs > max_pairs) pairs = max_pairs;
   const int grid = 2 * (int)(ptiles < pairs ? ptiles : pairs);
 #define MFP_TC2(G, F) launch_pdl(tc2::k_chain_tc2<G, F>, grid, tc2::kThreads2, sm, s, z, rows, q, net, sink)
   if (net.f16) {

@@ -69,6 +69,12 @@ struct GlobalPlan {
   std::vector<RankPlan> ranks;
 };
 
+// SM count of the current device (cudaDevAttrMultiProcessorCount, cached per
+// device): every grid is sized from it, never from a literal.  kMaxSMs bounds
+// the per-SM scratch carved from the workspace before a device is known.
+int num_sms();
+constexpr int kMaxSMs = 256;
+
 // Validates cfg and builds the plan for one rank (or every rank when rank < 0).
 mfp_status build_plan(const mfp_config* cfg, int rank, GlobalPlan* out, std::string* err);
 mfp_status validate_config(const mfp_config* cfg, std::string* err);

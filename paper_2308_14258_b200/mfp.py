@@ -103,7 +103,7 @@ _SIGS = {
     "mfp_scatter_phase": [_vp, _i32, _i32, _vp, _i64, _P(ctypes.c_float)],
     "mfp_set_exchange_every": [_vp, _i32],
     "mfp_p2p_export": [_vp, _vp],
-    "mfp_p2p_open": [_vp, _vp],
+    "mfp_p2p_open": [_vp, _vp, _i32],
     "mfp_nccl_get_unique_id": [_vp],
     "mfp_nccl_comm_init": [_i32, _vp, _i32, _P(_vp)],
     "mfp_nccl_comm_destroy": [_vp],
@@ -231,8 +231,12 @@ def mfp_p2p_export(ctx) -> bytes:
 def mfp_p2p_open(ctx, handles=None) -> None:
     """NEXT-2: switch to the peer-memory halo transport.  handles: the R
     exported handles in rank order (one process per GPU), None for ALL_RANKS."""
+    if handles is not None:
+        handles = list(handles)
+        if any(len(h) != 64 for h in handles):
+            raise MfpError(1, "p2p_open: every handle must be 64 bytes")
     buf = None if handles is None else ctypes.create_string_buffer(b"".join(handles), 64 * len(handles))
-    _check(_lib.mfp_p2p_open(ctx, buf), ctx)
+    _check(_lib.mfp_p2p_open(ctx, buf, 0 if handles is None else len(handles)), ctx)
 
 
 def mfp_step_phase(ctx, phase: int) -> None:

@@ -98,6 +98,10 @@ def test_p2p_errors(lib):
     with pytest.raises(lib.MfpError) as e:          # export is for one-process-per-GPU contexts
         lib.mfp_p2p_export(m.ctx)
     assert e.value.status == 1
+    with pytest.raises(lib.MfpError) as e:          # a short handle list (R = 4) is rejected in C
+        _ = lib._lib.mfp_p2p_open(m.ctx, None, 3)
+        lib._check(_, m.ctx)
+    assert e.value.status == 1
     lib.mfp_p2p_open(m.ctx)
     with pytest.raises(lib.MfpError) as e:          # once per context
         lib.mfp_p2p_open(m.ctx)

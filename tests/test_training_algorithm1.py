@@ -111,3 +111,16 @@ def test_data_parallel_step_equals_single_process():
         p.join(60)
         assert p.exitcode == 0
     assert np.max(np.abs(got - ref)) < 1e-12
+
+
+def test_lr_schedule_and_worker_scaling():
+    """§5.2 via SPEC's lr_at / scale_for_workers examples."""
+    from training.algorithm1 import lr_at, scale_for_workers
+    assert lr_at(1e-3, 0.01, 1.0, 0, 1000) == 0.0                 # ramp start
+    assert abs(lr_at(1e-3, 0.01, 1.0, 10, 1000) - 1e-3) < 1e-15   # ramp end (ceil(0.01 * 1000) = 10)
+    assert abs(lr_at(1e-3, 0.01, 1.0, 505, 1000) - 5e-4) < 1e-15  # halfway through the decay span
+    assert lr_at(1e-3, 0.01, 1.0, 1000, 1000) == 0.0               # 0 at the final iteration
+    assert abs(lr_at(1e-3, 0.01, 1.0, 9, 1000) - 9e-4) < 1e-15
+    assert abs(scale_for_workers(1e-3, 1e-3, 4)[0] - 2e-3) < 1e-15  # p = 4: sqrt rule
+    assert abs(scale_for_workers(1e-3, 1e-3, 16)[1] - 0.016) < 1e-15  # p = 16: linear warmup rule
+    assert scale_for_workers(1e-3, 0.1, 16)[1] == 0.5

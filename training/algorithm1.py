@@ -222,6 +222,30 @@ class Lamb(torch.optim.Optimizer):
 
 
 # ------------------------------------------------------------------ Algorithm 1
+# ---- learning-rate rules of §5.2: warmup + polynomial decay, and the
+# data-parallel scaling of max_lr (sqrt of the batch growth) and of the warmup
+# fraction (linear in the batch growth); SPEC lr_at / scale_for_workers.
+def lr_at(max_lr: float, warmup_frac: float, decay: float, it: int, total: int) -> float:
+    """Linear ramp 0 -> max_lr over ceil(warmup_frac * total) iterations, then
+    max_lr * (1 - progress)^decay down to 0 at it == total ("0.1% of
+    iterations for learning rate warmup ... polynomial learning rate decay with
+    the exponent set to one")."""
+    import math
+    w = int(math.ceil(warmup_frac * total))
+    if w > 0 and it < w:
+        return max_lr * it / w
+    span = max(total - w, 1)
+    prog = min(max((it - w) / span, 0.0), 1.0)
+    return max_lr * (1.0 - prog) ** decay
+
+
+def scale_for_workers(max_lr: float, warmup_frac: float, p: int) -> tuple[float, float]:
+    """"(a) We scale the maximum learning rate by the square root of the
+    increase in batch size. (b) The fraction of iterations used for learning rate
+    warmup is scaled linearly" (capped at 1/2)."""
+    return max_lr * p ** 0.5, min(warmup_frac * p, 0.5)
+
+
 def train_step(net: SDNet, opt: torch.optim.Optimizer, b: Batch, pde_weight: float = 1.0, world: int = 1):
     """One iteration of Algorithm 1; returns (data loss, pde loss) of this rank."""
     opt.zero_grad(set_to_none=False)
@@ -251,7 +275,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--batch", type=int, default=256, help="boundaries per rank per step")
-    ap.add_argument("--lr", type=float, default=2e-3)
+    ap.add_argument("--lr", type=float, default=1e-3, help="max_lr at one rank (P:75); scaled by sqrt(world)")
+    ap.add_argument("--warmup-frac", type=float, default=1e-3, help="warmup fraction at one rank (P:75)")
+    ap.add_argument("--decay", type=float, default=1.0, help="polynomial decay exponent (P:75)")
     ap.add_argument("--pde-weight", type=float, default=1e-3)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--init", default=None)
@@ -268,7 +294,10 @@ def main():
     net = SDNet().to(dev)
     if a.init:
         net.load_flat(np.load(a.init))
-    opt = Lamb(net.parameters(), lr=a.lr)
+    # each rank keeps its per-rank batch, so the global batch grows with world:
+    # the §5.2 scaling rules set the schedule for that global batch
+    max_lr, warmup = scale_for_workers(a.lr, a.warmup_frac, world)
+    opt = Lamb(net.parameters(), lr=max_lr)
     prob = Problem(dev, torch.float32)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 * a.seed + rank)           # each rank draws its own shard
@@ -276,6 +305,8 @@ def main():
     if dev.type == "cuda":
         torch.cuda.synchronize()
     for step in range(a.steps):
+        for grp in opt.param_groups:
+            grp["lr"] = lr_at(max_lr, warmup, a.decay, step, a.steps)
         ld, lp = train_step(net, opt, prob.batch(a.batch, gen), a.pde_weight, world)
         if rank == 0 and (step % 100 == 0 or step == a.steps - 1):
             log.append((step, ld, lp))
