@@ -3,10 +3,17 @@
 //
 // PAPER.md P:239 (1-D convolutions over g give the boundary embedding) and
 // Eq. 5 P:270 (z = g W1^T is computed once per boundary and broadcast over
-// the queries).  Per round a CTA embeds 128 subdomains:
-//   * 16 warps x 8 subdomains: gather the 128 perimeter values (G1 order;
-//     lane l owns positions 4l..4l+3), conv1 1->8 / conv2 8->1 (k = 5,
-//     circular) + GELU in registers with warp-shuffle windows;
+// the queries).  Per round a CTA embeds up to 128 subdomains:
+//   * a producer warp stages every subdomain's four perimeter edges (a1) into
+//     shared memory with TMA bulk copies (cp.async.bulk, one 128/144-byte edge
+//     segment per lane, completion counted in bytes on the consuming warp's
+//     mbarrier); it issues a warp's next round as soon as that warp has pulled
+//     the current one into registers, so the gathers overlap the conv stack,
+//     the MMAs and the z stores.  The W1 images arrive the same way before the
+//     PDL wait (weights do not depend on the previous kernel);
+//   * 16 warps x 8 subdomains: the 128 perimeter values (G1 order; lane l owns
+//     positions 4l..4l+3) from the staging slots, conv1 1->8 / conv2 8->1
+//     (k = 5, circular) + GELU in registers with warp-shuffle windows;
 //   * the embedding e (fp32) is split e = e_hi + e_lo into two bf16 SWIZZLE_128B
 //     A operands; W1 = W1_hi + W1_lo is resident as two bf16 B operands; one
 //     elected thread issues the three products hi.hi + hi.lo + lo.hi
@@ -29,7 +36,7 @@ constexpr int kThreadsE = 512;           // 16 warps
 constexpr int kImg = kRowsE * kNB * 2;   // 32 KB bf16 image
 constexpr int kPerWarp = kRowsE / 16;
 
-size_t smem_bytes() { return 4 * (size_t)kImg + 4 * (96 + kD) + 64; }
+size_t smem_bytes() { return 4 * (size_t)kImg + (size_t)kRowsE * 576 + 4 * (96 + kD) + 8 * 18 + 16; }
 
 // The conv stack of TWO subdomains at once: every value is an fp32 pair
 // (subdomain A, subdomain B) at the same perimeter position, so each weight is
@@ -90,6 +97,15 @@ __device__ __forceinline__ void conv_stack2(const f2 (&g4)[4], int lane, const D
   for (int p = 0; p < 4; p++) e[p] = emb_act2<GELU>(acc2[p]);
 }
 
+// Staged perimeter of one subdomain (TMA bulk copies of the four edge
+// segments): bottom [lx, lx+32) at 0, right [ly, ly+32) at 144, top
+// [lx, lx+36) at 288 and left [ly, ly+36) at 432 (floats; the reversed edges
+// need points lx+1..lx+32, and a bulk copy's source must be 16-byte aligned, so
+// their window starts at the 64-byte aligned corner).  A gb batch row (512 B)
+// is staged contiguously at 0.
+constexpr int kSlotB = 576;
+constexpr uint32_t kEdgeB = 4 * kM, kEdgeRB = 4 * (kM + 4);
+
 template <int GELU>
 __global__ void __launch_bounds__(kThreadsE, 1)
 k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ anchors,
@@ -99,24 +115,23 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
   uint8_t* sWlo = sWhi + kImg;
   uint8_t* sAhi = sWlo + kImg;
   uint8_t* sAlo = sAhi + kImg;
-  float* sCw = reinterpret_cast<float*>(sAlo + kImg);   // c1w[40] c1b[8] c2w[40] c2b[1]
+  uint8_t* sStage = sAlo + kImg;                         // [128][kSlotB]
+  float* sCw = reinterpret_cast<float*>(sStage + kRowsE * kSlotB);   // c1w[40] c1b[8] c2w[40] c2b[1]
   float* sB1 = sCw + 96;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sB1 + kD);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sB1 + kD);   // [0] MMA done, [1] W1 landed,
+  uint64_t* full = bar + 2;                                 // [2..17] warp's perimeters landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full + 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(net.W1img);
-    uint4* dst = reinterpret_cast<uint4*>(sWhi);
-    for (int i = threadIdx.x; i < 2 * kImg / 16; i += kThreadsE) dst[i] = __ldg(src + i);
-    if (threadIdx.x < kD) sB1[threadIdx.x] = __ldg(net.b1 + threadIdx.x);
-    if (threadIdx.x < 40) sCw[threadIdx.x] = __ldg(net.conv1_w + threadIdx.x);
-    if (threadIdx.x < 8) sCw[40 + threadIdx.x] = __ldg(net.conv1_b + threadIdx.x);
-    if (threadIdx.x < 40) sCw[48 + threadIdx.x] = __ldg(net.conv2_w + threadIdx.x);
-    if (threadIdx.x == 0) sCw[88] = __ldg(net.conv2_b);
-  }
+  if (threadIdx.x < kD) sB1[threadIdx.x] = __ldg(net.b1 + threadIdx.x);
+  if (threadIdx.x < 40) sCw[threadIdx.x] = __ldg(net.conv1_w + threadIdx.x);
+  if (threadIdx.x < 8) sCw[40 + threadIdx.x] = __ldg(net.conv1_b + threadIdx.x);
+  if (threadIdx.x < 40) sCw[48 + threadIdx.x] = __ldg(net.conv2_w + threadIdx.x);
+  if (threadIdx.x == 0) sCw[88] = __ldg(net.conv2_b);
   if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
   if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    for (int w = 0; w < 16; w++) mbar_init(&full[w], 1);   // lane 0's arrive.expect_tx + the copies' bytes
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -130,93 +145,152 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // W1 = W1_hi + W1_lo images (weights: no dependence on the previous grid)
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&bar[1], 2u * kImg);
+    for (int i = 0; i < 4; i++)
+      bulk_g2s(smem_u32(sWhi) + i * (kImg / 2), reinterpret_cast<const uint8_t*>(net.W1img) + i * (kImg / 2),
+               kImg / 2, &bar[1]);
+  }
   pdl_launch_dependents();
   pdl_wait();      // the lattice (previous phase's scatter) and z's readers complete from here on
-  const int i0 = 4 * lane;
-  const uint32_t a_hi = smem_u32(sAhi), a_lo = smem_u32(sAlo);
-  uint32_t phase = 0u;
   // `rows` (32, 64, 96 or 128) subdomains per round: small batches (a rank's share
   // on 8 GPUs) spread over more CTAs with fewer subdomains per warp, so the
   // serial conv work per warp shrinks with the batch; rows >= `rows` of the
   // 128-row MMA are don't-care (rows are independent in the MMA, never stored)
   const int pw = rows >> 4;   // subdomains per warp (even)
-  for (int64_t base = (int64_t)blockIdx.x * rows; base < B; base += (int64_t)gridDim.x * rows) {
-    // ---- gather + conv stack, pw subdomains per warp (gathers issued up front)
-    float4 gpre[kPerWarp];
-#pragma unroll
-    for (int j = 0; j < kPerWarp; j++) {
-      if (j >= pw) break;
+  const int64_t step = (int64_t)gridDim.x * rows;
+
+  // ---- a1: TMA bulk copies of this warp's pw perimeters (four edge segments
+  // each, one copy per lane) into its staging slots, completing on full[warp];
+  // a warp issues round r + 1 as soon as it has pulled round r into registers,
+  // so the gathers overlap the conv stack, the MMAs and the z stores
+  auto stage = [&](int64_t base) {
+    if (lane == 0) mbar_arrive_expect_tx(&full[warp], (uint32_t)pw * (gb ? 4u * kNB : 2u * (kEdgeB + kEdgeRB)));
+    __syncwarp();
+    const int j = lane >> 2, e = lane & 3;
+    if (j < pw) {
       int64_t s = base + warp * pw + j;
       if (s > B - 1) s = B - 1;
-      gpre[j] = gb ? __ldg(reinterpret_cast<const float4*>(gb + s * kNB + i0)) : gather4(lat, L, __ldg(anchors + s), lane);
-    }
-#pragma unroll
-    for (int jp = 0; jp < kPerWarp; jp += 2) {
-      if (jp >= pw) break;
-      const f2 g4[4] = {f2_make(gpre[jp].x, gpre[jp + 1].x), f2_make(gpre[jp].y, gpre[jp + 1].y),
-                        f2_make(gpre[jp].z, gpre[jp + 1].z), f2_make(gpre[jp].w, gpre[jp + 1].w)};
-      f2 e2[4];
-      conv_stack2<GELU>(g4, lane, net, e2);
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-      const int row = warp * pw + jp + h;
-      float e[4];
-#pragma unroll
-      for (int p = 0; p < 4; p++) {
-        float lo, hi;
-        f2_split(e2[p], lo, hi);
-        e[p] = h ? hi : lo;
-      }
-      // e = e_hi + e_lo, both bf16 (round to nearest)
-      uint32_t h01, h23, l01, l23;
-      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h01) : "f"(e[1]), "f"(e[0]));
-      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h23) : "f"(e[3]), "f"(e[2]));
-      const float r0 = e[0] - __uint_as_float(h01 << 16), r1 = e[1] - __uint_as_float(h01 & 0xffff0000u);
-      const float r2 = e[2] - __uint_as_float(h23 << 16), r3 = e[3] - __uint_as_float(h23 & 0xffff0000u);
-      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l01) : "f"(r1), "f"(r0));
-      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l23) : "f"(r3), "f"(r2));
-      const uint32_t off = sw128_off(row, i0) + (uint32_t)((i0 & 7) * 2);
-      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a_hi + off), "r"(h01), "r"(h23) : "memory");
-      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a_lo + off), "r"(l01), "r"(l23) : "memory");
+      const uint32_t slot = smem_u32(sStage) + (uint32_t)((warp * pw + j) * kSlotB);
+      if (gb) {
+        if (e == 0) bulk_g2s(slot, gb + s * kNB, 4u * kNB, &full[warp]);
+      } else {
+        int a, b;
+        unpack_anchor(__ldg(anchors + s), a, b);
+        const int lx = kH * a, ly = kH * b;
+        const float* src = e == 0 ? lat + (int64_t)b * L.strideH + lx
+                         : e == 1 ? lat + L.offV + (int64_t)(a + 2) * L.strideV + ly
+                         : e == 2 ? lat + (int64_t)(b + 2) * L.strideH + lx
+                                  : lat + L.offV + (int64_t)a * L.strideV + ly;
+        bulk_g2s(slot + (uint32_t)e * 144u, src, e < 2 ? kEdgeB : kEdgeRB, &full[warp]);
       }
     }
-    fence_proxy_async();
-    __syncthreads();
-    // ---- z = e W1^T on the tensor core: hi.hi + hi.lo + lo.hi
-    if (threadIdx.x == 0) {
+  };
+  {
+    const int i0 = 4 * lane;
+    const uint32_t a_hi = smem_u32(sAhi), a_lo = smem_u32(sAlo);
+    const int edge = lane >> 3, t0 = 4 * (lane & 7);
+    // byte offset of this lane's first value inside a staging slot
+    const uint32_t st_lane = smem_u32(sStage) + 4u * (uint32_t)(gb ? i0 : edge < 2 ? 36 * edge + t0 : 36 * edge + kM - t0);
+    uint32_t phase = 0u, pf = 0u;
+    bool w1_ready = false;
+    if ((int64_t)blockIdx.x * rows < B) stage((int64_t)blockIdx.x * rows);
+    for (int64_t base = (int64_t)blockIdx.x * rows; base < B; base += step) {
+      // ---- this warp's pw perimeters from the staging slots (G1 order; lane l
+      // owns positions 4l..4l+3)
+      mbar_wait(&full[warp], pf);
+      pf ^= 1u;
+      // smem reads right before use (2 subdomains live at a time), 32-bit
+      // shared addresses: lane offset within a slot fixed per lane
+      auto perim4 = [&](int j) -> float4 {
+        const uint32_t sl = st_lane + (uint32_t)((warp * pw + j) * kSlotB);
+        float4 v;
+        if (gb || edge < 2) {
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(sl));
+        } else {
+          asm volatile("ld.shared.f32 %0, [%4];\n\tld.shared.f32 %1, [%4+-4];\n\tld.shared.f32 %2, [%4+-8];\n\tld.shared.f32 %3, [%4+-12];"
+                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(sl));
+        }
+        return v;
+      };
+#pragma unroll
+      for (int jp = 0; jp < kPerWarp; jp += 2) {
+        if (jp >= pw) break;
+        const float4 ga = perim4(jp), gb4 = perim4(jp + 1);
+        const f2 g4[4] = {f2_make(ga.x, gb4.x), f2_make(ga.y, gb4.y), f2_make(ga.z, gb4.z), f2_make(ga.w, gb4.w)};
+        f2 e2[4];
+        conv_stack2<GELU>(g4, lane, net, e2);
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int row = warp * pw + jp + h;
+          float e[4];
+#pragma unroll
+          for (int p = 0; p < 4; p++) {
+            float lo, hi;
+            f2_split(e2[p], lo, hi);
+            e[p] = h ? hi : lo;
+          }
+          // e = e_hi + e_lo, both bf16 (round to nearest)
+          uint32_t h01, h23, l01, l23;
+          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h01) : "f"(e[1]), "f"(e[0]));
+          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h23) : "f"(e[3]), "f"(e[2]));
+          const float r0 = e[0] - __uint_as_float(h01 << 16), r1 = e[1] - __uint_as_float(h01 & 0xffff0000u);
+          const float r2 = e[2] - __uint_as_float(h23 << 16), r3 = e[3] - __uint_as_float(h23 & 0xffff0000u);
+          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l01) : "f"(r1), "f"(r0));
+          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l23) : "f"(r3), "f"(r2));
+          const uint32_t off = sw128_off(row, i0) + (uint32_t)((i0 & 7) * 2);
+          asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a_hi + off), "r"(h01), "r"(h23) : "memory");
+          asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a_lo + off), "r"(l01), "r"(l23) : "memory");
+        }
+      }
+      // next round's perimeters: the slots' generic-proxy reads (long since
+      // consumed) are ordered before the async-proxy (TMA) writes into them
+      fence_proxy_async();
+      __syncwarp();
+      if (base + step < B) stage(base + step);
+      __syncthreads();
+      // ---- z = e W1^T on the tensor core: hi.hi + hi.lo + lo.hi
+      if (threadIdx.x == 0) {
+        if (!w1_ready) {
+          mbar_wait(&bar[1], 0u);
+          w1_ready = true;
+        }
+        tc_fence_after();
+        const uint32_t w_hi = smem_u32(sWhi), w_lo = smem_u32(sWlo);
+#pragma unroll
+        for (int k = 0; k < kNB / 16; k++) {
+          const uint32_t off = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
+          mma_f16<0>(tmem, sw128_desc(a_hi + off), sw128_desc(w_hi + off), k > 0 ? 1u : 0u);
+          mma_f16<0>(tmem, sw128_desc(a_hi + off), sw128_desc(w_lo + off), 1u);
+          mma_f16<0>(tmem, sw128_desc(a_lo + off), sw128_desc(w_hi + off), 1u);
+        }
+        mma_commit(&bar[0]);
+      }
+      mbar_wait(&bar[0], phase);
+      phase ^= 1u;
       tc_fence_after();
-      const uint32_t w_hi = smem_u32(sWhi), w_lo = smem_u32(sWlo);
+      // ---- drain: warp w reads lanes 32 (w % 4).., columns 32 (w / 4)..
+      {
+        const int quad = warp & 3, cb = warp >> 2;
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(cb * 32), r);
+        tmem_wait_ld();
+        const int64_t s = base + quad * 32 + lane;
+        if (quad * 32 + lane < rows && s < B) {
+          float4* dst = reinterpret_cast<float4*>(z + s * kD + cb * 32);
+          const float* bb = sB1 + cb * 32;
 #pragma unroll
-      for (int k = 0; k < kNB / 16; k++) {
-        const uint32_t off = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
-        mma_f16<0>(tmem, sw128_desc(a_hi + off), sw128_desc(w_hi + off), k > 0 ? 1u : 0u);
-        mma_f16<0>(tmem, sw128_desc(a_hi + off), sw128_desc(w_lo + off), 1u);
-        mma_f16<0>(tmem, sw128_desc(a_lo + off), sw128_desc(w_hi + off), 1u);
+          for (int v = 0; v < 8; v++)
+            dst[v] = make_float4(__uint_as_float(r[4 * v]) + bb[4 * v], __uint_as_float(r[4 * v + 1]) + bb[4 * v + 1],
+                                 __uint_as_float(r[4 * v + 2]) + bb[4 * v + 2], __uint_as_float(r[4 * v + 3]) + bb[4 * v + 3]);
+        }
       }
-      mma_commit(bar);
+      tc_fence_before();
+      __syncthreads();   // A operands and the accumulator are reused next round
     }
-    mbar_wait(bar, phase);
-    phase ^= 1u;
-    tc_fence_after();
-    // ---- drain: warp w reads lanes 32 (w % 4).., columns 32 (w / 4)..
-    {
-      const int quad = warp & 3, cb = warp >> 2;
-      uint32_t r[32];
-      tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(cb * 32), r);
-      tmem_wait_ld();
-      const int64_t s = base + quad * 32 + lane;
-      if (quad * 32 + lane < rows && s < B) {
-        float4* dst = reinterpret_cast<float4*>(z + s * kD + cb * 32);
-        const float* bb = sB1 + cb * 32;
-#pragma unroll
-        for (int v = 0; v < 8; v++)
-          dst[v] = make_float4(__uint_as_float(r[4 * v]) + bb[4 * v], __uint_as_float(r[4 * v + 1]) + bb[4 * v + 1],
-                               __uint_as_float(r[4 * v + 2]) + bb[4 * v + 2], __uint_as_float(r[4 * v + 3]) + bb[4 * v + 3]);
-      }
-    }
-    tc_fence_before();
-    __syncthreads();   // A operands and the accumulator are reused next round
   }
+  __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128) : "memory");

@@ -99,8 +99,8 @@ def test_p2p_errors(lib):
         lib.mfp_p2p_export(m.ctx)
     assert e.value.status == 1
     with pytest.raises(lib.MfpError) as e:          # a short handle list (R = 4) is rejected in C
-        _ = lib._lib.mfp_p2p_open(m.ctx, None, 3)
-        lib._check(_, m.ctx)
+        from paper_2308_14258_b200 import mfp as binding
+        binding._check(binding._lib.mfp_p2p_open(m.ctx, None, 3), m.ctx)
     assert e.value.status == 1
     lib.mfp_p2p_open(m.ctx)
     with pytest.raises(lib.MfpError) as e:          # once per context

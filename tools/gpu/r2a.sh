@@ -1,0 +1,10 @@
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
+nproc > gpurun_out/nproc.txt; lscpu >> gpurun_out/nproc.txt
+python paper_2308_14258_b200/build.py > gpurun_out/build.log 2>&1
+timeout 600 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
+timeout 2400 python -m pytest tests -m gpu -q -x --durations=25 > gpurun_out/gpu_tests.log 2>&1
+tail -30 gpurun_out/gpu_tests.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
