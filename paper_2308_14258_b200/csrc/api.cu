@@ -236,7 +236,7 @@ mfp_status check_net(const mfp_sdnet_desc* n, std::string* err) {
     *err = "round-1 SDNet: conv 1->8->1, k=5 (reading G7)";
     return MFP_ERR_INVALID;
   }
-  if (n->d != kD) { *err = "round-1 SDNet: d must be 128"; return MFP_ERR_INVALID; }
+  if (n->d != kD && n->d != kD2) { *err = "SDNet width d must be 128 or 256 (SURVEY §8(b))"; return MFP_ERR_INVALID; }
   if (n->n_hidden < 1 || n->n_hidden > kMaxHidden) { *err = "n_hidden must be 1..3"; return MFP_ERR_INVALID; }
   if (n->gelu != 0 && n->gelu != 1) { *err = "gelu must be 0 or 1"; return MFP_ERR_INVALID; }
   return MFP_OK;
@@ -263,21 +263,23 @@ void carve(mfp_ctx* c, void* base, size_t* total) {
   const float* P = c->params;
   // parameter views (MFCK order)
   dn.conv1_w = P; dn.conv1_b = P + 40; dn.conv2_w = P + 48; dn.conv2_b = P + 88;
-  const int64_t oW1 = 89, oW2 = oW1 + kD * kNB, ob1 = oW2 + 2 * kD, oWh0 = ob1 + kD;
-  const int64_t owo = oWh0 + (int64_t)nh * (kD * kD + kD);
+  const int d = c->net.d;
+  const int64_t oW1 = 89, oW2 = oW1 + (int64_t)d * kNB, ob1 = oW2 + 2 * d, oWh0 = ob1 + d;
+  const int64_t owo = oWh0 + (int64_t)nh * ((int64_t)d * d + d);
   dn.b1 = P ? P + ob1 : nullptr;
   dn.W2 = P ? P + oW2 : nullptr;
   dn.wo = P ? P + owo : nullptr;
-  dn.bo = P ? P + owo + kD : nullptr;
+  dn.bo = P ? P + owo + d : nullptr;
+  dn.d = d;
   dn.n_hidden = nh;
   dn.gelu_tanh = c->net.gelu;
   dn.f16 = c->cfg.precision == MFP_FP16 ? 1 : 0;
-  dn.W1T = cv.take<float>((size_t)kNB * kD);
-  dn.WhT = cv.take<float>((size_t)nh * kD * kD);
-  dn.bh = cv.take<float>((size_t)nh * kD);
-  dn.QTc = cv.take<float>((size_t)kD * 64);
-  dn.QTf = cv.take<float>((size_t)kD * kQF);
-  dn.Wh_sw2 = cv.take<uint16_t>((size_t)nh * kWImg);
+  dn.W1T = cv.take<float>((size_t)kNB * d);
+  dn.WhT = cv.take<float>((size_t)nh * d * d);
+  dn.bh = cv.take<float>((size_t)nh * d);
+  dn.QTc = cv.take<float>((size_t)d * 64);
+  dn.QTf = cv.take<float>((size_t)d * kQF);
+  dn.Wh_sw2 = cv.take<uint16_t>(wimg_elems(d, nh));
   dn.W1img = cv.take<uint16_t>((size_t)2 * kD * kNB);
   dn.HcT = cv.take<float>((size_t)kNB * 64);
   dn.HfT = cv.take<float>((size_t)kNB * kQF);
@@ -297,7 +299,7 @@ void carve(mfp_ctx* c, void* base, size_t* total) {
     zc = std::max<int64_t>(zc, p.final_anchor.size());
     zc = std::max<int64_t>(zc, 4096);  // staging for mfp_sdnet_batch chunks
     rs.zcap = zc;
-    rs.z = cv.take<float>((size_t)zc * kD);
+    rs.z = cv.take<float>((size_t)zc * d);
     for (int k = 0; k < 4; k++) rs.anchors[k] = cv.take<uint32_t>(std::max<size_t>(1, p.phase_anchor[k].size()));
     rs.final_anchor = cv.take<uint32_t>(std::max<size_t>(1, p.final_anchor.size()));
     rs.final_lat_anchor = cv.take<uint32_t>(std::max<size_t>(1, p.final_lat_anchor.size()));
@@ -353,7 +355,9 @@ struct SpanGuard {
 // tcgen05 split-bf16 embed (kernels_embed_tc.cu), fp32 the SIMT one.
 void embed(mfp_ctx* c, const float* lat, const LatticeGeom& L, const uint32_t* anchors, const float* gb,
            int64_t B, float* z) {
-  if (c->cfg.precision != MFP_FP32 && embed_tc_enabled()) launch_embed_tc(lat, L, anchors, gb, B, c->dn, z, c->stream);
+  // (the tcgen05 embed holds d = 128 W1 images; d = 256 embeds on the SIMT kernel)
+  if (c->cfg.precision != MFP_FP32 && c->dn.d == kD && embed_tc_enabled())
+    launch_embed_tc(lat, L, anchors, gb, B, c->dn, z, c->stream);
   else launch_gather_embed(lat, L, anchors, gb, B, c->dn, z, c->stream);
 }
 
@@ -925,10 +929,10 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
   if (cfg->subsolver == MFP_SDNET) {
     CK(cudaMemcpyAsync(c->params, params, n_params * sizeof(float), cudaMemcpyHostToDevice, s));
     for (int i = 0; i < 89; i++) c->dn.convw[i] = params[i];   // MFCK order: conv1 w, b, conv2 w, b
-    CK(cudaMemsetAsync((void*)c->dn.Wh_sw2, 0, (size_t)net->n_hidden * kWImg * 2, s));
+    CK(cudaMemsetAsync((void*)c->dn.Wh_sw2, 0, wimg_elems(net->d, net->n_hidden) * 2, s));
     PrepArgs a;
-    a.P = c->params; a.n_hidden = net->n_hidden; a.f16 = cfg->precision == MFP_FP16 ? 1 : 0;
-    a.oW1 = 89; a.oW2 = 89 + kD * kNB; a.oWh0 = a.oW2 + 2 * kD + kD;
+    a.P = c->params; a.n_hidden = net->n_hidden; a.d = net->d; a.f16 = cfg->precision == MFP_FP16 ? 1 : 0;
+    a.oW1 = 89; a.oW2 = 89 + (int64_t)net->d * kNB; a.oWh0 = a.oW2 + 3 * (int64_t)net->d;
     a.W1T = (float*)c->dn.W1T; a.WhT = (float*)c->dn.WhT; a.bh = (float*)c->dn.bh;
     a.QTc = (float*)c->dn.QTc; a.QTf = (float*)c->dn.QTf;
     a.Wsw2 = (uint16_t*)c->dn.Wh_sw2;

@@ -21,40 +21,64 @@ __host__ __device__ __forceinline__ uint32_t sw128_offset(int r, int k) {
   return (uint32_t)(kb * 16384 + r * 128 + ((chunk ^ (r & 7)) << 4) + within * 2);
 }
 
+// 16-bit operand value of a weight (B operands are scaled by 1/2, exact,
+// because the tensor-core epilogue feeds h' = 2 GELU(x) into the next layer)
+__device__ __forceinline__ void put16(uint8_t* p, float v, int f16) {
+  if (f16) *reinterpret_cast<__half*>(p) = __float2half_rn(v);
+  else *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(v);
+}
+// b = b_hi + b_lo in the operand type (the bias step's two K columns)
+__device__ __forceinline__ void put_bias(uint8_t* p, float b, int f16) {
+  if (f16) {
+    const __half hi = __float2half_rn(b), lo = __float2half_rn(b - __half2float(hi));
+    *reinterpret_cast<__half*>(p) = hi;
+    *reinterpret_cast<__half*>(p + 2) = lo;
+  } else {
+    const __nv_bfloat16 hi = __float2bfloat16_rn(b), lo = __float2bfloat16_rn(b - __bfloat162float(hi));
+    *reinterpret_cast<__nv_bfloat16*>(p) = hi;
+    *reinterpret_cast<__nv_bfloat16*>(p + 2) = lo;
+  }
+}
+
 __global__ void k_prep(PrepArgs a) {
-  const int d = kD;
+  const int d = a.d;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  // W1T[k][c] = W1[c][k]; bf16 split images W1 = W1_hi + W1_lo (row c, K k)
+  // W1T[k][c] = W1[c][k]; at d = 128 also the bf16 split images W1 = W1_hi + W1_lo
+  // (row c, K k) of the tensor-core embed
   for (int64_t i = tid; i < (int64_t)kNB * d; i += nth) {
     int k = (int)(i / d), c = (int)(i % d);
     const float w = a.P[a.oW1 + (int64_t)c * kNB + k];
     a.W1T[i] = w;
-    const __nv_bfloat16 hi = __float2bfloat16_rn(w);
-    const __nv_bfloat16 lo = __float2bfloat16_rn(w - __bfloat162float(hi));
-    uint8_t* img = reinterpret_cast<uint8_t*>(a.W1img);
-    *reinterpret_cast<__nv_bfloat16*>(img + sw128_offset(c, k)) = hi;
-    *reinterpret_cast<__nv_bfloat16*>(img + kD * kNB * 2 + sw128_offset(c, k)) = lo;
+    if (d == kD) {
+      const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+      const __nv_bfloat16 lo = __float2bfloat16_rn(w - __bfloat162float(hi));
+      uint8_t* img = reinterpret_cast<uint8_t*>(a.W1img);
+      *reinterpret_cast<__nv_bfloat16*>(img + sw128_offset(c, k)) = hi;
+      *reinterpret_cast<__nv_bfloat16*>(img + kD * kNB * 2 + sw128_offset(c, k)) = lo;
+    }
   }
   // hidden layers
   for (int64_t i = tid; i < (int64_t)a.n_hidden * d * d; i += nth) {
-    int l = (int)(i / (d * d));
-    int rem = (int)(i % (d * d));
+    int l = (int)(i / ((int64_t)d * d));
+    int rem = (int)(i % ((int64_t)d * d));
     int k = rem / d, n = rem % d;
     const float* Wl = a.P + a.oWh0 + (int64_t)l * (d * d + d);
     const float w = Wl[(int64_t)n * d + k];
     a.WhT[i] = w;                                    // [l][k][n]
-    // CTA-pair image: half n/64 holds rows n%64 as a 64-row SW128 K-major
-    // block (two 8 KB K-halves) followed by its 2 KB bias block
-    uint8_t* img2 = reinterpret_cast<uint8_t*>(a.Wsw2 + (int64_t)l * kWImg) + (n >> 6) * (kWImg);
-    const int rr = n & 63;
-    const uint32_t off2 = (uint32_t)((k >> 6) * 8192 + rr * 128 + ((((k & 63) >> 3) ^ (rr & 7)) << 4) + (k & 7) * 2);
-    // B operand row n = output feature, K-major; scaled by 1/2 (exact) because
-    // the tensor-core epilogue feeds h' = 2 GELU(x) into the next layer
-    if (a.f16) {
-      *reinterpret_cast<__half*>(img2 + off2) = __float2half_rn(0.5f * w);
+    if (d == kD) {
+      // CTA-pair image: half n/64 holds rows n%64 as a 64-row SW128 K-major
+      // block (two 8 KB K-halves) followed by its 2 KB bias block
+      uint8_t* img2 = reinterpret_cast<uint8_t*>(a.Wsw2 + (int64_t)l * kWImg) + (n >> 6) * (kWImg);
+      const int rr = n & 63;
+      const uint32_t off2 = (uint32_t)((k >> 6) * 8192 + rr * 128 + ((((k & 63) >> 3) ^ (rr & 7)) << 4) + (k & 7) * 2);
+      put16(img2 + off2, 0.5f * w, a.f16);
     } else {
-      *reinterpret_cast<__nv_bfloat16*>(img2 + off2) = __float2bfloat16_rn(0.5f * w);
+      // d = 256: CTA n/128 holds rows n%128 as four 16 KB SW128 K-chunks of 64
+      uint8_t* img = reinterpret_cast<uint8_t*>(a.Wsw2 + (int64_t)l * kW2Layer + (int64_t)(n >> 7) * kW2Cta);
+      const int rr = n & 127;
+      const uint32_t off = (uint32_t)((k >> 6) * 16384 + rr * 128 + ((((k & 63) >> 3) ^ (rr & 7)) << 4) + (k & 7) * 2);
+      put16(img + off, 0.5f * w, a.f16);
     }
   }
   for (int64_t i = tid; i < (int64_t)a.n_hidden * d; i += nth) {
@@ -65,17 +89,14 @@ __global__ void k_prep(PrepArgs a) {
     // (SWIZZLE_NONE K-major: 8-row x 16-byte core matrices, LBO 128 B, SBO 256 B);
     // the A operand carries a constant 1 in those two columns, so the MMA adds
     // b_hi + b_lo (accurate to ~2^-17 relative) to the fp32 accumulator.
-    const int rr = c & 63;
-    uint8_t* blk2 = reinterpret_cast<uint8_t*>(a.Wsw2 + (int64_t)l * kWImg) + (c >> 6) * kWImg + 16384;
-    const uint32_t off2 = (uint32_t)((rr >> 3) * 256 + (rr & 7) * 16);
-    if (a.f16) {
-      const __half hi = __float2half_rn(b), lo = __float2half_rn(b - __half2float(hi));
-      *reinterpret_cast<__half*>(blk2 + off2) = hi;
-      *reinterpret_cast<__half*>(blk2 + off2 + 2) = lo;
+    if (d == kD) {
+      const int rr = c & 63;
+      uint8_t* blk2 = reinterpret_cast<uint8_t*>(a.Wsw2 + (int64_t)l * kWImg) + (c >> 6) * kWImg + 16384;
+      put_bias(blk2 + (rr >> 3) * 256 + (rr & 7) * 16, b, a.f16);
     } else {
-      const __nv_bfloat16 hi = __float2bfloat16_rn(b), lo = __float2bfloat16_rn(b - __bfloat162float(hi));
-      *reinterpret_cast<__nv_bfloat16*>(blk2 + off2) = hi;
-      *reinterpret_cast<__nv_bfloat16*>(blk2 + off2 + 2) = lo;
+      const int rr = c & 127;
+      uint8_t* blk = reinterpret_cast<uint8_t*>(a.Wsw2 + (int64_t)l * kW2Layer + (int64_t)(c >> 7) * kW2Cta) + 65536;
+      put_bias(blk + (rr >> 3) * 256 + (rr & 7) * 16, b, a.f16);
     }
   }
   // Q = X W2^T (b1 is folded into z): centre (64 padded) and interior (961)

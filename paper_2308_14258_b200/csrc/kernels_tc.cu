@@ -519,7 +519,374 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
 
 }  // namespace tc2
 
+// ---------------------------------------------------------------------------
+// d = 256 (the wide SDNet variant): CTA pair, M = 256,
+// N = 256, K = 16 x 16 per layer + the bias step, two tile slots (TMEM 2 x 256
+// columns).  One layer of this CTA's half of the weights is 64 KB (three do not
+// fit next to two 64 KB A operands), so a producer streams them with TMA bulk
+// copies through a four-chunk ring (one 16 KB K-chunk of 64 per stage) in the
+// MMA issue order: per round of two tiles, layer by layer, each chunk feeding
+// both tiles' MMAs before it is refilled with the next layer's chunk (one
+// fetch per two tiles, ~16 B/clk/SM of L2 traffic).  A relay thread in the odd
+// CTA forwards the arrival of its chunks to the even CTA, whose issuer needs
+// both halves before an MMA; the MMAs that last read a chunk commit (multicast)
+// to both CTAs' `empty` barriers.  Epilogue: 8 warps per slot and CTA, two
+// threads per row (column halves ch = 0 / 1, 128 columns each, so a thread's
+// work per layer equals the d = 128 kernel's); the head's two partial dots meet
+// in shared memory.  The split layer's constant halves are folded into ONE
+// staged copy z + (W2[:,0] + W2[:,1]) / 2, so every centre-line row needs one
+// FMA per element (query offsets x - 1/2, y - 1/2).
+namespace tc2w {
+using namespace tc;
+using tc2::cluster_rank;
+using tc2::cluster_sync;
+using tc2::commit2;
+using tc2::mbar_arrive_remote;
 
+constexpr int D = kD2;
+constexpr int kSlots = 2;
+constexpr int kEpiWarps = 8 * kSlots;                 // 16
+constexpr int kProdWarp = kEpiWarps, kIssueWarp = kEpiWarps + 1;
+constexpr int kThreads = 32 * (kEpiWarps + 2);        // 576
+constexpr int kA = kRows * D * 2;                     // 64 KB A operand per slot (4 SW128 K-atoms)
+constexpr int kChunkB = kW2Chunk * 2;                 // 16 KB
+constexpr int kRing = 4;
+constexpr int kBiasB = 128 * 16 * 2;                  // 4 KB
+
+template <int F16>
+constexpr uint32_t idesc_w() {
+  return (1u << 4) | ((F16 ? 0u : 1u) << 7) | ((F16 ? 0u : 1u) << 10) | ((uint32_t)(D >> 3) << 17) |
+         ((uint32_t)(256 >> 4) << 24);
+}
+template <int F16>
+__device__ __forceinline__ void mma_w(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc_w<F16>()), "r"(accum)
+      : "memory");
+}
+
+struct SmemW {
+  uint8_t* A;      // [2][64 KB]
+  uint8_t* ring;   // [4][16 KB]
+  uint8_t* bias;   // [nh][4 KB]
+  uint8_t* ones;   // 4 KB
+  float* zbuf;     // [2 slots][4 subdomains][256]: z + (W2[:,0] + W2[:,1]) / 2
+  float* w2;       // [2][256]: W2[:,0], W2[:,1]
+  float* wo;       // [256]
+  float* hpart;    // [2 slots][128]: head partial dot of the ch = 1 half
+  uint64_t* bars;  // a_full[2] d_full[2] full[4] pfull[4] empty[4]
+  uint32_t* tmem_slot;
+};
+__device__ __forceinline__ SmemW carve_w(uint8_t* raw) {
+  SmemW s;
+  s.A = raw;
+  s.ring = s.A + kSlots * kA;
+  s.bias = s.ring + kRing * kChunkB;
+  s.ones = s.bias + kMaxHidden * kBiasB;
+  s.zbuf = (float*)(s.ones + kOnes);
+  s.w2 = s.zbuf + kSlots * kZRows * D;
+  s.wo = s.w2 + 2 * D;
+  s.hpart = s.wo + D;
+  s.bars = (uint64_t*)(s.hpart + kSlots * kRows);
+  s.tmem_slot = (uint32_t*)(s.bars + 4 + 3 * kRing);
+  return s;
+}
+constexpr size_t smem_bytes_w() {
+  return (size_t)kSlots * kA + kRing * kChunkB + kMaxHidden * kBiasB + kOnes +
+         4 * ((size_t)kSlots * kZRows * D + 3 * D + kSlots * kRows) + 8 * (4 + 3 * kRing) + 16;
+}
+
+template <int GELU, int F16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+k_chain_tc2w(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, Sink sink) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int nh = net.n_hidden;
+  const SmemW S = carve_w(smem_raw);
+  uint64_t* a_full = S.bars;
+  uint64_t* d_full = S.bars + 2;
+  uint64_t* full = S.bars + 4;
+  uint64_t* pfull = full + kRing;
+  uint64_t* empty = pfull + kRing;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const uint8_t* Wcta = reinterpret_cast<const uint8_t*>(net.Wh_sw2) + (size_t)rank * kW2Cta * 2;
+
+  // ---- prologue: bias blocks (resident), head / split-layer vectors, the
+  // constant ones block of the bias step, barriers, TMEM
+  for (int l = 0; l < nh; l++) {
+    const uint4* src = reinterpret_cast<const uint4*>(Wcta + (size_t)l * kW2Layer * 2 + 4 * kChunkB);
+    uint4* dst = reinterpret_cast<uint4*>(S.bias + l * kBiasB);
+    for (int i = threadIdx.x; i < kBiasB / 16; i += kThreads) dst[i] = __ldg(src + i);
+  }
+  for (int i = threadIdx.x; i < D; i += kThreads) {
+    S.wo[i] = (GELU == 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
+    S.w2[i] = __ldg(net.W2 + 2 * i);
+    S.w2[D + i] = __ldg(net.W2 + 2 * i + 1);
+  }
+  if (threadIdx.x < kRows) {
+    const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
+    const int r = threadIdx.x;
+    *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + (r & 7) * 16) = make_uint4(one | (one << 16), 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + 128 + (r & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSlots; s++) {
+      mbar_init(&a_full[s], 16);   // 8 warps x 2 CTAs (elected lanes)
+      mbar_init(&d_full[s], 1);    // multicast commit
+    }
+    for (int i = 0; i < kRing; i++) {
+      mbar_init(&full[i], 1);      // producer's arrive.expect_tx + the chunk's bytes
+      mbar_init(&pfull[i], 1);     // (even CTA) the odd CTA's relay
+      mbar_init(&empty[i], 1);     // multicast commit after the chunk's last MMA
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kProdWarp) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // both CTAs' barriers initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *S.tmem_slot;
+  pdl_launch_dependents();
+
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int64_t ntiles = (total_rows + 2 * kRows - 1) / (2 * kRows);
+  const int64_t nloc = ntiles > cid ? (ntiles - cid + ncl - 1) / ncl : 0;
+  const int64_t nsub = total_rows / q;
+
+  if (warp == kProdWarp) {
+    // ---- producer (each CTA, its own half): the weights are constant, so the
+    // first layer's chunks stream in before the PDL wait
+    if (lane == 0) {
+      uint32_t pe = 1u;
+      const uint32_t ring = smem_u32(S.ring);
+      for (int64_t j0 = 0; j0 < nloc; j0 += kSlots)
+        for (int l = 0; l < nh; l++) {
+          for (int i = 0; i < kRing; i++) {
+            mbar_wait(&empty[i], pe);
+            mbar_arrive_expect_tx(&full[i], (uint32_t)kChunkB);
+            bulk_g2s(ring + (uint32_t)(i * kChunkB), Wcta + (size_t)l * kW2Layer * 2 + (size_t)i * kChunkB,
+                     (uint32_t)kChunkB, &full[i]);
+          }
+          pe ^= 1u;
+        }
+    }
+    __syncwarp();
+  } else if (warp == kIssueWarp) {
+    if (rank == 0 && lane == 0) {
+      // ---- MMA issuer (even CTA): per round of two tiles, layer-major, slots in order
+      uint32_t pa[kSlots] = {0u, 0u}, pf = 0u;
+      const uint32_t ones_addr = smem_u32(S.ones), ring = smem_u32(S.ring);
+      for (int64_t j0 = 0; j0 < nloc; j0 += kSlots) {
+        const int users = (int)(nloc - j0 < kSlots ? nloc - j0 : kSlots);
+        for (int l = 0; l < nh; l++) {
+          for (int s = 0; s < users; s++) {
+            mbar_wait(&a_full[s], pa[s]);   // both CTAs' A operands of layer l written
+            pa[s] ^= 1u;
+            tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)(s * D);
+            const uint32_t a0 = smem_u32(S.A + s * kA);
+            for (int i = 0; i < kRing; i++) {
+              if (s == 0) {
+                mbar_wait(&full[i], pf);    // this CTA's chunk i
+                mbar_wait(&pfull[i], pf);   // the odd CTA's chunk i (relayed)
+                tc_fence_after();
+              }
+              const uint32_t b0 = ring + (uint32_t)(i * kChunkB);
+#pragma unroll
+              for (int kk = 0; kk < 4; kk++)
+                mma_w<F16>(d, sw128_desc(a0 + (uint32_t)(i * 16384 + kk * 32)), sw128_desc(b0 + (uint32_t)(kk * 32)),
+                           (i | kk) ? 1u : 0u);
+              if (s == users - 1) commit2(&empty[i]);   // chunk free in both CTAs once these complete
+            }
+            mma_w<F16>(d, nosw_desc(ones_addr), nosw_desc(smem_u32(S.bias + l * kBiasB)), 1u);   // bias step
+            commit2(&d_full[s]);
+          }
+          pf ^= 1u;
+        }
+      }
+    } else if (rank == 1 && lane == 0) {
+      // ---- relay (odd CTA): forward each landed chunk to the even CTA's issuer
+      uint32_t pf = 0u;
+      for (int64_t j0 = 0; j0 < nloc; j0 += kSlots)
+        for (int l = 0; l < nh; l++) {
+          for (int i = 0; i < kRing; i++) {
+            mbar_wait(&full[i], pf);
+            mbar_arrive_remote(&pfull[i], 0u);
+          }
+          pf ^= 1u;
+        }
+    }
+    __syncwarp();
+  } else {
+    // ---- epilogue: slot = warp / 8; thread = (row, column half ch)
+    pdl_wait();      // z (embed) and the lattice (previous phases) complete from here on
+    const int slot = warp >> 3;
+    const int ch = (warp >> 2) & 1;
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const int tis = (warp & 7) * 32 + lane;   // 0..255 within the slot
+    const uint32_t a_row = smem_u32(S.A + slot * kA) + (uint32_t)row * 128u + ((uint32_t)(2 * ch) << 14);
+    const int r7 = row & 7;
+    uint32_t a_sw[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) a_sw[j] = a_row + ((uint32_t)(j ^ r7) << 4);
+    const uint32_t t_row = tmem + (uint32_t)(slot * D + ch * 128) + ((uint32_t)(quad * 32) << 16);
+    float* zb = S.zbuf + slot * kZRows * D;
+    const float bo = __ldg(net.bo);
+    const int zi = 4 * tis, zr_ = zi >> 8, zc = zi & (D - 1);
+    auto row0_of = [&](int64_t j) -> int64_t { return (cid + j * ncl) * (2 * kRows) + rank * kRows; };
+    auto z_fetch = [&](int64_t j) -> float4 {
+      int64_t sidx = row0_of(j) / q + zr_;
+      if (sidx > nsub - 1) sidx = nsub - 1;
+      return __ldg(reinterpret_cast<const float4*>(z + sidx * D + zc));
+    };
+    auto z_stage = [&](const float4 v) {
+      const float4 a = *reinterpret_cast<const float4*>(S.w2 + zc);
+      const float4 b = *reinterpret_cast<const float4*>(S.w2 + D + zc);
+      *reinterpret_cast<float4*>(zb + zi) = make_float4(fmaf(0.5f, a.x + b.x, v.x), fmaf(0.5f, a.y + b.y, v.y),
+                                                        fmaf(0.5f, a.z + b.z, v.z), fmaf(0.5f, a.w + b.w, v.w));
+    };
+    auto arrive_a = [&]() {
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&a_full[slot], 0u);
+    };
+    if (slot < nloc) z_stage(z_fetch(slot));
+    uint32_t pd = 0u;
+    for (int64_t j = slot; j < nloc; j += kSlots) {
+      const int64_t row0 = row0_of(j);
+      int64_t s_first = row0 / q;
+      if (s_first > nsub - 1) s_first = nsub - 1;
+      named_sync(1 + slot, 256);   // this tile's staged z visible to the slot's 8 warps
+      const bool have_next = j + kSlots < nloc;
+      float4 znext = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (have_next) znext = z_fetch(j + kSlots);
+      const int64_t grow = row0 + row;
+      const bool valid = grow < total_rows;
+      const int64_t gr = valid ? grow : total_rows - 1;
+      const int64_t sidx = gr / q;
+      const int p = (int)(gr - sidx * q);
+      float qx, qy;
+      query_xy(q, p, &qx, &qy);
+      int zo = (int)(sidx - s_first);
+      if (zo < 0 || zo >= kZRows) zo = 0;
+
+      // ---- split layer (Eq. 5, a3): h' = 2 GELU(z[s] + W2 x_p) over this
+      // thread's 128 columns -> A operand (K-atoms 2 ch, 2 ch + 1)
+      const bool centre = (q == kQC);
+      const bool vert = p < kM - 1;
+      // staged zc = z + (W2[:,0] + W2[:,1]) / 2: vertical centre line (x = 1/2)
+      // zc + W2[:,1] (y - 1/2); horizontal (y = 1/2) zc + W2[:,0] (x - 1/2);
+      // general queries zc + W2[:,0] (x - 1/2) + W2[:,1] (y - 1/2)
+      const float* zs = zb + zo * D + ch * 128;
+      const float* w1s = S.w2 + ((centre && vert) ? D : 0) + ch * 128;
+      const float q1 = (centre && vert) ? qy - 0.5f : qx - 0.5f;
+#pragma unroll 1
+      for (int kh = 0; kh < 2; kh++) {
+#pragma unroll
+        for (int j16 = 0; j16 < 4; j16++) {
+          const int c0 = 64 * kh + 16 * j16;
+          float v[16];
+          const f2 Q1 = f2_make(q1, q1);
+#pragma unroll
+          for (int i = 0; i < 4; i++) {
+            const float4 zz = *reinterpret_cast<const float4*>(zs + c0 + 4 * i);
+            const float4 aa = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
+            f2 v01 = ffma2(f2_make(aa.x, aa.y), Q1, f2_make(zz.x, zz.y));
+            f2 v23 = ffma2(f2_make(aa.z, aa.w), Q1, f2_make(zz.z, zz.w));
+            if (!centre) {
+              const float4 bb = *reinterpret_cast<const float4*>(S.w2 + D + ch * 128 + c0 + 4 * i);
+              const f2 QY = f2_make(qy - 0.5f, qy - 0.5f);
+              v01 = ffma2(f2_make(bb.x, bb.y), QY, v01);
+              v23 = ffma2(f2_make(bb.z, bb.w), QY, v23);
+            }
+            f2_split(v01, v[4 * i], v[4 * i + 1]);
+            f2_split(v23, v[4 * i + 2], v[4 * i + 3]);
+          }
+          uint32_t w[8];
+          act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v), *reinterpret_cast<uint32_t(*)[4]>(w));
+          act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v + 8), *reinterpret_cast<uint32_t(*)[4]>(w + 4));
+          st_shared_v4(a_sw[2 * j16] + ((uint32_t)kh << 14), w[0], w[1], w[2], w[3]);
+          st_shared_v4(a_sw[2 * j16 + 1] + ((uint32_t)kh << 14), w[4], w[5], w[6], w[7]);
+        }
+      }
+      fence_proxy_async();
+      arrive_a();
+
+      // ---- hidden layers (a4) and head (a5)
+      f2 yacc = f2_make(0.f, 0.f);
+      for (int l = 0; l < nh; l++) {
+        mbar_wait(&d_full[slot], pd);
+        pd ^= 1u;
+        tc_fence_after();
+        auto layer_epi = [&](auto last_tag) {
+          constexpr bool LAST = decltype(last_tag)::value;
+          auto work16 = [&](const uint32_t (&r)[16], int c16) {
+            if constexpr (!LAST) {
+#pragma unroll
+              for (int c8 = 0; c8 < 2; c8++) {
+                const int g = 2 * c16 + c8;   // 8-column group: K-atom 2 ch + g / 8, chunk g % 8
+                float v[8];
+#pragma unroll
+                for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[c8 * 8 + e]);
+                uint32_t w[4];
+                act8<GELU, F16>(v, w);
+                st_shared_v4(a_sw[g & 7] + ((uint32_t)(g >> 3) << 14), w[0], w[1], w[2], w[3]);
+              }
+            } else {
+              head32<GELU, 16>(r, S.wo + ch * 128 + c16 * 16, yacc);
+            }
+          };
+          uint32_t ra[16], rb[16];
+          tmem_ld16(t_row, ra);
+          tmem_wait_ld_dep16(ra);
+#pragma unroll
+          for (int c16 = 0; c16 < 8; c16 += 2) {
+            tmem_ld16(t_row + (uint32_t)((c16 + 1) * 16), rb);
+            work16(ra, c16);
+            tmem_wait_ld_dep16(rb);
+            if (c16 + 2 < 8) tmem_ld16(t_row + (uint32_t)((c16 + 2) * 16), ra);
+            work16(rb, c16 + 1);
+            if (c16 + 2 < 8) tmem_wait_ld_dep16(ra);
+          }
+        };
+        const bool last = (l == nh - 1);
+        if (last) layer_epi(std::true_type{});
+        else layer_epi(std::false_type{});
+        tc_fence_before();
+        if (!last) {
+          fence_proxy_async();
+          arrive_a();
+        }
+      }
+      float y0, y1;
+      f2_split(yacc, y0, y1);
+      // ---- the row's two partial head dots meet in shared memory
+      if (ch == 1) S.hpart[slot * kRows + row] = y0 + y1;
+      named_sync(1 + slot, 256);
+      if (have_next) z_stage(znext);   // every thread of the slot is past this tile's split layer
+      if (ch == 0 && valid) sink_store(sink, sidx, p, ((y0 + y1) + S.hpart[slot * kRows + row]) + bo);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == kProdWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
+}
+
+}  // namespace tc2w
 
 bool chain_tc_available() { return true; }
 
@@ -537,6 +904,11 @@ void tc_kernel_attributes() {
   cudaFuncSetAttribute(tc2::k_chain_tc2<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
   cudaFuncSetAttribute(tc2::k_chain_tc2<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
   cudaFuncSetAttribute(tc2::k_chain_tc2<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  const int mxw = (int)tc2w::smem_bytes_w();
+  cudaFuncSetAttribute(tc2w::k_chain_tc2w<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxw);
+  cudaFuncSetAttribute(tc2w::k_chain_tc2w<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxw);
+  cudaFuncSetAttribute(tc2w::k_chain_tc2w<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxw);
+  cudaFuncSetAttribute(tc2w::k_chain_tc2w<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxw);
 }
 
 // Persistent grid: one CTA pair per TPC (74 clusters), or fewer for small batches.
@@ -544,7 +916,7 @@ void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const 
                      cudaStream_t s) {
   if (B <= 0) return;
   const int64_t rows = B * q;
-  const size_t sm = tc2::smem_bytes2(net.n_hidden);
+  const size_t sm = net.d == kD2 ? tc2w::smem_bytes_w() : tc2::smem_bytes2(net.n_hidden);
   const int64_t ptiles = (rows + 2 * tc::kRows - 1) / (2 * tc::kRows);
   int64_t pairs = num_sms / 2;
   // MFP_MAX_PAIRS=n (sanitizer runs only): cap the persistent grid so a small
@@ -552,7 +924,11 @@ void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const 
   static const int max_pairs = getenv("MFP_MAX_PAIRS") ? atoi(getenv("MFP_MAX_PAIRS")) : 0;
   if (max_pairs > 0 && pairs > max_pairs) pairs = max_pairs;
   const int grid = 2 * (int)(ptiles < pairs ? ptiles : pairs);
-#define MFP_TC2(G, F) launch_pdl(tc2::k_chain_tc2<G, F>, grid, tc2::kThreads2, sm, s, z, rows, q, net, sink)
+#define MFP_TC2(G, F)                                                                              \
+  do {                                                                                             \
+    if (net.d == kD2) launch_pdl(tc2w::k_chain_tc2w<G, F>, grid, tc2w::kThreads, sm, s, z, rows, q, net, sink); \
+    else launch_pdl(tc2::k_chain_tc2<G, F>, grid, tc2::kThreads2, sm, s, z, rows, q, net, sink);   \
+  } while (0)
   if (net.f16) {
     if (net.gelu_tanh) MFP_TC2(1, 1); else MFP_TC2(0, 1);
   } else {

@@ -17,7 +17,8 @@ constexpr int kH = kM / 2;         // lattice spacing m/2
 constexpr int kNB = 4 * kM;        // perimeter length 4m = 128 (G1)
 constexpr int kQC = 2 * kM - 3;    // centre-line queries 61 (G3)
 constexpr int kQF = (kM - 1) * (kM - 1);  // interior queries 961
-constexpr int kD = 128;            // SDNet width (G7)
+constexpr int kD = 128;            // SDNet width, canonical (G7)
+constexpr int kD2 = 256;           // the wide variant (d = 128 | 256)
 constexpr int kC1 = 8;             // conv channels 1 -> 8 -> 1, k = 5 (G7)
 constexpr int kK = 5;
 constexpr int kMaxHidden = 3;
@@ -27,6 +28,17 @@ constexpr int kMaxHidden = 3;
 constexpr int kWImgW = kD * kD;             // elements
 constexpr int kWImgB = kD * 16;
 constexpr int kWImg = kWImgW + kWImgB;      // 18432 elements = 36 KB
+// d = 256: per hidden layer and CTA of the pair, this CTA's 128 output rows
+// (B operand rows 128 r .. 128 r + 127 of the N = 256 pair MMA) as four K-chunks
+// of 64 (128 rows x 128 B SWIZZLE_128B, 16 KB each, streamed by TMA) followed by
+// its 128 x 16 bias block (4 KB, resident).
+constexpr int kW2Chunk = 128 * 64;            // elements (16 KB)
+constexpr int kW2Cta = 4 * kW2Chunk + 128 * 16;   // 34816 elements = 68 KB
+constexpr int kW2Layer = 2 * kW2Cta;
+// 16-bit hidden-weight image elements for width d
+inline size_t wimg_elems(int d, int n_hidden) {
+  return (size_t)n_hidden * (d == kD2 ? (size_t)kW2Layer : (size_t)kWImg);
+}
 
 // Local lattice of one rank: horizontal lines y = RY0 + 16 i
 // (x-contiguous, RX0..RX1) then vertical lines x = RX0 + 16 j (y-contiguous,
@@ -99,11 +111,13 @@ struct DevNet {
   const float* bh;       // [n_hidden][d]
   const float* wo;       // [d]
   const float* bo;       // [1]
+  int d;                 // SDNet width: kD (128) or kD2 (256)
   int n_hidden;
   int gelu_tanh;
   int f16;               // tensor-core operands fp16 (1) or bf16 (0)
   // bf16 tables (tcgen05 path): weights pre-swizzled into the SW128 K-major image
-  const uint16_t* Wh_sw2; // [n_hidden][2][18 KB half] (CTA-pair chain: rows 64h..64h+63)
+  const uint16_t* Wh_sw2; // d = 128: [n_hidden][2][18 KB half] (CTA-pair chain: rows 64h..64h+63)
+                          // d = 256: [n_hidden][2 CTAs][4 chunks x 16 KB + 4 KB bias] (kW2Cta)
   const uint16_t* W1img;  // [2][128*128] bf16 SW128 images of W1 = W1_hi + W1_lo (tensor-core embed)
   // exact subsolver
   const float* HcT;      // [128 k][64]  (61 used)
@@ -211,6 +225,7 @@ void launch_final_lines(const float* lat, const LatticeGeom& L, int X0, int Y0, 
 struct PrepArgs {
   const float* P;          // raw params, MFCK order
   int n_hidden;
+  int d;                   // 128 or 256
   int f16;                 // tensor-core operand images in fp16 (1) or bf16 (0)
   int64_t oW1, oW2, oWh0;  // offsets; Wh_l at oWh0 + l*(d*d + d), bh_l right after
   float* W1T; float* WhT; float* bh;
