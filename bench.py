@@ -66,6 +66,43 @@ def parse():
     return p.parse_args()
 
 
+# ------------------------------------------------------------------ d = 256 leg
+def wide_leg(mfp, torch, stream, cfg, g_dev, u_dev, flush, ppi, peaks, T=16, steps=3):
+    """The same MFP with the wide SDNet (d = 256, SURVEY §8(b)/(d) "report both d
+    values"): predictions/s over `steps` solves of T iterations (device events,
+    L2 flushed between solves, outside the events) and the roofline of its chain
+    k_chain_tc2w (rows x 3 x 2 x 256^2 FLOP per launch / the launch's event time)."""
+    from mfp_inputs import random_weights
+    D = 256
+    mw = mfp.Mfp(cfg, mfp.make_net(d=D, gelu=1), random_weights(0, d=D), stream=stream)
+    for _ in range(2):
+        mw.solve_device(g_dev, T, 0.0, u_dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(float(i))
+            ev[i][0].record(stream)
+        mw.solve_device(g_dev, T, 0.0, u_dev)
+        with torch.cuda.stream(stream):
+            ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    prof = mw.profile(4)
+    chain_ms = prof.chain_ms_total / max(prof.chain_launches, 1)
+    flop = prof.chain_rows / max(prof.chain_launches, 1) * 3 * 2 * D * D
+    peak = peaks.get("bf16_tflops_sustained", 1400.0)
+    achieved = flop / (chain_ms / 1000.0) / 1e12
+    mw.close()
+    return {"d": D, "value": ppi * T * steps / (ms / 1000.0), "unit": "predictions/s",
+            "ms_per_solve": ms / steps, "iters_per_solve": T,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "kernel": "k_chain_tc2w (d = 256 hidden GEMM chain)",
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                         "flop_per_launch": flop, "chain_ms_per_launch": chain_ms,
+                         "chain_per_phase_ms": prof.ms_chain, "gather_embed_per_phase_ms": prof.ms_gather_embed,
+                         "iteration_ms": prof.ms_per_iter}}
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """nvidia-smi-equivalent clock / throttle-reason sampling (NVML) during the timed region."""
@@ -616,7 +653,9 @@ def main():
                             "iterations at 2049^2 on 1 A30, 880 s)"}
                 mf.close()
 
-    bio = sweep = None
+    bio = sweep = wide = None
+    if world == 1 and tensor:
+        wide = wide_leg(mfp, torch, stream, cfg, g_dev, u_dev, flush, ppi, peaks)
     if world == 1:
         sweep = sdnet_batch_sweep(m, torch, stream)
         bio = boundary_io_bench(mfp, torch, peaks)
@@ -629,7 +668,8 @@ def main():
                 "scaling": args.scaling, "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
                 "config": bench_config(T, grid, tensor, nx, ny, args.scaling),
                 "points_iter_per_s": (nx + 1) * (ny + 1) * T * args.steps / (ms / 1000.0),
-                "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "roofline_d256": wide,
+                "cpu_baseline": cpu,
                 "time_to_converge": ttc, "sdnet_batch_sweep": sweep, "boundary_io": bio,
                 "paper_context": {"note": "the paper's own numbers, other hardware (context, not a baseline; "
                                           "BASELINE.md)",
