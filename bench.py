@@ -67,14 +67,15 @@ def parse():
 
 
 # ------------------------------------------------------------------ d = 256 leg
-def wide_leg(mfp, torch, stream, cfg, g_dev, u_dev, flush, ppi, peaks, T=16, steps=3):
-    """The same MFP with the wide SDNet (d = 256, SURVEY §8(b)/(d) "report both d
-    values"): predictions/s over `steps` solves of T iterations (device events,
-    L2 flushed between solves, outside the events) and the roofline of its chain
-    k_chain_tc2w (rows x 3 x 2 x 256^2 FLOP per launch / the launch's event time)."""
+def wide_leg(mfp, torch, stream, cfg, g_dev, u_dev, flush, ppi, peaks, T=16, steps=3, D=256, gelu=1,
+             kernel="k_chain_tc2w (d = 256 hidden GEMM chain)"):
+    """The same MFP with another SDNet variant — by default the wide SDNet (d = 256,
+    SURVEY §8(b)/(d) "report both d values"); with cfg.precision = FP16X the
+    accuracy mode: predictions/s over `steps` solves of T iterations (device
+    events, L2 flushed between solves, outside the events) and the roofline of its
+    chain (rows x 3 x 2 x d^2 FLOP per launch / the launch's event time)."""
     from mfp_inputs import random_weights
-    D = 256
-    mw = mfp.Mfp(cfg, mfp.make_net(d=D, gelu=1), random_weights(0, d=D), stream=stream)
+    mw = mfp.Mfp(cfg, mfp.make_net(d=D, gelu=gelu), random_weights(0, d=D), stream=stream)
     for _ in range(2):
         mw.solve_device(g_dev, T, 0.0, u_dev)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
@@ -96,7 +97,7 @@ def wide_leg(mfp, torch, stream, cfg, g_dev, u_dev, flush, ppi, peaks, T=16, ste
     return {"d": D, "value": ppi * T * steps / (ms / 1000.0), "unit": "predictions/s",
             "ms_per_solve": ms / steps, "iters_per_solve": T,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "kernel": "k_chain_tc2w (d = 256 hidden GEMM chain)",
+                         "frac": achieved / peak, "kernel": kernel,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                          "flop_per_launch": flop, "chain_ms_per_launch": chain_ms,
                          "chain_per_phase_ms": prof.ms_chain, "gather_embed_per_phase_ms": prof.ms_gather_embed,
@@ -653,9 +654,19 @@ def main():
                             "iterations at 2049^2 on 1 A30, 880 s)"}
                 mf.close()
 
-    bio = sweep = wide = None
+    bio = sweep = wide = acc = None
     if world == 1 and tensor:
         wide = wide_leg(mfp, torch, stream, cfg, g_dev, u_dev, flush, ppi, peaks)
+        # the tensor-core accuracy mode (split fp16 activations + accurate GELU;
+        # holds 3e-3 per field with trained weights, tests/test_gpu_fp16x.py): its
+        # throughput cost on the same workload
+        cfg_x = mfp.make_config(nx, ny, grid, precision=mfp.FP16X, subsolver=mfp.SDNET, check_every=16)
+        acc = wide_leg(mfp, torch, stream, cfg_x, g_dev, u_dev, flush, ppi, peaks, D=128, gelu=2,
+                       kernel="k_chain_tc2s (MFP_FP16X: split fp16 activations, d = 128)")
+        acc["chain_time_vs_headline_chain"] = acc["roofline"]["chain_ms_per_launch"] / roofline["chain_ms_per_launch"]
+        acc["note"] = ("value counts the same 65,025 unique predictions per iteration; each solve of T = 16 "
+                       "iterations includes the final phase, so compare chain_time_vs_headline_chain, not value, "
+                       "with the headline")
     if world == 1:
         sweep = sdnet_batch_sweep(m, torch, stream)
         bio = boundary_io_bench(mfp, torch, peaks)
@@ -669,6 +680,7 @@ def main():
                 "config": bench_config(T, grid, tensor, nx, ny, args.scaling),
                 "points_iter_per_s": (nx + 1) * (ny + 1) * T * args.steps / (ms / 1000.0),
                 "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "roofline_d256": wide,
+                "accuracy_mode_fp16x": acc,
                 "cpu_baseline": cpu,
                 "time_to_converge": ttc, "sdnet_batch_sweep": sweep, "boundary_io": bio,
                 "paper_context": {"note": "the paper's own numbers, other hardware (context, not a baseline; "

@@ -80,8 +80,13 @@ typedef enum {
 /* Arithmetic of the SDNet MLP chain: FP32 = SIMT fp32 with exact-erf GELU (the
  * parity twin); BF16 / FP16 = tcgen05 tensor cores with operands rounded to
  * bf16 / fp16 and fp32 accumulation in TMEM (same throughput; fp16 has 8x
- * smaller unit roundoff). */
-enum { MFP_FP32 = 0, MFP_BF16 = 1, MFP_FP16 = 2 };
+ * smaller unit roundoff); FP16X = the accuracy mode of the
+ * tensor-core path (d = 128): every activation feeding an MMA is split
+ * h = h_hi + h_lo into two fp16 operands and both products are accumulated
+ * against the fp16 weights, so only the weights are rounded (
+ * with trained weights and gelu = 2 it holds the 3e-3 per-field bar that the
+ * single-rounding modes miss). */
+enum { MFP_FP32 = 0, MFP_BF16 = 1, MFP_FP16 = 2, MFP_FP16X = 3 };
 enum { MFP_SDNET = 0, MFP_EXACT_LAPLACE = 1 };  /* subdomain solver   */
 enum { MFP_QUERY_CENTRE = 0, MFP_QUERY_INTERIOR = 1 };
 
@@ -93,13 +98,14 @@ typedef struct {
   int32_t stride;      /* must be m/2 (paper d = 2)                           */
   int32_t grid_rows;   /* Py: processor rows    ((ny/m) % Py == 0)                  */
   int32_t grid_cols;   /* Px: processor columns ((nx/m) % Px == 0)                  */
-  int32_t precision;   /* MFP_FP32 | MFP_BF16 | MFP_FP16                             */
+  int32_t precision;   /* MFP_FP32 | MFP_BF16 | MFP_FP16 | MFP_FP16X                 */
   int32_t subsolver;   /* MFP_SDNET | MFP_EXACT_LAPLACE                              */
   int32_t check_every; /* c >= 1: convergence test every c iterations                */
 } mfp_config;
 
-/* SDNet shape (sizes are reading G7).  Round 1 supports
- * n_conv = 2, conv_k = {5,5}, conv_ch = {1,8,1}, d = 128, 1 <= n_hidden <= 3. */
+/* SDNet shape (sizes are reading G7).  Supported:
+ * n_conv = 2, conv_k = {5,5}, conv_ch = {1,8,1}, d = 128 or 256 (
+ * MFP_FP16X: d = 128), 1 <= n_hidden <= 3. */
 typedef struct {
   int32_t n_conv;
   int32_t conv_k[4];
@@ -107,9 +113,10 @@ typedef struct {
   int32_t d;
   int32_t n_hidden;
   int32_t gelu;        /* 0: erff-based GELU; 1: fast GELU on the tensor-core paths —
-                        * the same exact GELU x Phi(x) from fitted tanh / polynomial
-                        * forms, |error of 2 GELU| <= 4e-4 (reading GELU).
-                        * The fp32 path always uses erff.                          */
+                        * the classic tanh form of x Phi(x), |error of 2 GELU| <= 9.5e-4;
+                        * 2: accurate tanh form tanh(x (c0 + t (c1 + t c2))),
+                        * t = min(x^2, 16), |error of 2 GELU| <= 5e-5 (DESIGN.md
+                        * reading GELU).  The fp32 chain always uses erff.          */
 } mfp_sdnet_desc;
 
 typedef struct {

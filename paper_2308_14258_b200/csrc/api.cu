@@ -238,7 +238,7 @@ mfp_status check_net(const mfp_sdnet_desc* n, std::string* err) {
   }
   if (n->d != kD && n->d != kD2) { *err = "SDNet width d must be 128 or 256 (SURVEY §8(b))"; return MFP_ERR_INVALID; }
   if (n->n_hidden < 1 || n->n_hidden > kMaxHidden) { *err = "n_hidden must be 1..3"; return MFP_ERR_INVALID; }
-  if (n->gelu != 0 && n->gelu != 1) { *err = "gelu must be 0 or 1"; return MFP_ERR_INVALID; }
+  if (n->gelu < 0 || n->gelu > 2) { *err = "gelu must be 0, 1 or 2"; return MFP_ERR_INVALID; }
   return MFP_OK;
 }
 
@@ -273,7 +273,8 @@ void carve(mfp_ctx* c, void* base, size_t* total) {
   dn.d = d;
   dn.n_hidden = nh;
   dn.gelu_tanh = c->net.gelu;
-  dn.f16 = c->cfg.precision == MFP_FP16 ? 1 : 0;
+  dn.f16 = (c->cfg.precision == MFP_FP16 || c->cfg.precision == MFP_FP16X) ? 1 : 0;
+  dn.split = c->cfg.precision == MFP_FP16X ? 1 : 0;
   dn.W1T = cv.take<float>((size_t)kNB * d);
   dn.WhT = cv.take<float>((size_t)nh * d * d);
   dn.bh = cv.take<float>((size_t)nh * d);
@@ -866,6 +867,8 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
   }
   if (cfg->precision != MFP_FP32 && cfg->subsolver == MFP_SDNET && !chain_tc_available())
     return fail(c, MFP_ERR_INVALID, "tcgen05 chain not built into this library");
+  if (cfg->precision == MFP_FP16X && cfg->subsolver == MFP_SDNET && net->d != kD)
+    return fail(c, MFP_ERR_INVALID, "MFP_FP16X (split activations) supports d = 128");
   // collective validation: every rank of the communicator must
   // hold the same config, SDNet shape and weights; a rank whose local checks
   // failed makes every rank fail instead of leaving its peers blocked in the
@@ -931,7 +934,7 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
     for (int i = 0; i < 89; i++) c->dn.convw[i] = params[i];   // MFCK order: conv1 w, b, conv2 w, b
     CK(cudaMemsetAsync((void*)c->dn.Wh_sw2, 0, wimg_elems(net->d, net->n_hidden) * 2, s));
     PrepArgs a;
-    a.P = c->params; a.n_hidden = net->n_hidden; a.d = net->d; a.f16 = cfg->precision == MFP_FP16 ? 1 : 0;
+    a.P = c->params; a.n_hidden = net->n_hidden; a.d = net->d; a.f16 = (cfg->precision == MFP_FP16 || cfg->precision == MFP_FP16X) ? 1 : 0;
     a.oW1 = 89; a.oW2 = 89 + (int64_t)net->d * kNB; a.oWh0 = a.oW2 + 3 * (int64_t)net->d;
     a.W1T = (float*)c->dn.W1T; a.WhT = (float*)c->dn.WhT; a.bh = (float*)c->dn.bh;
     a.QTc = (float*)c->dn.QTc; a.QTf = (float*)c->dn.QTf;

@@ -30,6 +30,18 @@ __device__ __forceinline__ float tanh_approx(float x) {
 // of the chain's throughput — DESIGN.md §7.
 constexpr float kGF0 = 0.7978845608028654f, kGF1 = 0.7978845608028654f * 0.044715f;
 
+// Accurate form (mfp_sdnet_desc.gelu = 2; the accuracy mode MFP_FP16X):
+// 2 GELU(x) ~= x + x tanh(x (a0 + t (a1 + t a2))), t = min(x^2, 16), minimax fit
+// of x erf(x / sqrt 2) (tools/fit_gelu_poly.py --three): |error of 2 GELU| <=
+// 5.04e-5 everywhere (the classic form: 9.5e-4), for two more instructions per
+// element.
+constexpr float kGA0 = 0.79750786895f, kGA1 = 0.037005660849f, kGA2 = -3.5151936221e-4f;
+__device__ __forceinline__ float gelu2_acc(float x) {
+  const float t = fminf(x * x, 16.0f);
+  const float u = x * fmaf(t, fmaf(t, kGA2, kGA1), kGA0);
+  return fmaf(x, tanh_approx(u), x);
+}
+
 // 2 GELU(x) (scalar).
 __device__ __forceinline__ float gelu2_fast(float x) {
   const float u = x * fmaf(kGF1, x * x, kGF0);
@@ -105,6 +117,7 @@ __device__ __forceinline__ void circ_window(const float (&v)[4], int lane, float
 template <int GELU>
 __device__ __forceinline__ float emb_act(float x) {
   if constexpr (GELU == 1) return gelu_fast(x);
+  else if constexpr (GELU == 2) return 0.5f * gelu2_acc(x);
   else return gelu_erf(x);
 }
 

@@ -56,7 +56,11 @@ __device__ __forceinline__ void circ_window2(const f2 (&v)[4], int lane, f2 (&w)
 }
 template <int GELU>
 __device__ __forceinline__ f2 emb_act2(f2 x) {
-  if constexpr (GELU == 1) {
+  if constexpr (GELU == 2) {   // accurate form (device_common.cuh gelu2_acc), halved
+    float a, b;
+    f2_split(x, a, b);
+    return f2_make(0.5f * gelu2_acc(a), 0.5f * gelu2_acc(b));
+  } else if constexpr (GELU == 1) {
     float u0, u1;
     f2_split(fmul2(x, ffma2(fmul2(x, x), f2_make(kGF1, kGF1), f2_make(kGF0, kGF0))), u0, u1);
     const f2 hx = fmul2(x, f2_make(0.5f, 0.5f));
@@ -311,6 +315,7 @@ bool embed_tc_enabled() {
 void embed_tc_kernel_attributes() {
   cudaFuncSetAttribute(emb::k_embed_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)emb::smem_bytes());
   cudaFuncSetAttribute(emb::k_embed_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)emb::smem_bytes());
+  cudaFuncSetAttribute(emb::k_embed_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)emb::smem_bytes());
 }
 
 void launch_embed_tc(const float* lat, const LatticeGeom& L, const uint32_t* anchors, const float* gb,
@@ -325,7 +330,9 @@ void launch_embed_tc(const float* lat, const LatticeGeom& L, const uint32_t* anc
   int64_t blocks = (B + rows - 1) / rows;
   if (blocks > sms) blocks = sms;
   const size_t sm = emb::smem_bytes();
-  if (net.gelu_tanh)
+  if (net.gelu_tanh == 2)
+    launch_pdl(emb::k_embed_tc<2>, (int)blocks, emb::kThreadsE, sm, s, lat, L, anchors, gb, B, rows, net, z);
+  else if (net.gelu_tanh == 1)
     launch_pdl(emb::k_embed_tc<1>, (int)blocks, emb::kThreadsE, sm, s, lat, L, anchors, gb, B, rows, net, z);
   else
     launch_pdl(emb::k_embed_tc<0>, (int)blocks, emb::kThreadsE, sm, s, lat, L, anchors, gb, B, rows, net, z);

@@ -122,9 +122,9 @@ void launch_gather_embed(const float* lat, const LatticeGeom& L, const uint32_t*
   if (blocks > per_sm * num_sms()) blocks = per_sm * num_sms();
 #define MFP_EMB(G, D) k_gather_embed<G, D><<<(int)blocks, kEmbWarps * 32, emb_smem<D>(), s>>>(lat, L, anchors, gb, B, net, z)
   if (net.d == kD) {
-    if (net.gelu_tanh) MFP_EMB(1, kD); else MFP_EMB(0, kD);
+    if (net.gelu_tanh == 2) MFP_EMB(2, kD); else if (net.gelu_tanh) MFP_EMB(1, kD); else MFP_EMB(0, kD);
   } else {
-    if (net.gelu_tanh) MFP_EMB(1, kD2); else MFP_EMB(0, kD2);
+    if (net.gelu_tanh == 2) MFP_EMB(2, kD2); else if (net.gelu_tanh) MFP_EMB(1, kD2); else MFP_EMB(0, kD2);
   }
 #undef MFP_EMB
 }
@@ -263,6 +263,8 @@ void sdnet_kernel_attributes() {
   cudaFuncSetAttribute(k_gather_embed<1, kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, emb_smem<kD>());
   cudaFuncSetAttribute(k_gather_embed<0, kD2>, cudaFuncAttributeMaxDynamicSharedMemorySize, emb_smem<kD2>());
   cudaFuncSetAttribute(k_gather_embed<1, kD2>, cudaFuncAttributeMaxDynamicSharedMemorySize, emb_smem<kD2>());
+  cudaFuncSetAttribute(k_gather_embed<2, kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, emb_smem<kD>());
+  cudaFuncSetAttribute(k_gather_embed<2, kD2>, cudaFuncAttributeMaxDynamicSharedMemorySize, emb_smem<kD2>());
   cudaFuncSetAttribute(k_chain_fp32<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)simt_smem<kD>(kMaxHidden));
   cudaFuncSetAttribute(k_chain_fp32<kD2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)simt_smem<kD2>(kMaxHidden));
 }

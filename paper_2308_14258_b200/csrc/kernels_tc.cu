@@ -74,6 +74,18 @@ __device__ __forceinline__ f2 gelu2_mufu(f2 x) {
 #endif
 }
 
+// Accurate form (gelu = 2, device_common.cuh gelu2_acc) on an fp32 pair:
+// t = min(x^2, 16) per lane, u = x (a0 + t (a1 + t a2)), h' = x + x tanh(u).
+__device__ __forceinline__ f2 gelu2_acc2(f2 x) {
+  float t0, t1;
+  f2_split(fmul2(x, x), t0, t1);
+  const f2 t = f2_make(fminf(t0, 16.0f), fminf(t1, 16.0f));
+  const f2 p = ffma2(t, ffma2(t, f2_make(kGA2, kGA2), f2_make(kGA1, kGA1)), f2_make(kGA0, kGA0));
+  float u0, u1;
+  f2_split(fmul2(x, p), u0, u1);
+  return ffma2(x, f2_make(tanh_approx(u0), tanh_approx(u1)), x);
+}
+
 // FMA-pipe form of h' = 2 GELU(x) for pairs feeding a 16-bit MMA (MFP_POLY_EVERY
 // builds): x (1 + S(x)), S(x) ~ x_c P(x_c^2), x_c = clamp(x, -3.4, 3.4), degree-5
 // minimax fit with S(3.4) = 1 (tools/fit_gelu_poly.py --n 5 --a 3.4): |dh'| <= 2.3e-3,
@@ -97,16 +109,18 @@ __device__ __forceinline__ f2 gelu2_poly(f2 x) {
 template <int GELU>
 __device__ __forceinline__ float act_head(float x) {
   if constexpr (GELU == 1) return gelu2_fast(x);
+  else if constexpr (GELU == 2) return gelu2_acc(x);
   else return gelu_erf(x);
 }
 // Last layer + head on one 32-column TMEM chunk: acc += wo . act(x), the fast
 // form in packed fp32x2; the erf form scalar.
 template <int GELU, int N = 32>
 __device__ __forceinline__ void head32(const uint32_t (&r)[N], const float* wo, f2& acc) {
-  if constexpr (GELU == 1) {
+  if constexpr (GELU >= 1) {
 #pragma unroll
     for (int e = 0; e < N / 2; e++) {
-      const f2 h = gelu2_mufu(f2_make(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])));
+      const f2 x = f2_make(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+      const f2 h = GELU == 2 ? gelu2_acc2(x) : gelu2_mufu(x);
       const float2 w = *reinterpret_cast<const float2*>(wo + 2 * e);
       acc = ffma2(f2_make(w.x, w.y), h, acc);
     }
@@ -129,7 +143,9 @@ __device__ __forceinline__ void act8(const float (&v)[8], uint32_t (&w)[4]) {
 #pragma unroll
   for (int e = 0; e < 4; e++) {
     float h0, h1;
-    if constexpr (GELU == 1) {
+    if constexpr (GELU == 2) {
+      f2_split(gelu2_acc2(f2_make(v[2 * e], v[2 * e + 1])), h0, h1);
+    } else if constexpr (GELU == 1) {
 #ifdef MFP_POLY_EVERY
       if (e % MFP_POLY_EVERY == MFP_POLY_EVERY - 1)
         f2_split(gelu2_poly(f2_make(v[2 * e], v[2 * e + 1])), h0, h1);
@@ -275,7 +291,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       for (int i = threadIdx.x; i < kHalf / 16; i += kThreads2) dst[i] = __ldg(src + i);
     }
     for (int i = threadIdx.x; i < kD; i += kThreads2) {
-      S.wo[i] = (GELU == 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
+      S.wo[i] = (GELU >= 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
       S.w2[i] = __ldg(net.W2 + 2 * i);
       S.w2[kD + i] = __ldg(net.W2 + 2 * i + 1);
     }
@@ -621,7 +637,7 @@ k_chain_tc2w(const float* __restrict__ z, int64_t total_rows, int q, DevNet net,
     for (int i = threadIdx.x; i < kBiasB / 16; i += kThreads) dst[i] = __ldg(src + i);
   }
   for (int i = threadIdx.x; i < D; i += kThreads) {
-    S.wo[i] = (GELU == 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
+    S.wo[i] = (GELU >= 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
     S.w2[i] = __ldg(net.W2 + 2 * i);
     S.w2[D + i] = __ldg(net.W2 + 2 * i + 1);
   }
@@ -888,6 +904,320 @@ k_chain_tc2w(const float* __restrict__ z, int64_t total_rows, int q, DevNet net,
 
 }  // namespace tc2w
 
+// ---------------------------------------------------------------------------
+// MFP_FP16X, the accuracy mode (d = 128): every activation feeding an MMA is
+// split h' = h_hi + h_lo into two fp16 operands (h_lo = RN(h' - h_hi), so the
+// pair carries ~22 bits), and each layer accumulates A_hi W + A_lo W (16 K-steps
+// against the SAME resident fp16 weight half-images) + the bias step: only the
+// weights are rounded.  Emulated on trained weights: 4.6e-4 of
+// max|y| with an accurate GELU vs 2.3e-3 (fp16) / 1.5e-2 (bf16) for the single-
+// rounding modes.  The split doubles the A footprint (64 KB per slot), so two
+// tile slots x 8 epilogue warps per CTA: thread = (row, 64-column half), TMEM
+// 2 x 128 columns; the head's two partial dots meet in shared memory as in
+// tc2w.  Costs ~2x the MMA work (the d = 128 tensor pipe is ~70 % idle) and four
+// more epilogue instructions per element pair.
+namespace tc2s {
+using namespace tc;
+using tc2::cluster_rank;
+using tc2::cluster_sync;
+using tc2::commit2;
+using tc2::mbar_arrive_remote;
+using tc2::mma2;
+
+constexpr int kSlots = 2;
+constexpr int kEpiWarps = 16;
+constexpr int kAllocWarp = 16, kIssueWarp = 17;
+constexpr int kThreads = 32 * (kEpiWarps + 2);   // 576
+constexpr int kHalfB = kWImg;                    // bytes of one CTA's half image per layer (18 KB)
+constexpr int kAs = 2 * kTile;                   // 64 KB per slot: A_hi (32 KB) then A_lo
+
+struct SmemS {
+  uint8_t* A;      // [2][hi 32 KB | lo 32 KB]
+  uint8_t* W;      // [nh][18 KB]
+  uint8_t* ones;   // 4 KB
+  float* zbuf;     // [2 slots][4 subdomains][128]: z + (W2[:,0] + W2[:,1]) / 2
+  float* w2;       // [2][128]
+  float* wo;       // [128]
+  float* hpart;    // [2][128]
+  uint64_t* bars;  // a_full[2] d_full[2]
+  uint32_t* tmem_slot;
+};
+__device__ __forceinline__ SmemS carve_s(uint8_t* raw) {
+  SmemS s;
+  s.A = raw;
+  s.W = s.A + kSlots * kAs;
+  s.ones = s.W + kMaxHidden * kHalfB;
+  s.zbuf = (float*)(s.ones + kOnes);
+  s.w2 = s.zbuf + kSlots * kZRows * kD;
+  s.wo = s.w2 + 2 * kD;
+  s.hpart = s.wo + kD;
+  s.bars = (uint64_t*)(s.hpart + kSlots * kRows);
+  s.tmem_slot = (uint32_t*)(s.bars + 2 * kSlots);
+  return s;
+}
+constexpr size_t smem_bytes_s() {
+  return (size_t)kSlots * kAs + kMaxHidden * kHalfB + kOnes +
+         4 * ((size_t)kSlots * kZRows * kD + 3 * kD + kSlots * kRows) + 16 * kSlots + 16;
+}
+
+__device__ __forceinline__ void unpack_f16x2(uint32_t w, float& f0, float& f1) {
+  asm("{\n\t.reg .f16 a, b;\n\tmov.b32 {a, b}, %2;\n\tcvt.f32.f16 %0, a;\n\tcvt.f32.f16 %1, b;\n\t}"
+      : "=f"(f0), "=f"(f1)
+      : "r"(w));
+}
+// 8 pre-activations -> h' = 2 GELU as hi / lo fp16 words (h' = hi + lo to ~2^-22)
+template <int GELU>
+__device__ __forceinline__ void act8_split(const float (&v)[8], uint32_t (&hi)[4], uint32_t (&lo)[4]) {
+#pragma unroll
+  for (int e = 0; e < 4; e++) {
+    float h0, h1;
+    if constexpr (GELU == 2) f2_split(gelu2_acc2(f2_make(v[2 * e], v[2 * e + 1])), h0, h1);
+    else if constexpr (GELU == 1) f2_split(gelu2_mufu(f2_make(v[2 * e], v[2 * e + 1])), h0, h1);
+    else { h0 = 2.f * gelu_erf(v[2 * e]); h1 = 2.f * gelu_erf(v[2 * e + 1]); }
+    hi[e] = pack2_rn<1>(h0, h1);
+    float f0, f1;
+    unpack_f16x2(hi[e], f0, f1);
+    float r0, r1;
+    f2_split(fadd2(f2_make(h0, h1), f2_make(-f0, -f1)), r0, r1);
+    lo[e] = pack2_rn<1>(r0, r1);
+  }
+}
+
+template <int GELU>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+k_chain_tc2s(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, Sink sink) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int nh = net.n_hidden;
+  const SmemS S = carve_s(smem_raw);
+  uint64_t* a_full = S.bars;
+  uint64_t* d_full = S.bars + kSlots;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  for (int l = 0; l < nh; l++) {
+    const uint4* src =
+        reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(net.Wh_sw2) + (size_t)l * 2 * kHalfB + rank * kHalfB);
+    uint4* dst = reinterpret_cast<uint4*>(S.W + l * kHalfB);
+    for (int i = threadIdx.x; i < kHalfB / 16; i += kThreads) dst[i] = __ldg(src + i);
+  }
+  for (int i = threadIdx.x; i < kD; i += kThreads) {
+    S.wo[i] = (GELU >= 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
+    S.w2[i] = __ldg(net.W2 + 2 * i);
+    S.w2[kD + i] = __ldg(net.W2 + 2 * i + 1);
+  }
+  if (threadIdx.x < kRows) {
+    const uint32_t one = 0x3C00u;
+    const int r = threadIdx.x;
+    *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + (r & 7) * 16) = make_uint4(one | (one << 16), 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(S.ones + (r >> 3) * 256 + 128 + (r & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSlots; s++) {
+      mbar_init(&a_full[s], 16);   // 8 warps x 2 CTAs (elected lanes)
+      mbar_init(&d_full[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kAllocWarp) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
+                 "r"(256)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *S.tmem_slot;
+  pdl_launch_dependents();
+  pdl_wait();
+
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int64_t ntiles = (total_rows + 2 * kRows - 1) / (2 * kRows);
+  const int64_t nloc = ntiles > cid ? (ntiles - cid + ncl - 1) / ncl : 0;
+  const int64_t nsub = total_rows / q;
+
+  if (warp == kIssueWarp) {
+    if (rank == 0 && lane == 0) {
+      uint32_t pa[kSlots] = {0u, 0u};
+      const uint32_t ones_addr = smem_u32(S.ones);
+      for (int64_t j0 = 0; j0 < nloc; j0 += kSlots)
+        for (int l = 0; l < nh; l++)
+          for (int s = 0; s < kSlots; s++) {
+            if (j0 + s >= nloc) continue;
+            mbar_wait(&a_full[s], pa[s]);
+            pa[s] ^= 1u;
+            tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)(s * kD);
+            const uint32_t ah = smem_u32(S.A + s * kAs), al = ah + (uint32_t)kTile, b0 = smem_u32(S.W + l * kHalfB);
+#pragma unroll
+            for (int k = 0; k < kD / 16; k++) {
+              const uint32_t offa = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
+              const uint32_t offb = (uint32_t)((k >> 2) * 8192 + (k & 3) * 32);
+              mma2<1>(d, sw128_desc(ah + offa), sw128_desc(b0 + offb), k > 0 ? 1u : 0u);
+            }
+#pragma unroll
+            for (int k = 0; k < kD / 16; k++) {
+              const uint32_t offa = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
+              const uint32_t offb = (uint32_t)((k >> 2) * 8192 + (k & 3) * 32);
+              mma2<1>(d, sw128_desc(al + offa), sw128_desc(b0 + offb), 1u);
+            }
+            mma2<1>(d, nosw_desc(ones_addr), nosw_desc(b0 + 16384u), 1u);   // bias step
+            commit2(&d_full[s]);
+          }
+    }
+    __syncwarp();
+  } else if (warp < kEpiWarps) {
+    const int slot = warp >> 3;
+    const int ch = (warp >> 2) & 1;
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const int tis = (warp & 7) * 32 + lane;
+    const uint32_t a_row = smem_u32(S.A + slot * kAs) + (uint32_t)row * 128u + ((uint32_t)ch << 14);
+    const int r7 = row & 7;
+    uint32_t a_sw[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) a_sw[j] = a_row + ((uint32_t)(j ^ r7) << 4);
+    const uint32_t t_row = tmem + (uint32_t)(slot * kD + ch * 64) + ((uint32_t)(quad * 32) << 16);
+    float* zb = S.zbuf + slot * kZRows * kD;
+    const float bo = __ldg(net.bo);
+    const int zi = 2 * tis, zr_ = zi >> 7, zc = zi & (kD - 1);
+    auto row0_of = [&](int64_t j) -> int64_t { return (cid + j * ncl) * (2 * kRows) + rank * kRows; };
+    auto z_fetch = [&](int64_t j) -> float2 {
+      int64_t sidx = row0_of(j) / q + zr_;
+      if (sidx > nsub - 1) sidx = nsub - 1;
+      return __ldg(reinterpret_cast<const float2*>(z + sidx * kD + zc));
+    };
+    auto z_stage = [&](const float2 v) {
+      *reinterpret_cast<float2*>(zb + zi) = make_float2(fmaf(0.5f, S.w2[zc] + S.w2[kD + zc], v.x),
+                                                        fmaf(0.5f, S.w2[zc + 1] + S.w2[kD + zc + 1], v.y));
+    };
+    auto arrive_a = [&]() {
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&a_full[slot], 0u);
+    };
+    auto store8 = [&](int g, const uint32_t (&hi)[4], const uint32_t (&lo)[4]) {
+      st_shared_v4(a_sw[g], hi[0], hi[1], hi[2], hi[3]);
+      st_shared_v4(a_sw[g] + (uint32_t)kTile, lo[0], lo[1], lo[2], lo[3]);
+    };
+    if (slot < nloc) z_stage(z_fetch(slot));
+    uint32_t pd = 0u;
+    for (int64_t j = slot; j < nloc; j += kSlots) {
+      const int64_t row0 = row0_of(j);
+      int64_t s_first = row0 / q;
+      if (s_first > nsub - 1) s_first = nsub - 1;
+      named_sync(1 + slot, 256);
+      const bool have_next = j + kSlots < nloc;
+      float2 znext = make_float2(0.f, 0.f);
+      if (have_next) znext = z_fetch(j + kSlots);
+      const int64_t grow = row0 + row;
+      const bool valid = grow < total_rows;
+      const int64_t gr = valid ? grow : total_rows - 1;
+      const int64_t sidx = gr / q;
+      const int p = (int)(gr - sidx * q);
+      float qx, qy;
+      query_xy(q, p, &qx, &qy);
+      int zo = (int)(sidx - s_first);
+      if (zo < 0 || zo >= kZRows) zo = 0;
+      // ---- split layer (Eq. 5) over this thread's 64 columns (K-atom ch)
+      const bool centre = (q == kQC);
+      const bool vert = p < kM - 1;
+      const float* zs = zb + zo * kD + ch * 64;
+      const float* w1s = S.w2 + ((centre && vert) ? kD : 0) + ch * 64;
+      const float q1 = (centre && vert) ? qy - 0.5f : qx - 0.5f;
+#pragma unroll
+      for (int j16 = 0; j16 < 4; j16++) {
+        const int c0 = 16 * j16;
+        float v[16];
+        const f2 Q1 = f2_make(q1, q1);
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const float4 zz = *reinterpret_cast<const float4*>(zs + c0 + 4 * i);
+          const float4 aa = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
+          f2 v01 = ffma2(f2_make(aa.x, aa.y), Q1, f2_make(zz.x, zz.y));
+          f2 v23 = ffma2(f2_make(aa.z, aa.w), Q1, f2_make(zz.z, zz.w));
+          if (!centre) {
+            const float4 bb = *reinterpret_cast<const float4*>(S.w2 + kD + ch * 64 + c0 + 4 * i);
+            const f2 QY = f2_make(qy - 0.5f, qy - 0.5f);
+            v01 = ffma2(f2_make(bb.x, bb.y), QY, v01);
+            v23 = ffma2(f2_make(bb.z, bb.w), QY, v23);
+          }
+          f2_split(v01, v[4 * i], v[4 * i + 1]);
+          f2_split(v23, v[4 * i + 2], v[4 * i + 3]);
+        }
+        uint32_t hi[4], lo[4];
+        act8_split<GELU>(*reinterpret_cast<const float(*)[8]>(v), hi, lo);
+        store8(2 * j16, hi, lo);
+        act8_split<GELU>(*reinterpret_cast<const float(*)[8]>(v + 8), hi, lo);
+        store8(2 * j16 + 1, hi, lo);
+      }
+      fence_proxy_async();
+      arrive_a();
+      // ---- hidden layers (a4) and head (a5)
+      f2 yacc = f2_make(0.f, 0.f);
+      for (int l = 0; l < nh; l++) {
+        mbar_wait(&d_full[slot], pd);
+        pd ^= 1u;
+        tc_fence_after();
+        auto layer_epi = [&](auto last_tag) {
+          constexpr bool LAST = decltype(last_tag)::value;
+          auto work16 = [&](const uint32_t (&r)[16], int c16) {
+            if constexpr (!LAST) {
+#pragma unroll
+              for (int c8 = 0; c8 < 2; c8++) {
+                float v[8];
+#pragma unroll
+                for (int e = 0; e < 8; e++) v[e] = __uint_as_float(r[c8 * 8 + e]);
+                uint32_t hi[4], lo[4];
+                act8_split<GELU>(v, hi, lo);
+                store8(2 * c16 + c8, hi, lo);
+              }
+            } else {
+              head32<GELU, 16>(r, S.wo + ch * 64 + c16 * 16, yacc);
+            }
+          };
+          uint32_t ra[16], rb[16];
+          tmem_ld16(t_row, ra);
+          tmem_wait_ld_dep16(ra);
+#pragma unroll
+          for (int c16 = 0; c16 < 4; c16 += 2) {
+            tmem_ld16(t_row + (uint32_t)((c16 + 1) * 16), rb);
+            work16(ra, c16);
+            tmem_wait_ld_dep16(rb);
+            if (c16 + 2 < 4) tmem_ld16(t_row + (uint32_t)((c16 + 2) * 16), ra);
+            work16(rb, c16 + 1);
+            if (c16 + 2 < 4) tmem_wait_ld_dep16(ra);
+          }
+        };
+        const bool last = (l == nh - 1);
+        if (last) layer_epi(std::true_type{});
+        else layer_epi(std::false_type{});
+        tc_fence_before();
+        if (!last) {
+          fence_proxy_async();
+          arrive_a();
+        }
+      }
+      float y0, y1;
+      f2_split(yacc, y0, y1);
+      if (ch == 1) S.hpart[slot * kRows + row] = y0 + y1;
+      named_sync(1 + slot, 256);
+      if (have_next) z_stage(znext);
+      if (ch == 0 && valid) sink_store(sink, sidx, p, ((y0 + y1) + S.hpart[slot * kRows + row]) + bo);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == kAllocWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
+  }
+}
+
+}  // namespace tc2s
+
 bool chain_tc_available() { return true; }
 
 #ifdef MFP_TRACE
@@ -904,11 +1234,19 @@ void tc_kernel_attributes() {
   cudaFuncSetAttribute(tc2::k_chain_tc2<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
   cudaFuncSetAttribute(tc2::k_chain_tc2<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
   cudaFuncSetAttribute(tc2::k_chain_tc2<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  cudaFuncSetAttribute(tc2::k_chain_tc2<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2);
+  const int mxs = (int)tc2s::smem_bytes_s();
+  cudaFuncSetAttribute(tc2s::k_chain_tc2s<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxs);
+  cudaFuncSetAttribute(tc2s::k_chain_tc2s<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxs);
+  cudaFuncSetAttribute(tc2s::k_chain_tc2s<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxs);
   const int mxw = (int)tc2w::smem_bytes_w();
   cudaFuncSetAttribute(tc2w::k_chain_tc2w<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxw);
   cudaFuncSetAttribute(tc2w::k_chain_tc2w<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxw);
   cudaFuncSetAttribute(tc2w::k_chain_tc2w<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxw);
   cudaFuncSetAttribute(tc2w::k_chain_tc2w<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxw);
+  cudaFuncSetAttribute(tc2w::k_chain_tc2w<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxw);
+  cudaFuncSetAttribute(tc2w::k_chain_tc2w<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxw);
 }
 
 // Persistent grid: one CTA pair per TPC (74 clusters), or fewer for small batches.
@@ -916,7 +1254,8 @@ void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const 
                      cudaStream_t s) {
   if (B <= 0) return;
   const int64_t rows = B * q;
-  const size_t sm = net.d == kD2 ? tc2w::smem_bytes_w() : tc2::smem_bytes2(net.n_hidden);
+  const size_t sm = net.split ? tc2s::smem_bytes_s()
+                  : net.d == kD2 ? tc2w::smem_bytes_w() : tc2::smem_bytes2(net.n_hidden);
   const int64_t ptiles = (rows + 2 * tc::kRows - 1) / (2 * tc::kRows);
   int64_t pairs = num_sms / 2;
   // MFP_MAX_PAIRS=n (sanitizer runs only): cap the persistent grid so a small
@@ -924,15 +1263,21 @@ void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const 
   static const int max_pairs = getenv("MFP_MAX_PAIRS") ? atoi(getenv("MFP_MAX_PAIRS")) : 0;
   if (max_pairs > 0 && pairs > max_pairs) pairs = max_pairs;
   const int grid = 2 * (int)(ptiles < pairs ? ptiles : pairs);
+  if (net.split) {   // MFP_FP16X (fp16 operands, d = 128)
+    if (net.gelu_tanh == 2) launch_pdl(tc2s::k_chain_tc2s<2>, grid, tc2s::kThreads, sm, s, z, rows, q, net, sink);
+    else if (net.gelu_tanh == 1) launch_pdl(tc2s::k_chain_tc2s<1>, grid, tc2s::kThreads, sm, s, z, rows, q, net, sink);
+    else launch_pdl(tc2s::k_chain_tc2s<0>, grid, tc2s::kThreads, sm, s, z, rows, q, net, sink);
+    return;
+  }
 #define MFP_TC2(G, F)                                                                              \
   do {                                                                                             \
     if (net.d == kD2) launch_pdl(tc2w::k_chain_tc2w<G, F>, grid, tc2w::kThreads, sm, s, z, rows, q, net, sink); \
     else launch_pdl(tc2::k_chain_tc2<G, F>, grid, tc2::kThreads2, sm, s, z, rows, q, net, sink);   \
   } while (0)
   if (net.f16) {
-    if (net.gelu_tanh) MFP_TC2(1, 1); else MFP_TC2(0, 1);
+    if (net.gelu_tanh == 2) MFP_TC2(2, 1); else if (net.gelu_tanh) MFP_TC2(1, 1); else MFP_TC2(0, 1);
   } else {
-    if (net.gelu_tanh) MFP_TC2(1, 0); else MFP_TC2(0, 0);
+    if (net.gelu_tanh == 2) MFP_TC2(2, 0); else if (net.gelu_tanh) MFP_TC2(1, 0); else MFP_TC2(0, 0);
   }
 #undef MFP_TC2
 }

@@ -115,6 +115,7 @@ struct DevNet {
   int n_hidden;
   int gelu_tanh;
   int f16;               // tensor-core operands fp16 (1) or bf16 (0)
+  int split;             // MFP_FP16X: activations split h_hi + h_lo (two MMAs per K step)
   // bf16 tables (tcgen05 path): weights pre-swizzled into the SW128 K-major image
   const uint16_t* Wh_sw2; // d = 128: [n_hidden][2][18 KB half] (CTA-pair chain: rows 64h..64h+63)
                           // d = 256: [n_hidden][2 CTAs][4 chunks x 16 KB + 4 KB bias] (kW2Cta)

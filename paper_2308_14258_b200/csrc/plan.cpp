@@ -32,7 +32,7 @@ mfp_status validate_config(const mfp_config* c, std::string* err) {
     *err = "processor grid does not divide the atomic-subdomain grid (S:75)";
     return MFP_ERR_NOT_TILEABLE;
   }
-  if (c->precision < MFP_FP32 || c->precision > MFP_FP16) { *err = "bad precision"; return MFP_ERR_INVALID; }
+  if (c->precision < MFP_FP32 || c->precision > MFP_FP16X) { *err = "bad precision"; return MFP_ERR_INVALID; }
   if (c->subsolver != MFP_SDNET && c->subsolver != MFP_EXACT_LAPLACE) { *err = "bad subsolver"; return MFP_ERR_INVALID; }
   if (c->check_every < 1) { *err = "check_every must be >= 1"; return MFP_ERR_INVALID; }
   return MFP_OK;

@@ -23,7 +23,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 ABI_VERSION = 1
 ALL_RANKS = -1
-FP32, BF16, FP16 = 0, 1, 2
+FP32, BF16, FP16, FP16X = 0, 1, 2, 3
 SDNET, EXACT_LAPLACE = 0, 1
 QUERY_CENTRE, QUERY_INTERIOR = 0, 1
 

@@ -50,12 +50,12 @@ def c5_ref():
     return g, w, ref
 
 
-@pytest.mark.parametrize("precision,ce", [(1, 3), (2, 16), (1, 16)])
+@pytest.mark.parametrize("precision,ce", [(1, 3), (2, 16), (1, 16), (3, 3)])
 def test_c5_whole_field(lib, c5_ref, precision, ce):
     nx = ny = 4096
     g, w, ref = c5_ref
     cfg = lib.make_config(nx, ny, (1, 1), precision=precision, subsolver=lib.SDNET, check_every=ce)
-    m = lib.Mfp(cfg, lib.make_net(gelu=1), w)
+    m = lib.Mfp(cfg, lib.make_net(gelu=2 if precision == 3 else 1), w)
     u, rep = m.solve(g, 3, 0.0)
     assert rep.iterations == 3 and rep.predictions == 65025 * 3
     L = lattice_to_global(m.lines(), nx, ny)
@@ -72,7 +72,7 @@ def test_c5_whole_field(lib, c5_ref, precision, ce):
     e_inner = float(np.max(np.abs(u.astype(np.float64) - ref.u)[inner]) / np.max(np.abs(ref.u)))
     print(f"  interior (final phase) {e_inner:.2e}")
     assert e_inner <= TOL
-    if precision == 2:
+    if precision in (2, 3):
         # fp16 operands hold the bar even against the interior's own scale
         # (bf16 does not: the W-rand head cancels to ~1% of its terms)
         assert rel_err(u, ref.u, inner) <= TOL

@@ -295,11 +295,13 @@ WFIT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
 # for fp16 on one prediction batch; the field after 10 MFP iterations (interior
 # predictions of the final phase included) is held to 2x the measured 4.0e-3,
 # bf16 to 2x its emulated 1.4e-2.
-WFIT_TOL = {0: (FP32_TOL, FP32_TOL), 1: (3e-2, 3e-2), 2: (BF16_TOL, 8e-3)}
+# The accuracy mode MFP_FP16X (split fp16 activations, accurate GELU, precision 3)
+# holds the north_star bar itself: 3e-3 per batch and per field.
+WFIT_TOL = {0: (FP32_TOL, FP32_TOL), 1: (3e-2, 3e-2), 2: (BF16_TOL, 8e-3), 3: (BF16_TOL, BF16_TOL)}
 
 
 @pytest.mark.skipif(not os.path.exists(WFIT), reason="fitted weights not generated (tools/fit_sdnet.py)")
-@pytest.mark.parametrize("precision", [0, 1, 2])
+@pytest.mark.parametrize("precision", [0, 1, 2, 3])
 def test_fitted_weights_parity(lib, precision):
     """W-fit (tools/fit_sdnet.py): outputs are O(1) harmonic-extension values, so
     every precision is held to its bound relative to the output itself."""
@@ -308,7 +310,7 @@ def test_fitted_weights_parity(lib, precision):
     w = np.load(WFIT)
     nx = ny = 128
     cfg = lib.make_config(nx, ny, precision=precision, subsolver=lib.SDNET, check_every=1)
-    m = lib.Mfp(cfg, lib.make_net(gelu=1 if precision else 0), w)
+    m = lib.Mfp(cfg, lib.make_net(gelu={0: 0, 1: 1, 2: 1, 3: 2}[precision]), w)
     gb = random_boundaries(500, seed=13)
     out = m.sdnet_batch(torch.from_numpy(gb).cuda(), 0).cpu().numpy()
     ref = oracle.sdnet_forward(w.astype(np.float64), gb.astype(np.float64), oracle.writeset(0, 0)[1])

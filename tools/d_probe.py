@@ -20,10 +20,10 @@ pk = json.load(open(os.path.join(root, "MEASURED_PEAKS.json"))) if os.path.exist
 peak = pk.get("bf16_tflops_sustained", 1400.0)
 nx = ny = 4096
 g = gp_boundary(nx, ny, 0)
-for d in (128, 256):
+for d in ((128,) if prec == 3 else (128, 256)):
     w = random_weights(0, d=d)
     m = mfp.Mfp(mfp.make_config(nx, ny, precision=prec, subsolver=mfp.SDNET, check_every=16),
-                mfp.make_net(d=d, gelu=1), w)
+                mfp.make_net(d=d, gelu=2 if prec == 3 else 1), w)
     m.solve(g, 2, 0.0)
     m.profile(2)
     p = m.profile(iters)
