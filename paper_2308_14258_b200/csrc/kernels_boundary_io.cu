@@ -51,7 +51,7 @@ k_gather_phase(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __r
 // one shared-memory step).  blockmax[blockIdx.x] = that maximum (fp32 bits) and
 // bit 31 of blockflag set on a non-finite prediction.  Cells of one phase are
 // written by exactly one subdomain, so the result is order independent.
-__global__ void __launch_bounds__(kIoWarps * 32, 4)
+__global__ void __launch_bounds__(kIoWarps * 32, 5)
 k_scatter_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ anchors, int64_t B,
                 const float* __restrict__ pred, unsigned int* __restrict__ blockmax) {
   __shared__ float red[kIoWarps];
@@ -66,9 +66,10 @@ k_scatter_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restri
   // kIoUnroll subdomains per warp per round: every load of the round (predictions
   // and old values) is issued before the first store, so a warp keeps
   // 4 x ~0.5 KB in flight instead of one dependent load/store pair at a time.
+  // Cell indices are 32-bit (a rank's lattice holds < 2^31 cells; checked at
+  // launch), which keeps the kernel at <= 48 registers: 5 resident blocks per SM.
   for (int64_t s0 = ((int64_t)blockIdx.x * kIoWarps + warp) * kIoUnroll; s0 < B; s0 += nw * kIoUnroll) {
-    int64_t c0[kIoUnroll], c1[kIoUnroll];
-    int32_t dupo[kIoUnroll];   // centre copy, as an offset from c0 (-1: none)
+    int32_t c0[kIoUnroll], c1[kIoUnroll], cd[kIoUnroll];   // cd: the centre's second copy or -1
     float y0[kIoUnroll], y1[kIoUnroll], o0[kIoUnroll], o1[kIoUnroll];
 #pragma unroll
     for (int u = 0; u < kIoUnroll; u++) {
@@ -76,9 +77,9 @@ k_scatter_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restri
       int a, b;
       unpack_anchor(__ldg(anchors + s), a, b);
       int64_t d0c, d1;
-      c0[u] = centre_cell(a, b, lane, L.strideH, L.strideV, L.offV, &d0c);
-      dupo[u] = d0c >= 0 ? (int32_t)(d0c - c0[u] + (int64_t)0x40000000) : -1;
-      c1[u] = two ? centre_cell(a, b, lane + 32, L.strideH, L.strideV, L.offV, &d1) : c0[u];
+      c0[u] = (int32_t)centre_cell(a, b, lane, L.strideH, L.strideV, L.offV, &d0c);
+      cd[u] = (int32_t)d0c;
+      c1[u] = two ? (int32_t)centre_cell(a, b, lane + 32, L.strideH, L.strideV, L.offV, &d1) : c0[u];
       y0[u] = __ldcs(pred + s * kQC + lane);
       y1[u] = two ? __ldcs(pred + s * kQC + lane + 32) : y0[u];
     }
@@ -98,7 +99,7 @@ k_scatter_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restri
     for (int u = 0; u < kIoUnroll; u++) {
       if (s0 + u >= B) continue;
       lat[c0[u]] = y0[u];
-      if (dupo[u] >= 0) lat[c0[u] + ((int64_t)dupo[u] - 0x40000000)] = y0[u];
+      if (cd[u] >= 0) lat[cd[u]] = y0[u];
       if (two) lat[c1[u]] = y1[u];
     }
   }
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(1024) k_reduce_max(const unsigned int* __restr
   }
 }
 
-// Grid: a multiple of the SM count (8 warps per block, 8 blocks per SM).
+// Grid: a multiple of the SM count (8 warps per block, up to 8 blocks per SM).
 static int io_blocks(int64_t units, int per_block) {
   int64_t b = (units + per_block - 1) / per_block;
   const int64_t cap = (int64_t)(num_sms() < kMaxSMs ? num_sms() : kMaxSMs) * 8;
@@ -163,6 +164,7 @@ void launch_gather_phase(const float* lat, const LatticeGeom& L, const uint32_t*
 void launch_scatter_phase(float* lat, const LatticeGeom& L, const uint32_t* anchors, int64_t B, const float* pred,
                           unsigned int* blockmax, unsigned int* out, cudaStream_t s) {
   const int nb = scatter_grid(B);
+  if (L.cells >= ((int64_t)1 << 31)) __builtin_trap();   // 32-bit cell indices (never at 16385^2: 3.4e7 cells)
   if (B > 0) k_scatter_phase<<<nb, kIoWarps * 32, 0, s>>>(lat, L, anchors, B, pred, blockmax);
   else cudaMemsetAsync(blockmax, 0, sizeof(unsigned int) * nb, s);
   k_reduce_max<<<1, 1024, 0, s>>>(blockmax, nb, out);

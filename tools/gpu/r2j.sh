@@ -1,0 +1,3 @@
+python paper_2308_14258_b200/build.py > /dev/null 2>&1
+for u in 4 8; do echo "unroll $u"; MFP_IO_UNROLL=$u timeout 300 python tools/bench_io.py 10 | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print(d['gather']['us'], d['gather']['frac'], d['scatter']['us'], d['scatter']['frac'])"; done
+timeout 600 python -m pytest tests/test_gpu_boundary_io.py -q 2>&1 | tail -2
