@@ -79,6 +79,10 @@ struct mfp_ctx {
   bool p2p = false;                    // halo transport: peer-memory kernels (NEXT-2) instead of NCCL / copies
   std::vector<void*> p2p_opened;       // IPC-mapped peer regions (multi-process)
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // [0] plain block, [1] block ending in a check
+  cudaGraphExec_t gloop = nullptr;     // WHILE graph: blocks of c iterations + on-device stopping rule
+  int gloop_launches = 0;              // kernels per loop-body block
+  unsigned int* loopst = nullptr;      // device {iterations, t, tol bits, blocks}
+  unsigned int* hloop = nullptr;       // pinned host mirror
   int glaunches[2] = {0, 0};
   std::vector<RankState> ranks;
   DevNet dn{};
@@ -286,6 +290,7 @@ void carve(mfp_ctx* c, void* base, size_t* total) {
   dn.HfT = cv.take<float>((size_t)kNB * kQF);
   c->gstage = cv.take<float>((size_t)2 * (c->cfg.nx + c->cfg.ny));
   c->delta = cv.take<unsigned int>(4);
+  c->loopst = cv.take<unsigned int>(4);
   c->iomax = cv.take<unsigned int>(kMaxSMs * 8);   // >= scatter_grid(B) for any B
   c->ioout = cv.take<unsigned int>(2);
   const bool need_full = (c->rank == MFP_ALL_RANKS || c->rank == 0);
@@ -512,7 +517,7 @@ mfp_status iterate(mfp_ctx* c, bool exchange = true) {
 
 // delta_k (reading G5) -> host, max over ranks; returns nonfinite flag
 // Enqueue the delta reduction (no host sync: capturable into a graph).
-mfp_status enqueue_delta(mfp_ctx* c) {
+mfp_status enqueue_delta(mfp_ctx* c, bool to_host = true) {
   CK(cudaMemsetAsync(c->delta, 0, 2 * sizeof(unsigned int), c->stream));
   {
     SpanGuard g(c, kKindDelta, 0);
@@ -522,7 +527,7 @@ mfp_status enqueue_delta(mfp_ctx* c) {
     }
   }
   if (c->comm) NK(ncclAllReduce(c->delta, c->delta, 2, ncclUint32, ncclMax, c->comm, c->stream));
-  CK(cudaMemcpyAsync(c->hdelta, c->delta, 2 * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
+  if (to_host) CK(cudaMemcpyAsync(c->hdelta, c->delta, 2 * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
   return MFP_OK;
 }
 
@@ -575,6 +580,76 @@ mfp_status run_block(mfp_ctx* c, int kind) {
   }
   CK(cudaGraphLaunch(c->gexec[kind], c->stream));
   c->launches += c->glaunches[kind];
+  return MFP_OK;
+}
+
+// On-device convergence loop: ONE graph launch runs blocks of
+// c iterations until delta <= tol, a non-finite prediction, or no whole block
+// fits into t — a CUDA graph WHILE node whose body is the check block (c
+// iterations, snapshot, delta) followed by k_loop_ctl, which sets the node's
+// condition on the device.  The host reads the loop state once at the end.
+// Used for single-process contexts (R == 1 or MFP_ALL_RANKS); with an NCCL
+// communicator the host checks every c iterations (NCCL kernels inside a
+// conditional body are not validated on a one-GPU box).  MFP_NO_DEVICE_LOOP=1
+// disables it (A/B).
+bool device_loop_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MFP_NO_DEVICE_LOOP");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+mfp_status run_loop(mfp_ctx* c, int it, int t, float tol) {
+  const int ce = c->cfg.check_every;
+  if (!c->gloop) {
+    cudaGraph_t g = nullptr;
+    CK(cudaGraphCreate(&g, 0));
+    struct G { cudaGraph_t g; ~G() { if (g) cudaGraphDestroy(g); } } guard{g};
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, g, 1u, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    const int l0 = c->launches;
+    CK(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    mfp_status st = MFP_OK;
+    for (int i = 0; i < ce && st == MFP_OK; i++) {
+      if (i == ce - 1)
+        for (auto& rs : c->ranks)
+          cudaMemcpyAsync(rs.snap, rs.lat, rs.plan.lat.cells * sizeof(float), cudaMemcpyDeviceToDevice, c->stream);
+      st = iterate(c, (i + 1) % c->exchange_every == 0);
+    }
+    if (st == MFP_OK) st = exchange_wait(c);
+    if (st == MFP_OK) st = enqueue_delta(c, false);
+    if (st == MFP_OK) {
+      launch_loop_ctl(h, c->delta, c->loopst, ce, c->stream);
+      c->launches++;
+    }
+    cudaGraph_t out = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &out);
+    if (st != MFP_OK) return st;
+    if (e != cudaSuccess) return fail(c, MFP_ERR_CUDA, std::string("loop capture: ") + cudaGetErrorString(e));
+    const cudaError_t ei = cudaGraphInstantiate(&c->gloop, g, 0);
+    if (ei != cudaSuccess) return fail(c, MFP_ERR_CUDA, std::string("loop instantiate: ") + cudaGetErrorString(ei));
+    c->gloop_launches = c->launches - l0;
+    c->launches = l0;
+  }
+  float tolv = tol;
+  c->hloop[0] = (unsigned int)it;
+  c->hloop[1] = (unsigned int)t;
+  memcpy(&c->hloop[2], &tolv, 4);
+  c->hloop[3] = 0u;
+  CK(cudaMemcpyAsync(c->loopst, c->hloop, 4 * sizeof(unsigned int), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaGraphLaunch(c->gloop, c->stream));
+  CK(cudaMemcpyAsync(c->hloop + 4, c->loopst, 4 * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->hdelta, c->delta, 2 * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
   return MFP_OK;
 }
 
@@ -700,6 +775,18 @@ mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, floa
     // A whole block of c iterations (starting on a block boundary, no exchange
     // in flight) replays one captured CUDA graph: c x (4 phases + exchange),
     // plus the snapshot / delta / allreduce of the check iteration.
+    if (c->use_graphs && !c->comm && tol > 0.f && device_loop_enabled() && it % ce == 0 && t - it >= ce &&
+        !c->pending) {
+      mfp_status st = run_loop(c, it, t, tol);
+      if (st) return st;
+      bool bad = false;
+      if ((st = read_delta(c, &delta, &bad))) return st;   // waits for the loop
+      it = (int)c->hloop[4];
+      c->launches += (int)c->hloop[7] * c->gloop_launches;
+      if (bad) return fail(c, MFP_ERR_NONFINITE, "non-finite prediction (S:345)");
+      if (delta <= tol) { converged = true; break; }
+      continue;   // fewer than c iterations left: the per-iteration path below
+    }
     if (c->use_graphs && it % ce == 0 && t - it >= ce && !c->pending) {
       // every block ends in a check (delta every c iterations, reading G5),
       // also in parity mode (tol == 0), where only the stop is disabled
@@ -898,6 +985,7 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
     return fail(c, MFP_ERR_WORKSPACE, "workspace too small or not 256-byte aligned");
   carve(c, workspace, &need);
   CK(cudaMallocHost(&c->hdelta, 4 * sizeof(unsigned int)));
+  CK(cudaMallocHost(&c->hloop, 8 * sizeof(unsigned int)));
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   // graphs need a capturable (non-legacy) stream; MFP_NO_GRAPHS=1 disables them
   c->use_graphs = c->stream != nullptr && !(getenv("MFP_NO_GRAPHS") && getenv("MFP_NO_GRAPHS")[0] == '1');
@@ -957,6 +1045,8 @@ void mfp_destroy(mfp_ctx* c) {
   if (!c) return;
   for (auto e : c->evpool) cudaEventDestroy(e);
   if (c->hdelta) cudaFreeHost(c->hdelta);
+  if (c->hloop) cudaFreeHost(c->hloop);
+  if (c->gloop) cudaGraphExecDestroy(c->gloop);
   if (c->side) {
     cudaStreamSynchronize(c->side);
     cudaStreamDestroy(c->side);
@@ -1118,6 +1208,7 @@ mfp_status mfp_set_exchange_every(mfp_ctx* c, int32_t s) {
   if (s != c->exchange_every) {
     for (auto& g : c->gexec)
       if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    if (c->gloop) { cudaGraphExecDestroy(c->gloop); c->gloop = nullptr; }
     c->exchange_every = s;
   }
   return MFP_OK;
@@ -1222,6 +1313,7 @@ mfp_status mfp_p2p_open(mfp_ctx* c, const void* handles, int32_t n_handles) {
   }
   for (auto& g : c->gexec)
     if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+  if (c->gloop) { cudaGraphExecDestroy(c->gloop); c->gloop = nullptr; }
   c->p2p = true;
   return MFP_OK;
 }

@@ -221,6 +221,28 @@ void launch_delta(const float* lat, const float* snap, const int64_t* segs, int 
   k_delta<<<blocks, 256, 0, s>>>(lat, snap, segs, nseg, out);
 }
 
+// ------------------------------------------------ a8: on-device stopping rule
+// The body of the solve's WHILE graph (api.cu run_loop) ends with this kernel:
+// after a block of c iterations and its delta, decide on the device whether
+// another block runs (iterate until delta <= eps or t iterations),
+// so a converging solve needs no host round trip per block.
+// st = {iterations done, t, tol bits, blocks run}; delta = {max bits, non-finite}.
+__global__ void k_loop_ctl(cudaGraphConditionalHandle h, const unsigned int* __restrict__ delta,
+                           unsigned int* __restrict__ st, int ce) {
+  const unsigned int it = st[0] + (unsigned int)ce;
+  st[0] = it;
+  st[3] += 1u;
+  const float d = __uint_as_float(delta[0]);
+  const float tol = __uint_as_float(st[2]);
+  const bool stop = delta[1] != 0u || d <= tol || it + (unsigned int)ce > st[1];
+  cudaGraphSetConditional(h, stop ? 0u : 1u);
+}
+
+void launch_loop_ctl(cudaGraphConditionalHandle h, const unsigned int* delta, unsigned int* st, int ce,
+                     cudaStream_t s) {
+  k_loop_ctl<<<1, 1, 0, s>>>(h, delta, st, ce);
+}
+
 // --------------------------------------------------------- N7: halo pack/unpack
 __global__ void k_pack(const float* __restrict__ lat, const int32_t* __restrict__ idx, int64_t n,
                        float* __restrict__ buf) {

@@ -185,6 +185,8 @@ void launch_gather_phase(const float* lat, const LatticeGeom& L, const uint32_t*
 void launch_scatter_phase(float* lat, const LatticeGeom& L, const uint32_t* anchors, int64_t B, const float* pred,
                           unsigned int* blockmax /* scatter_grid(B) */, unsigned int* out /* [2] */,
                           cudaStream_t s);
+void launch_loop_ctl(cudaGraphConditionalHandle h, const unsigned int* delta, unsigned int* st, int ce,
+                     cudaStream_t s);
 void launch_delta(const float* lat, const float* snap, const int64_t* segs, int nseg,
                   unsigned int* out /* [0]=max bits, [1]=nonfinite flag */, cudaStream_t s);
 void launch_pack(const float* lat, const int32_t* idx, int64_t n, float* buf, cudaStream_t s);
