@@ -285,7 +285,7 @@ void carve(mfp_ctx* c, void* base, size_t* total) {
   dn.QTc = cv.take<float>((size_t)d * 64);
   dn.QTf = cv.take<float>((size_t)d * kQF);
   dn.Wh_sw2 = cv.take<uint16_t>(wimg_elems(d, nh));
-  dn.W1img = cv.take<uint16_t>((size_t)2 * kD * kNB);
+  dn.W1img = cv.take<uint16_t>((size_t)2 * d * kNB);   // [d / 128 halves][hi | lo][128 x 128]
   dn.HcT = cv.take<float>((size_t)kNB * 64);
   dn.HfT = cv.take<float>((size_t)kNB * kQF);
   c->gstage = cv.take<float>((size_t)2 * (c->cfg.nx + c->cfg.ny));
@@ -361,8 +361,7 @@ struct SpanGuard {
 // tcgen05 split-bf16 embed (kernels_embed_tc.cu), fp32 the SIMT one.
 void embed(mfp_ctx* c, const float* lat, const LatticeGeom& L, const uint32_t* anchors, const float* gb,
            int64_t B, float* z) {
-  // (the tcgen05 embed holds d = 128 W1 images; d = 256 embeds on the SIMT kernel)
-  if (c->cfg.precision != MFP_FP32 && c->dn.d == kD && embed_tc_enabled())
+  if (c->cfg.precision != MFP_FP32 && embed_tc_enabled())
     launch_embed_tc(lat, L, anchors, gb, B, c->dn, z, c->stream);
   else launch_gather_embed(lat, L, anchors, gb, B, c->dn, z, c->stream);
 }

@@ -36,7 +36,8 @@ constexpr int kThreadsE = 512;           // 16 warps
 constexpr int kImg = kRowsE * kNB * 2;   // 32 KB bf16 image
 constexpr int kPerWarp = kRowsE / 16;
 
-size_t smem_bytes() { return 4 * (size_t)kImg + (size_t)kRowsE * 576 + 4 * (96 + kD) + 8 * 18 + 16; }
+// W1 buffer (hi + lo images of 128 output rows) + A hi / lo + staging + vectors + barriers
+constexpr size_t smem_bytes(int D) { return 4 * (size_t)kImg + (size_t)kRowsE * 576 + 4 * (96 + D) + 8 * 19 + 16; }
 
 // The conv stack of TWO subdomains at once: every value is an fp32 pair
 // (subdomain A, subdomain B) at the same perimeter position, so each weight is
@@ -110,7 +111,12 @@ __device__ __forceinline__ void conv_stack2(const f2 (&g4)[4], int lane, const D
 constexpr int kSlotB = 576;
 constexpr uint32_t kEdgeB = 4 * kM, kEdgeRB = 4 * (kM + 4);
 
-template <int GELU>
+// D = 256: z has two 128-column halves; the W1 buffer holds one half's hi / lo
+// images at a time (the three images would not fit beside the staging), so the
+// MMA issuer runs half A, waits for those MMAs, reloads the buffer with half B
+// by TMA and runs it; the order alternates per round so the half loaded last is
+// reused by the next round's first MMAs.
+template <int GELU, int D>
 __global__ void __launch_bounds__(kThreadsE, 1)
 k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ anchors,
            const float* __restrict__ gb, int64_t B, int rows, DevNet net, float* __restrict__ z) {
@@ -122,11 +128,12 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
   uint8_t* sStage = sAlo + kImg;                         // [128][kSlotB]
   float* sCw = reinterpret_cast<float*>(sStage + kRowsE * kSlotB);   // c1w[40] c1b[8] c2w[40] c2b[1]
   float* sB1 = sCw + 96;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sB1 + kD);   // [0] MMA done, [1] W1 landed,
-  uint64_t* full = bar + 2;                                 // [2..17] warp's perimeters landed
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sB1 + D);   // [0] MMA done, [1] W1 landed, [2] W1 free
+  uint64_t* full = bar + 3;                                // [3..18] warp's perimeters landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full + 16);
+  constexpr int NH = D / 128;                              // W1 halves
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x < kD) sB1[threadIdx.x] = __ldg(net.b1 + threadIdx.x);
+  for (int i = threadIdx.x; i < D; i += kThreadsE) sB1[i] = __ldg(net.b1 + i);
   if (threadIdx.x < 40) sCw[threadIdx.x] = __ldg(net.conv1_w + threadIdx.x);
   if (threadIdx.x < 8) sCw[40 + threadIdx.x] = __ldg(net.conv1_b + threadIdx.x);
   if (threadIdx.x < 40) sCw[48 + threadIdx.x] = __ldg(net.conv2_w + threadIdx.x);
@@ -135,12 +142,13 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
     for (int w = 0; w < 16; w++) mbar_init(&full[w], 1);   // lane 0's arrive.expect_tx + the copies' bytes
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(128)
+                 "r"(D)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -198,7 +206,9 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
     // byte offset of this lane's first value inside a staging slot
     const uint32_t st_lane = smem_u32(sStage) + 4u * (uint32_t)(gb ? i0 : edge < 2 ? 36 * edge + t0 : 36 * edge + kM - t0);
     uint32_t phase = 0u, pf = 0u;
-    bool w1_ready = false;
+    uint32_t wph = 0u, fph = 0u;   // (thread 0) W1-landed / W1-free barrier parities
+    bool w1_pending = true;        // the prologue load not waited for yet
+    int round = 0;
     if ((int64_t)blockIdx.x * rows < B) stage((int64_t)blockIdx.x * rows);
     for (int64_t base = (int64_t)blockIdx.x * rows; base < B; base += step) {
       // ---- this warp's pw perimeters from the staging slots (G1 order; lane l
@@ -254,40 +264,62 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
       __syncwarp();
       if (base + step < B) stage(base + step);
       __syncthreads();
-      // ---- z = e W1^T on the tensor core: hi.hi + hi.lo + lo.hi
+      // ---- z = e W1^T on the tensor core: hi.hi + hi.lo + lo.hi (per W1 half)
       if (threadIdx.x == 0) {
-        if (!w1_ready) {
-          mbar_wait(&bar[1], 0u);
-          w1_ready = true;
-        }
-        tc_fence_after();
         const uint32_t w_hi = smem_u32(sWhi), w_lo = smem_u32(sWlo);
+        for (int hh = 0; hh < NH; hh++) {
+          const int h = (NH == 2 && (round & 1)) ? 1 - hh : hh;
+          if (hh > 0) {
+            // the buffer is overwritten with half h once the MMAs reading it are done
+            mma_commit(&bar[2]);
+            mbar_wait(&bar[2], fph);
+            fph ^= 1u;
+            mbar_arrive_expect_tx(&bar[1], 2u * kImg);
+            for (int i = 0; i < 4; i++)
+              bulk_g2s(smem_u32(sWhi) + i * (kImg / 2),
+                       reinterpret_cast<const uint8_t*>(net.W1img) + (size_t)h * 2 * kImg + i * (kImg / 2), kImg / 2,
+                       &bar[1]);
+            w1_pending = true;
+          }
+          if (w1_pending) {
+            mbar_wait(&bar[1], wph);
+            wph ^= 1u;
+            w1_pending = false;
+          }
+          tc_fence_after();
+          const uint32_t d = tmem + (uint32_t)(128 * h);
 #pragma unroll
-        for (int k = 0; k < kNB / 16; k++) {
-          const uint32_t off = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
-          mma_f16<0>(tmem, sw128_desc(a_hi + off), sw128_desc(w_hi + off), k > 0 ? 1u : 0u);
-          mma_f16<0>(tmem, sw128_desc(a_hi + off), sw128_desc(w_lo + off), 1u);
-          mma_f16<0>(tmem, sw128_desc(a_lo + off), sw128_desc(w_hi + off), 1u);
+          for (int k = 0; k < kNB / 16; k++) {
+            const uint32_t off = (uint32_t)((k >> 2) * 16384 + (k & 3) * 32);
+            mma_f16<0>(d, sw128_desc(a_hi + off), sw128_desc(w_hi + off), k > 0 ? 1u : 0u);
+            mma_f16<0>(d, sw128_desc(a_hi + off), sw128_desc(w_lo + off), 1u);
+            mma_f16<0>(d, sw128_desc(a_lo + off), sw128_desc(w_hi + off), 1u);
+          }
         }
         mma_commit(&bar[0]);
       }
+      round++;
       mbar_wait(&bar[0], phase);
       phase ^= 1u;
       tc_fence_after();
-      // ---- drain: warp w reads lanes 32 (w % 4).., columns 32 (w / 4)..
+      // ---- drain: warp w reads lanes 32 (w % 4).., columns 32 NH (w / 4)..
       {
         const int quad = warp & 3, cb = warp >> 2;
-        uint32_t r[32];
-        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(cb * 32), r);
-        tmem_wait_ld();
         const int64_t s = base + quad * 32 + lane;
-        if (quad * 32 + lane < rows && s < B) {
-          float4* dst = reinterpret_cast<float4*>(z + s * kD + cb * 32);
-          const float* bb = sB1 + cb * 32;
 #pragma unroll
-          for (int v = 0; v < 8; v++)
-            dst[v] = make_float4(__uint_as_float(r[4 * v]) + bb[4 * v], __uint_as_float(r[4 * v + 1]) + bb[4 * v + 1],
-                                 __uint_as_float(r[4 * v + 2]) + bb[4 * v + 2], __uint_as_float(r[4 * v + 3]) + bb[4 * v + 3]);
+        for (int hc = 0; hc < NH; hc++) {
+          const int col = (cb * NH + hc) * 32;
+          uint32_t r[32];
+          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)col, r);
+          tmem_wait_ld();
+          if (quad * 32 + lane < rows && s < B) {
+            float4* dst = reinterpret_cast<float4*>(z + s * D + col);
+            const float* bb = sB1 + col;
+#pragma unroll
+            for (int v = 0; v < 8; v++)
+              dst[v] = make_float4(__uint_as_float(r[4 * v]) + bb[4 * v], __uint_as_float(r[4 * v + 1]) + bb[4 * v + 1],
+                                   __uint_as_float(r[4 * v + 2]) + bb[4 * v + 2], __uint_as_float(r[4 * v + 3]) + bb[4 * v + 3]);
+          }
         }
       }
       tc_fence_before();
@@ -297,7 +329,7 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(D) : "memory");
   }
 }
 
@@ -313,9 +345,13 @@ bool embed_tc_enabled() {
 }
 
 void embed_tc_kernel_attributes() {
-  cudaFuncSetAttribute(emb::k_embed_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)emb::smem_bytes());
-  cudaFuncSetAttribute(emb::k_embed_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)emb::smem_bytes());
-  cudaFuncSetAttribute(emb::k_embed_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)emb::smem_bytes());
+  const int a = (int)emb::smem_bytes(kD), b = (int)emb::smem_bytes(kD2);
+  cudaFuncSetAttribute(emb::k_embed_tc<0, kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, a);
+  cudaFuncSetAttribute(emb::k_embed_tc<1, kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, a);
+  cudaFuncSetAttribute(emb::k_embed_tc<2, kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, a);
+  cudaFuncSetAttribute(emb::k_embed_tc<0, kD2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  cudaFuncSetAttribute(emb::k_embed_tc<1, kD2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  cudaFuncSetAttribute(emb::k_embed_tc<2, kD2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
 }
 
 void launch_embed_tc(const float* lat, const LatticeGeom& L, const uint32_t* anchors, const float* gb,
@@ -329,13 +365,14 @@ void launch_embed_tc(const float* lat, const LatticeGeom& L, const uint32_t* anc
   if (rows < 32) rows = 32;
   int64_t blocks = (B + rows - 1) / rows;
   if (blocks > sms) blocks = sms;
-  const size_t sm = emb::smem_bytes();
-  if (net.gelu_tanh == 2)
-    launch_pdl(emb::k_embed_tc<2>, (int)blocks, emb::kThreadsE, sm, s, lat, L, anchors, gb, B, rows, net, z);
-  else if (net.gelu_tanh == 1)
-    launch_pdl(emb::k_embed_tc<1>, (int)blocks, emb::kThreadsE, sm, s, lat, L, anchors, gb, B, rows, net, z);
-  else
-    launch_pdl(emb::k_embed_tc<0>, (int)blocks, emb::kThreadsE, sm, s, lat, L, anchors, gb, B, rows, net, z);
+  const size_t sm = emb::smem_bytes(net.d);
+#define MFP_EMB(G, D) launch_pdl(emb::k_embed_tc<G, D>, (int)blocks, emb::kThreadsE, sm, s, lat, L, anchors, gb, B, rows, net, z)
+  if (net.d == kD2) {
+    if (net.gelu_tanh == 2) MFP_EMB(2, kD2); else if (net.gelu_tanh == 1) MFP_EMB(1, kD2); else MFP_EMB(0, kD2);
+  } else {
+    if (net.gelu_tanh == 2) MFP_EMB(2, kD); else if (net.gelu_tanh == 1) MFP_EMB(1, kD); else MFP_EMB(0, kD);
+  }
+#undef MFP_EMB
 }
 
 }  // namespace mfp

@@ -44,18 +44,19 @@ __global__ void k_prep(PrepArgs a) {
   const int d = a.d;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  // W1T[k][c] = W1[c][k]; at d = 128 also the bf16 split images W1 = W1_hi + W1_lo
-  // (row c, K k) of the tensor-core embed
+  // W1T[k][c] = W1[c][k]; and the bf16 split images W1 = W1_hi + W1_lo (row c,
+  // K k) of the tensor-core embed
   for (int64_t i = tid; i < (int64_t)kNB * d; i += nth) {
     int k = (int)(i / d), c = (int)(i % d);
     const float w = a.P[a.oW1 + (int64_t)c * kNB + k];
     a.W1T[i] = w;
-    if (d == kD) {
+    {
+      // [half c / 128][hi | lo][128 rows x 128 K] (d = 256 holds two halves)
       const __nv_bfloat16 hi = __float2bfloat16_rn(w);
       const __nv_bfloat16 lo = __float2bfloat16_rn(w - __bfloat162float(hi));
-      uint8_t* img = reinterpret_cast<uint8_t*>(a.W1img);
-      *reinterpret_cast<__nv_bfloat16*>(img + sw128_offset(c, k)) = hi;
-      *reinterpret_cast<__nv_bfloat16*>(img + kD * kNB * 2 + sw128_offset(c, k)) = lo;
+      uint8_t* img = reinterpret_cast<uint8_t*>(a.W1img) + (size_t)(c >> 7) * 2 * (kD * kNB * 2);
+      *reinterpret_cast<__nv_bfloat16*>(img + sw128_offset(c & 127, k)) = hi;
+      *reinterpret_cast<__nv_bfloat16*>(img + kD * kNB * 2 + sw128_offset(c & 127, k)) = lo;
     }
   }
   // hidden layers

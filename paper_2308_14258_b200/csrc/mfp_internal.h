@@ -119,7 +119,7 @@ struct DevNet {
   // bf16 tables (tcgen05 path): weights pre-swizzled into the SW128 K-major image
   const uint16_t* Wh_sw2; // d = 128: [n_hidden][2][18 KB half] (CTA-pair chain: rows 64h..64h+63)
                           // d = 256: [n_hidden][2 CTAs][4 chunks x 16 KB + 4 KB bias] (kW2Cta)
-  const uint16_t* W1img;  // [2][128*128] bf16 SW128 images of W1 = W1_hi + W1_lo (tensor-core embed)
+  const uint16_t* W1img;  // [d/128][2][128*128] bf16 SW128 images of W1 = W1_hi + W1_lo (tensor-core embed)
   // exact subsolver
   const float* HcT;      // [128 k][64]  (61 used)
   const float* HfT;      // [128 k][961]
@@ -234,7 +234,7 @@ struct PrepArgs {
   float* W1T; float* WhT; float* bh;
   float* QTc; float* QTf;
   uint16_t* Wsw2;          // [n_hidden][kWImg] CTA-pair half images
-  uint16_t* W1img;         // [2][128*128] W1 hi / lo bf16 images
+  uint16_t* W1img;         // [d/128][2][128*128] W1 hi / lo bf16 images
 };
 bool embed_tc_enabled();
 void launch_embed_tc(const float* lat, const LatticeGeom& L, const uint32_t* anchors, const float* gb,
