@@ -288,6 +288,24 @@ mfp_status mfp_set_exchange_every(mfp_ctx* ctx, int32_t s);
 mfp_status mfp_p2p_export(mfp_ctx* ctx, void* handle_out);
 mfp_status mfp_p2p_open(mfp_ctx* ctx, const void* handles, int32_t n_handles);
 
+/* NEXT-2, device-initiated halo from the epilogue ("the scatter
+ * epilogue puts strips into neighbours' halos"; P:193 NVSHMEM-style direct
+ * GPU-GPU transfers).  After mfp_p2p_open, mode MFP_P2P_PUT makes the SDNet
+ * chain's epilogue store every owned cell a stencil peer holds as a halo cell
+ * straight into that peer's put buffer (peer memory; parity by exchange epoch)
+ * as it writes the cell; the iteration's exchange is then one publish kernel
+ * per rank (system fence + put-done flag to each peer; waits until every peer
+ * has unpacked the previous exchange) and a local unpack on the receiver,
+ * overlapped with the interior phase-0 subdomains as before — no pack kernel
+ * and no remote reads.  MFP_P2P_PULL restores pack + pull.  Same results as
+ * every other transport, bit for bit (the last write of the iteration wins in
+ * the put buffer, as the pack would read it).  Collective, at an iteration
+ * boundary; resets the region's flags and epochs.
+ * Errors: INVALID (p2p not open, exchange in flight, bad mode, PUT with the
+ * exact subsolver), CUDA. */
+enum { MFP_P2P_PULL = 0, MFP_P2P_PUT = 1 };
+mfp_status mfp_p2p_set_mode(mfp_ctx* ctx, int32_t mode);
+
 /* Run ONE phase (class 0..3 in G2 order) on the current lattice of every local
  * rank, without exchange (debug / sampled parity at full size). */
 mfp_status mfp_step_phase(mfp_ctx* ctx, int32_t phase);

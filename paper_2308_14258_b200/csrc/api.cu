@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include <time.h>
@@ -58,6 +59,13 @@ struct RankState {
   char* p2p = nullptr;         // NEXT-2 peer-memory region (own cudaMalloc, IPC-exportable)
   P2PPeer* p2p_tab = nullptr;  // device table of the stencil peers' regions
   int p2p_np = 0;
+  // put mode (mfp_p2p_set_mode): sender tables and the receiver's unpack list
+  int32_t* putmap = nullptr;   // [lattice cells]: -1 or first << 2 | count into putdst
+  int32_t* putdst = nullptr;   // peer index << 24 | slot in the peer's putbuf
+  float** putbufs = nullptr;   // [2 * npeers]: peer i's putbuf[parity]
+  int32_t* pu_idx = nullptr;   // receiver: halo cells refreshed by puts (∂Ω cells excluded)
+  int32_t* pu_slot = nullptr;  //           and their slots in the own putbuf
+  int64_t npu = 0;
 };
 
 }  // namespace
@@ -77,6 +85,7 @@ struct mfp_ctx {
   bool use_graphs = false;             // replay blocks of c iterations as CUDA graphs
   int exchange_every = 1;              // halo exchange after every s-th iteration (NEXT-4)
   bool p2p = false;                    // halo transport: peer-memory kernels (NEXT-2) instead of NCCL / copies
+  bool p2p_put = false;                // ... with puts from the chain epilogue instead of pack + pull
   std::vector<void*> p2p_opened;       // IPC-mapped peer regions (multi-process)
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // [0] plain block, [1] block ending in a check
   cudaGraphExec_t gloop = nullptr;     // WHILE graph: blocks of c iterations + on-device stopping rule
@@ -331,6 +340,12 @@ Sink lattice_sink(RankState& rs, int kphase) {
   s.mode = 0; s.q = kQC; s.lat = rs.lat; s.offV = rs.plan.lat.offV;
   s.strideH = rs.plan.lat.strideH; s.strideV = rs.plan.lat.strideV;
   s.anchors = rs.anchors[kphase];
+  if (rs.putmap) {   // NEXT-2 put transport
+    s.putmap = rs.putmap;
+    s.putdst = rs.putdst;
+    s.putbufs = rs.putbufs;
+    s.put_epoch = (const unsigned long long*)(rs.p2p + kP2PEpochOff) + 1;
+  }
   return s;
 }
 
@@ -409,12 +424,41 @@ P2PSelf p2p_self(const RankState& rs) {
   s.counter = (unsigned int*)(rs.p2p + kP2PCounterOff);
   s.sendbuf[0] = (float*)(rs.p2p + kP2PHeader);
   s.sendbuf[1] = (float*)(rs.p2p + kP2PHeader + p2p_parity_bytes(rs.nsend));
+  s.putbuf[0] = (float*)(rs.p2p + kP2PHeader + 2 * p2p_parity_bytes(rs.nsend));
+  s.putbuf[1] = (float*)(rs.p2p + kP2PHeader + 2 * p2p_parity_bytes(rs.nsend) + p2p_parity_bytes(rs.nrecv));
   return s;
 }
 
 // NEXT-2 transport (kernels_p2p.cu): pack + publish on the main stream, then
 // the fused pull + unpack on the side stream; no NCCL call, no host wait.
 mfp_status exchange_begin_p2p(mfp_ctx* c) {
+  if (c->p2p_put) {
+    // put mode: the epilogues already stored the halo values into the peers'
+    // put buffers; publish them, then unpack the own put buffer on the side stream
+    for (auto& rs : c->ranks) {
+      launch_put_publish(p2p_self(rs), rs.p2p_np, rs.p2p_tab, c->stream);
+      c->launches++;
+    }
+    CK(cudaEventRecord(c->ev_packed, c->stream));
+    CK(cudaStreamWaitEvent(c->side, c->ev_packed, 0));
+    cudaEvent_t h0 = nullptr;
+    if (c->profiling) {
+      h0 = ev(c);
+      cudaEventRecord(h0, c->side);
+    }
+    for (auto& rs : c->ranks) {
+      launch_put_unpack(rs.lat, rs.pu_idx, rs.pu_slot, rs.npu, p2p_self(rs), rs.p2p_np, rs.p2p_tab, c->side);
+      c->launches++;
+    }
+    CK(cudaEventRecord(c->ev_unpacked, c->side));
+    if (c->profiling) {
+      cudaEvent_t h1 = ev(c);
+      cudaEventRecord(h1, c->side);
+      c->spans.push_back({h0, h1, kKindHalo, 0});
+    }
+    c->pending = true;
+    return MFP_OK;
+  }
   for (auto& rs : c->ranks) {
     launch_pack_p2p(rs.lat, rs.send_idx, rs.nsend, p2p_self(rs), rs.p2p_np, rs.p2p_tab, c->stream);
     c->launches++;
@@ -877,8 +921,9 @@ namespace {
 void p2p_quiesce(mfp_ctx* c) {
   RankState& rs = c->ranks[0];
   if (!rs.p2p) return;
-  unsigned long long epoch = 0;
-  if (cudaMemcpy(&epoch, rs.p2p + kP2PEpochOff, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  unsigned long long epoch = 0;   // the exchanges this rank published (pull epoch, or put epoch)
+  if (cudaMemcpy(&epoch, rs.p2p + kP2PEpochOff + (c->p2p_put ? 8 : 0), 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return;
   std::vector<unsigned long long> flags(kP2PConsumed + kP2PMaxRanks);
   for (int spin = 0; spin < 300000; spin++) {
     if (cudaMemcpy(flags.data(), rs.p2p, flags.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
@@ -1062,6 +1107,8 @@ void mfp_destroy(mfp_ctx* c) {
   for (auto& rs : c->ranks) {
     if (rs.p2p) cudaFree(rs.p2p);
     if (rs.p2p_tab) cudaFree(rs.p2p_tab);
+    for (void* q : {(void*)rs.putmap, (void*)rs.putdst, (void*)rs.putbufs, (void*)rs.pu_idx, (void*)rs.pu_slot})
+      if (q) cudaFree(q);
   }
   delete c;
 }
@@ -1217,7 +1264,7 @@ namespace {
 mfp_status p2p_alloc_own(mfp_ctx* c) {
   for (auto& rs : c->ranks)
     if (!rs.p2p) {
-      const size_t bytes = p2p_region_bytes(rs.nsend);
+      const size_t bytes = p2p_region_bytes(rs.nsend, rs.nrecv);
       CK(cudaMalloc((void**)&rs.p2p, bytes));
       CK(cudaMemset(rs.p2p, 0, bytes));
     }
@@ -1314,6 +1361,136 @@ mfp_status mfp_p2p_open(mfp_ctx* c, const void* handles, int32_t n_handles) {
     if (g) { cudaGraphExecDestroy(g); g = nullptr; }
   if (c->gloop) { cudaGraphExecDestroy(c->gloop); c->gloop = nullptr; }
   c->p2p = true;
+  return MFP_OK;
+}
+
+mfp_status mfp_p2p_set_mode(mfp_ctx* c, int32_t mode) {
+  if (!c) return MFP_ERR_INVALID;
+  if (c->poisoned) return MFP_ERR_STATE;
+  if (mode != MFP_P2P_PULL && mode != MFP_P2P_PUT) return fail(c, MFP_ERR_INVALID, "p2p_set_mode: bad mode");
+  if (!c->p2p) return fail(c, MFP_ERR_INVALID, "p2p_set_mode: call mfp_p2p_open first");
+  if (c->pending) return fail(c, MFP_ERR_INVALID, "p2p_set_mode: an exchange is in flight");
+  if ((mode == MFP_P2P_PUT) == c->p2p_put) return MFP_OK;
+  if (mode == MFP_P2P_PUT && c->cfg.subsolver != MFP_SDNET)
+    return fail(c, MFP_ERR_INVALID, "p2p_set_mode: puts come from the SDNet chain epilogue (MFP_SDNET only)");
+  // switching resets the epochs: both transports start from a clean region
+  // (collective: every rank switches at the same iteration boundary)
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaStreamSynchronize(c->side));
+  auto free_put = [&](RankState& rs) {
+    for (void* q : {(void*)rs.putmap, (void*)rs.putdst, (void*)rs.putbufs, (void*)rs.pu_idx, (void*)rs.pu_slot})
+      if (q) cudaFree(q);
+    rs.putmap = rs.putdst = rs.pu_idx = rs.pu_slot = nullptr;
+    rs.putbufs = nullptr;
+    rs.npu = 0;
+  };
+  for (auto& rs : c->ranks) free_put(rs);
+  if (mode == MFP_P2P_PUT) {
+    GlobalPlan gp;
+    std::string err;
+    if (mfp_status st = build_plan(&c->cfg, MFP_ALL_RANKS, &gp, &err)) return fail(c, st, err);
+    const int nx = c->cfg.nx, ny = c->cfg.ny;
+    auto on_boundary = [&](int x, int y) { return x == 0 || x == nx || y == 0 || y == ny; };
+    std::vector<P2PPeer> tab;
+    for (auto& rs : c->ranks) {
+      const RankPlan& p = rs.plan;
+      // sender: owned cell -> (peer i, slot in peer q's recv numbering); the
+      // peer's recv segment from this rank has the same order as this rank's
+      // send list to it (the pull transport relies on the same fact)
+      std::vector<std::vector<int32_t>> dst((size_t)p.lat.cells);
+      for (size_t i = 0; i < p.peers.size(); i++) {
+        const RankPlan& qp = gp.ranks[p.peers[i].rank];
+        int64_t base = 0;
+        bool found = false;
+        for (const auto& x : qp.peers) {
+          if (x.rank == p.rank) { found = true; break; }
+          base += (int64_t)x.recv_idx.size();
+        }
+        if (!found) return fail(c, MFP_ERR_INVALID, "p2p_set_mode: asymmetric stencil");
+        const auto& sp = p.peers[i];
+        for (size_t k = 0; k < sp.send_idx.size(); k++) {
+          if (on_boundary(sp.send_x[k], sp.send_y[k])) continue;   // never rewritten: no put
+          dst[(size_t)sp.send_idx[k]].push_back((int32_t)((i << 24) | (size_t)(base + (int64_t)k)));
+        }
+      }
+      std::vector<int32_t> map((size_t)p.lat.cells, -1), lst;
+      for (size_t cell = 0; cell < dst.size(); cell++) {
+        if (dst[cell].empty()) continue;
+        if (dst[cell].size() > 3) return fail(c, MFP_ERR_INVALID, "p2p_set_mode: a cell in more than 3 halos");
+        map[cell] = (int32_t)((lst.size() << 2) | dst[cell].size());
+        lst.insert(lst.end(), dst[cell].begin(), dst[cell].end());
+      }
+      // receiver: every recv slot except the domain-boundary cells (their halo
+      // copy is g, written by every rank's own init)
+      std::vector<int32_t> uidx, uslot;
+      int64_t o = 0;
+      for (const auto& rp : p.peers)
+        for (size_t k = 0; k < rp.recv_idx.size(); k++, o++)
+          if (!on_boundary(rp.recv_x[k], rp.recv_y[k])) {
+            uidx.push_back(rp.recv_idx[k]);
+            uslot.push_back((int32_t)o);
+          }
+      // the peers' put buffers, parity 0 / 1
+      tab.resize(p.peers.size());
+      if (!p.peers.empty())
+        CK(cudaMemcpy(tab.data(), rs.p2p_tab, p.peers.size() * sizeof(P2PPeer), cudaMemcpyDeviceToHost));
+      std::vector<float*> bufs;
+      for (size_t i = 0; i < p.peers.size(); i++) {
+        const RankPlan& qp = gp.ranks[p.peers[i].rank];
+        int64_t qs = 0, qr = 0;
+        for (const auto& x : qp.peers) { qs += (int64_t)x.send_idx.size(); qr += (int64_t)x.recv_idx.size(); }
+        char* qbase = (char*)tab[i].flags;   // the peer's region base
+        bufs.push_back((float*)(qbase + kP2PHeader + 2 * p2p_parity_bytes(qs)));
+        bufs.push_back((float*)(qbase + kP2PHeader + 2 * p2p_parity_bytes(qs) + p2p_parity_bytes(qr)));
+      }
+      auto up = [&](auto** dptr, const auto& v) -> cudaError_t {
+        using T = typename std::remove_reference<decltype(v)>::type::value_type;
+        cudaError_t e = cudaMalloc((void**)dptr, std::max<size_t>(1, v.size()) * sizeof(T));
+        if (e == cudaSuccess && !v.empty()) e = cudaMemcpy(*dptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+        return e;
+      };
+      cudaError_t e = up(&rs.putmap, map);
+      if (e == cudaSuccess) e = up(&rs.putdst, lst);
+      if (e == cudaSuccess) e = up(&rs.putbufs, bufs);
+      if (e == cudaSuccess) e = up(&rs.pu_idx, uidx);
+      if (e == cudaSuccess) e = up(&rs.pu_slot, uslot);
+      if (e != cudaSuccess) {
+        for (auto& r2 : c->ranks) free_put(r2);
+        return fail(c, MFP_ERR_CUDA, std::string("p2p_set_mode: ") + cudaGetErrorString(e));
+      }
+      rs.npu = (int64_t)uidx.size();
+    }
+  }
+  // anchors: bit 31 marks the subdomains whose centre-line cells feed a peer's
+  // halo (the epilogue looks up the put map only for those); plain in pull mode
+  for (auto& rs : c->ranks) {
+    const RankPlan& p = rs.plan;
+    std::vector<int32_t> map;
+    if (mode == MFP_P2P_PUT) {
+      map.resize((size_t)p.lat.cells);
+      CK(cudaMemcpy(map.data(), rs.putmap, map.size() * 4, cudaMemcpyDeviceToHost));
+    }
+    for (int k = 0; k < 4; k++) {
+      std::vector<uint32_t> an = p.phase_anchor[k];
+      if (mode == MFP_P2P_PUT)
+        for (auto& pk : an) {
+          const int a = (int)(pk & 0xffffu), b = (int)(pk >> 16), lx = kH * a, ly = kH * b;
+          bool feeds = false;
+          for (int t = 1; t < kM && !feeds; t++)
+            feeds = map[(size_t)(p.lat.offV + (int64_t)(a + 1) * p.lat.strideV + ly + t)] >= 0 ||
+                    map[(size_t)((int64_t)(b + 1) * p.lat.strideH + lx + t)] >= 0;
+          if (feeds) pk |= 0x80000000u;
+        }
+      if (!an.empty()) CK(cudaMemcpy(rs.anchors[k], an.data(), an.size() * 4, cudaMemcpyHostToDevice));
+    }
+  }
+  // fresh flags, epochs and tickets for the new protocol
+  for (auto& rs : c->ranks) CK(cudaMemset(rs.p2p, 0, kP2PHeader));
+  CK(cudaDeviceSynchronize());
+  for (auto& g : c->gexec)
+    if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+  if (c->gloop) { cudaGraphExecDestroy(c->gloop); c->gloop = nullptr; }
+  c->p2p_put = (mode == MFP_P2P_PUT);
   return MFP_OK;
 }
 

@@ -54,7 +54,7 @@ __device__ __forceinline__ float gelu_fast(float x) { return 0.5f * gelu2_fast(x
 // bottom edge (lx = 16 a, ly = 16 b).
 __device__ __forceinline__ void unpack_anchor(uint32_t p, int& a, int& b) {
   a = (int)(p & 0xffffu);
-  b = (int)(p >> 16);
+  b = (int)((p >> 16) & 0x7fffu);   // bit 31: "writes a cell some peer holds as halo" (put mode)
 }
 
 // Perimeter value i (0..127) in G1 order: bottom L->R, right B->T, top R->L, left T->B.
@@ -169,15 +169,35 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+// NEXT-2 put transport: an owned cell some peer holds as a halo cell is also
+// stored into that peer's put buffer (peer memory over NVLink, or this device
+// under MFP_ALL_RANKS) of parity (put epoch + 1) & 1; a cell sits in at most 3
+// peers' halos (a corner).  Only subdomains whose anchor carries bit 31 look
+// their cells up, so the common path costs one predicated branch.
+__device__ __forceinline__ void put_halo(const Sink& sk, int64_t c, float y) {
+  const int32_t pm = __ldg(sk.putmap + c);
+  if (pm < 0) return;
+  const int par = (int)((*sk.put_epoch + 1ull) & 1ull);
+  for (int k = 0; k < (pm & 3); k++) {
+    const int32_t d = __ldg(sk.putdst + (pm >> 2) + k);
+    sk.putbufs[2 * (d >> 24) + par][d & 0xffffff] = y;
+  }
+}
+
 // Write one chain output (row = s * q + p) to its sink.
 __device__ __forceinline__ void sink_store(const Sink& sk, int64_t s, int p, float y) {
   if (sk.mode == 0) {
     int a, b;
-    unpack_anchor(__ldg(sk.anchors + s), a, b);
+    const uint32_t pk = __ldg(sk.anchors + s);
+    unpack_anchor(pk, a, b);
     int64_t dup;
     int64_t c = centre_cell(a, b, p, sk.strideH, sk.strideV, sk.offV, &dup);
     sk.lat[c] = y;
     if (dup >= 0) sk.lat[dup] = y;
+    if (sk.putmap && (pk >> 31)) {   // only subdomains whose centre lines feed a peer's halo
+      put_halo(sk, c, y);
+      if (dup >= 0) put_halo(sk, dup, y);
+    }
   } else if (sk.mode == 1) {
     uint32_t pk = __ldg(sk.anchors + s);
     int bx = (int)(pk & 0xffffu), by = (int)(pk >> 16);

@@ -96,6 +96,51 @@ __global__ void k_pull_p2p(float* __restrict__ lat, const int32_t* __restrict__ 
   }
 }
 
+// ---- put mode (device-initiated halo from the chain epilogue, SURVEY NEXT-2:
+// "the scatter epilogue puts strips into neighbours' halos").  During the
+// phases of exchange e the chain epilogues of the SENDER store every owned cell
+// a peer holds as a halo cell straight into the peer's putbuf[e & 1]
+// (device_common.cuh put_halo; the last write of the iteration wins, so the
+// buffer ends with the owner's end-of-iteration values, as a pack would).
+//   k_put_publish (sender, main stream, after the iteration's last phase):
+//     one system fence, put_done[me] = e on every peer; then wait until every
+//     peer has unpacked exchange e - 1 (so the next iteration's puts, parity
+//     (e + 1) & 1, overwrite a buffer nobody still reads), and advance the put
+//     epoch the epilogues read.
+//   k_put_unpack (receiver, side stream): wait for put_done >= e of every peer,
+//     copy putbuf[e & 1] into the halo cells (local reads), publish
+//     consumed[me] = e on every peer, advance the unpack epoch.
+// No cycle: publish(e) waits on unpack(e - 1), unpack(e) on publish(e).
+__global__ void k_put_publish(P2PSelf self, int npeers, const P2PPeer* __restrict__ peers) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long e = self.epoch[1] + 1;
+  // the chain kernels that stored the puts precede this kernel in stream order
+  // (kernel boundary: their writes happen before this thread's operations), and
+  // fence.sc.sys is cumulative: the flag below is ordered after those puts, as
+  // after this thread's own writes — no fence in the 148 x 576 epilogue threads
+  __threadfence_system();
+  for (int i = 0; i < npeers; i++) st_relaxed_sys(peers[i].flags + kP2PPutDone + self.rank, e);
+  for (int i = 0; i < npeers; i++)
+    while (ld_acquire_sys(self.flags + kP2PConsumed + peers[i].rank) + 1 < e) __nanosleep(64);
+  self.epoch[1] = e;
+}
+
+__global__ void k_put_unpack(float* __restrict__ lat, const int32_t* __restrict__ idx,
+                             const int32_t* __restrict__ slot, int64_t n, P2PSelf self, int npeers,
+                             const P2PPeer* __restrict__ peers) {
+  const unsigned long long e = self.epoch[2] + 1;
+  block_wait_peers(npeers, [&](int i) { return (const unsigned long long*)self.flags + kP2PPutDone + peers[i].rank; },
+                   e);
+  const float* buf = self.putbuf[e & 1];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    lat[__ldg(idx + j)] = buf[__ldg(slot + j)];
+  if (last_block(self.counter + 2)) {
+    __threadfence_system();
+    for (int i = 0; i < npeers; i++) st_relaxed_sys(peers[i].flags + kP2PConsumed + self.rank, e);
+    self.epoch[2] = e;
+  }
+}
+
 static int grid_p2p(int64_t n) {
   int64_t b = (n + 255) / 256;
   // every pull block polls the <= 8 peer flags (one thread per peer, nanosleep
@@ -113,6 +158,13 @@ void launch_pack_p2p(const float* lat, const int32_t* idx, int64_t n, const P2PS
 void launch_pull_p2p(float* lat, const int32_t* idx, int64_t n, const P2PSelf& self, int npeers,
                      const P2PPeer* peers, cudaStream_t s) {
   k_pull_p2p<<<grid_p2p(n), 256, 0, s>>>(lat, idx, n, self, npeers, peers);
+}
+void launch_put_publish(const P2PSelf& self, int npeers, const P2PPeer* peers, cudaStream_t s) {
+  k_put_publish<<<1, 32, 0, s>>>(self, npeers, peers);
+}
+void launch_put_unpack(float* lat, const int32_t* idx, const int32_t* slot, int64_t n, const P2PSelf& self,
+                       int npeers, const P2PPeer* peers, cudaStream_t s) {
+  k_put_unpack<<<grid_p2p(n), 256, 0, s>>>(lat, idx, slot, n, self, npeers, peers);
 }
 
 }  // namespace mfp

@@ -136,6 +136,14 @@ struct Sink {
   float* field;
   int ld;
   float* out;
+  // mode 0, NEXT-2 put transport (nullptr otherwise): owned cells in a peer's
+  // halo are also stored straight into that peer's put buffer of parity
+  // (*put_epoch + 1) & 1.  putmap[cell] = -1 or (first << 2 | count) into
+  // putdst; putdst = peer index << 24 | slot; putbufs[2 * peer + parity].
+  const int32_t* putmap;
+  const int32_t* putdst;
+  float* const* putbufs;
+  const unsigned long long* put_epoch;
 };
 
 // Launch with programmatic stream serialization (PDL, see tc_common.cuh) so the
@@ -192,24 +200,31 @@ void launch_delta(const float* lat, const float* snap, const int64_t* segs, int 
 void launch_pack(const float* lat, const int32_t* idx, int64_t n, float* buf, cudaStream_t s);
 void launch_unpack(float* lat, const int32_t* idx, int64_t n, const float* buf, cudaStream_t s);
 // NEXT-2 peer-memory halo transport (kernels_p2p.cu).  A rank's P2P region
-// (one cudaMalloc, IPC-exportable): u64 flags[kP2PFlags] at 0 (packed epoch at
-// kP2PPacked, consumed epoch of consumer rank r at kP2PConsumed + r), the u64
-// epoch at kP2PEpochOff, two u32 block counters at kP2PCounterOff, then
-// sendbuf[0] at kP2PHeader and sendbuf[1] at kP2PHeader + p2p_parity_bytes(nsend).
+// (one cudaMalloc, IPC-exportable): u64 flags at 0 — packed epoch at
+// kP2PPacked, consumed epoch of consumer rank r at kP2PConsumed + r, put-done
+// epoch of sender rank r at kP2PPutDone + r — then the u64 epochs at
+// kP2PEpochOff (pull epoch, put epoch of this sender, put-unpack epoch of this
+// receiver), u32 block counters at kP2PCounterOff, then sendbuf[0], sendbuf[1]
+// (pull mode, nsend floats each) and putbuf[0], putbuf[1] (put mode: written by
+// the SENDERS' chain epilogues, nrecv floats each) from kP2PHeader.
 constexpr int kP2PMaxRanks = 256;
 constexpr int kP2PPacked = 0;
 constexpr int kP2PConsumed = 8;
-constexpr size_t kP2PEpochOff = (size_t)(kP2PConsumed + kP2PMaxRanks) * 8;
+constexpr int kP2PPutDone = kP2PConsumed + kP2PMaxRanks;
+constexpr size_t kP2PEpochOff = (size_t)(kP2PPutDone + kP2PMaxRanks) * 8;
 constexpr size_t kP2PCounterOff = kP2PEpochOff + 64;
-constexpr size_t kP2PHeader = 4096;
-inline size_t p2p_parity_bytes(int64_t nsend) { return ((size_t)(nsend > 0 ? nsend : 1) * 4 + 255) / 256 * 256; }
-inline size_t p2p_region_bytes(int64_t nsend) { return kP2PHeader + 2 * p2p_parity_bytes(nsend); }
+constexpr size_t kP2PHeader = 8192;
+inline size_t p2p_parity_bytes(int64_t n) { return ((size_t)(n > 0 ? n : 1) * 4 + 255) / 256 * 256; }
+inline size_t p2p_region_bytes(int64_t nsend, int64_t nrecv) {
+  return kP2PHeader + 2 * p2p_parity_bytes(nsend) + 2 * p2p_parity_bytes(nrecv);
+}
 struct P2PSelf {
   int rank;
   unsigned long long* flags;  // own region
-  unsigned long long* epoch;
-  unsigned int* counter;      // [2]
+  unsigned long long* epoch;  // [0] pull epoch, [1] put epoch (sender), [2] put-unpack epoch (receiver)
+  unsigned int* counter;      // [3]: pack, pull, put-unpack last-block tickets
   float* sendbuf[2];
+  float* putbuf[2];           // own put-receive buffers
 };
 struct P2PPeer {               // device table, one entry per stencil peer, recv_off ascending
   int rank;
@@ -222,6 +237,10 @@ void launch_pack_p2p(const float* lat, const int32_t* idx, int64_t n, const P2PS
                      const P2PPeer* peers, cudaStream_t s);
 void launch_pull_p2p(float* lat, const int32_t* idx, int64_t n, const P2PSelf& self, int npeers,
                      const P2PPeer* peers, cudaStream_t s);
+// put mode: publish (sender, end of iteration) and unpack (receiver, side stream)
+void launch_put_publish(const P2PSelf& self, int npeers, const P2PPeer* peers, cudaStream_t s);
+void launch_put_unpack(float* lat, const int32_t* idx, const int32_t* slot, int64_t n, const P2PSelf& self,
+                       int npeers, const P2PPeer* peers, cudaStream_t s);
 void launch_final_lines(const float* lat, const LatticeGeom& L, int X0, int Y0, int bw, int bh,
                         float* field, int ld, cudaStream_t s);
 // one-time preparation (kernels_prep.cu)

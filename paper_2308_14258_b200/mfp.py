@@ -104,6 +104,7 @@ _SIGS = {
     "mfp_set_exchange_every": [_vp, _i32],
     "mfp_p2p_export": [_vp, _vp],
     "mfp_p2p_open": [_vp, _vp, _i32],
+    "mfp_p2p_set_mode": [_vp, _i32],
     "mfp_nccl_get_unique_id": [_vp],
     "mfp_nccl_comm_init": [_i32, _vp, _i32, _P(_vp)],
     "mfp_nccl_comm_destroy": [_vp],
@@ -237,6 +238,15 @@ def mfp_p2p_open(ctx, handles=None) -> None:
             raise MfpError(1, "p2p_open: every handle must be 64 bytes")
     buf = None if handles is None else ctypes.create_string_buffer(b"".join(handles), 64 * len(handles))
     _check(_lib.mfp_p2p_open(ctx, buf, 0 if handles is None else len(handles)), ctx)
+
+
+P2P_PULL, P2P_PUT = 0, 1
+
+
+def mfp_p2p_set_mode(ctx, mode: int) -> None:
+    """NEXT-2: after mfp_p2p_open, P2P_PUT makes the chain epilogue store halo
+    cells straight into the peers' put buffers (P2P_PULL: pack + pull)."""
+    _check(_lib.mfp_p2p_set_mode(ctx, mode), ctx)
 
 
 def mfp_step_phase(ctx, phase: int) -> None:

@@ -1,6 +1,8 @@
 """NEXT-2 timing: device time of an MFP solve on every rank of a Py x Px grid on
 one GPU (MFP_ALL_RANKS), halo through device copies (pack, cudaMemcpyAsync,
-unpack) vs the peer-memory kernels (pack+publish, fused pull+unpack).  One
+unpack) vs the peer-memory kernels (pack+publish, fused pull+unpack) vs the
+put transport (halo cells stored into the peers' put buffers by the chain
+epilogue, publish, local unpack).  One
 device serialises all ranks, so this compares launch counts and per-exchange
 overhead of the transports, not NVLink bandwidth.
 
@@ -31,11 +33,13 @@ def main():
     w = random_weights(0)
     res = {"workload": f"{a.n + 1}^2, grid {a.grid[0]}x{a.grid[1]} all ranks on one GPU, bf16 SDNet (W-rand), "
                        f"{a.iters} iterations, check_every 16", "transports": {}}
-    for name in ("copy", "p2p"):
+    for name in ("copy", "p2p", "put"):
         cfg = mfp.make_config(a.n, a.n, tuple(a.grid), precision=1, subsolver=mfp.SDNET, check_every=16)
         m = mfp.Mfp(cfg, mfp.make_net(gelu=1), w, rank=mfp.ALL_RANKS)
-        if name == "p2p":
+        if name in ("p2p", "put"):
             mfp.mfp_p2p_open(m.ctx)
+        if name == "put":
+            mfp.mfp_p2p_set_mode(m.ctx, mfp.P2P_PUT)
         ms, u_last = [], None
         for _ in range(a.reps + 1):
             u, rep = m.solve(g, a.iters, 0.0)
@@ -48,8 +52,8 @@ def main():
                                    "halo_ms_per_iter_profiled": prof.ms_halo,
                                    "halo_bytes_per_iter": rep.halo_bytes_sent / a.iters}
         res["transports"][name]["_u"] = u_last
-    same = np.array_equal(res["transports"]["copy"].pop("_u"), res["transports"]["p2p"].pop("_u"))
-    res["bit_identical"] = bool(same)
+    u0 = res["transports"]["copy"].pop("_u")
+    res["bit_identical"] = {k: bool(np.array_equal(u0, res["transports"][k].pop("_u"))) for k in ("p2p", "put")}
     print(json.dumps(res, indent=1))
     if a.out:
         with open(a.out, "w") as f:
