@@ -42,13 +42,17 @@ def test_sdnet_matches_torch_fp64(qs):
     assert np.max(np.abs(got - want)) < 1e-12 * max(1.0, np.max(np.abs(want)))
 
 
-def test_sdnet_other_width():
-    net = oracle.NetShape(d=64, n_hidden=2)
-    flat = random_weights(5, d=64, n_hidden=2).astype(np.float64)
+@pytest.mark.parametrize("d,nh", [(64, 2), (256, 3)])
+def test_sdnet_other_width(d, nh):
+    """Other widths, including the wide variant the d = 256 kernels are checked
+    against (SURVEY §8(b) d = 128 | 256)."""
+    net = oracle.NetShape(d=d, n_hidden=nh)
+    flat = random_weights(5, d=d, n_hidden=nh).astype(np.float64)
     gb = random_boundaries(3, seed=4).astype(np.float64)
-    q = oracle.writeset(0, 0)[1]
-    got = oracle.sdnet_forward(flat, gb, q, net=net)
-    assert np.max(np.abs(got - torch_sdnet(flat, gb, q, d=64, n_hidden=2))) < 1e-12
+    for q in (oracle.writeset(0, 0)[1], oracle.interior_queries()):
+        got = oracle.sdnet_forward(flat, gb, q, net=net)
+        want = torch_sdnet(flat, gb, q, d=d, n_hidden=nh)
+        assert np.max(np.abs(got - want)) < 1e-12 * max(1.0, np.max(np.abs(want)))
 
 
 def test_param_count_matches_layout():
