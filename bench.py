@@ -94,10 +94,11 @@ def wide_leg(mfp, torch, stream, cfg, g_dev, u_dev, flush, ppi, peaks, T=16, ste
     peak = peaks.get("bf16_tflops_sustained", 1400.0)
     achieved = flop / (chain_ms / 1000.0) / 1e12
     mw.close()
+    burst = peaks.get("bf16_tflops", 1630.0)
     return {"d": D, "value": ppi * T * steps / (ms / 1000.0), "unit": "predictions/s",
             "ms_per_solve": ms / steps, "iters_per_solve": T,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "kernel": kernel,
+                         "frac": achieved / peak, "frac_vs_burst_peak": achieved / burst, "kernel": kernel,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                          "flop_per_launch": flop, "chain_ms_per_launch": chain_ms,
                          "chain_per_phase_ms": prof.ms_chain, "gather_embed_per_phase_ms": prof.ms_gather_embed,
@@ -549,8 +550,13 @@ def main():
     tfile = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tfile):
         traffic = json.load(open(tfile)).get("chain_tc_dram_bytes_per_launch")
+    burst = peaks.get("bf16_tflops", 1630.0)
     roofline = {"bound": "tensor" if tensor else "alu", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                # the chain runs unthrottled (MUFU-bound, well under the power cap), so the
+                # burst figure is the stricter denominator; both are reported
+                "frac_vs_burst_peak": achieved / burst if tensor else None,
+                "burst_peak": burst if tensor else None,
                 "kernel": "k_chain_tc2 (hidden GEMM chain a4 + epilogues a3/a5/a6)" if tensor else "k_chain_fp32",
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"
                 if tensor else "derived fp32 SIMT peak (DESIGN.md §7)",
