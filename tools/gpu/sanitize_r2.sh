@@ -23,3 +23,16 @@ timeout 1200 compute-sanitizer --tool memcheck --print-limit 10 python -m pytest
   -k "(field_parity and 64) or (fitted_field and 128 and sdnet_fit_d128.npy)" 2>&1 | tail -3
 } > gpurun_out/sanitize_r2.log 2>&1
 cat gpurun_out/sanitize_r2.log
+# round-2 host paths: the put transport (epilogue puts, publish / unpack spin
+# protocol) and the on-device convergence loop (graphs on: the WHILE node)
+{
+for t in memcheck synccheck racecheck; do
+  echo "== $t p2p put"
+  MFP_NO_GRAPHS=1 timeout 900 compute-sanitizer --tool $t --print-limit 10 python -m pytest tests/test_gpu_p2p_put.py -q -x \
+    -k "bit_identical and (grid0 or grid2)" 2>&1 | tail -3
+done
+echo "== memcheck device loop"
+unset MFP_NO_GRAPHS
+timeout 900 compute-sanitizer --tool memcheck --print-limit 10 python -m pytest tests/test_gpu_device_loop.py -q -x 2>&1 | tail -3
+} >> gpurun_out/sanitize_r2.log 2>&1
+tail -16 gpurun_out/sanitize_r2.log
