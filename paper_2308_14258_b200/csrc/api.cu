@@ -89,6 +89,8 @@ struct mfp_ctx {
   std::vector<void*> p2p_opened;       // IPC-mapped peer regions (multi-process)
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // [0] plain block, [1] block ending in a check
   cudaGraphExec_t gloop = nullptr;     // WHILE graph: blocks of c iterations + on-device stopping rule
+  bool exact_persist = false;          // exact subsolver, one rank: persistent dataflow iteration kernel
+  ExactIterArgs xargs{};               // its tables (device, owned by the context)
   int gloop_launches = 0;              // kernels per loop-body block
   unsigned int* loopst = nullptr;      // device {iterations, t, tol bits, blocks}
   unsigned int* hloop = nullptr;       // pinned host mirror
@@ -546,6 +548,14 @@ mfp_status exchange_wait(mfp_ctx* c) {
 // is in flight, then the halo-touching ones), phases 1-3, then the exchange.
 mfp_status iterate(mfp_ctx* c, bool exchange = true) {
   mfp_status st;
+  if (c->exact_persist) {   // one launch: the 4 phases with dataflow stamps (single rank, no exchange)
+    SpanGuard g(c, kKindExact, c->xargs.B[0] + c->xargs.B[1] + c->xargs.B[2] + c->xargs.B[3]);
+    ExactIterArgs a = c->xargs;
+    a.K = 1;
+    launch_exact_iter(a, c->stream);
+    c->launches++;
+    return MFP_OK;
+  }
   if (c->pending) {
     for (auto& rs : c->ranks) run_phase(c, rs, 0, 0, rs.plan.n0_interior);
     if ((st = exchange_wait(c))) return st;
@@ -914,6 +924,92 @@ mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, floa
 }  // namespace
 
 namespace {
+// Dependency plan of the persistent exact-subsolver iteration (k_exact_iter):
+// groups of 8 consecutive subdomains per phase (the warp granularity of the
+// exact phase kernel); a group depends on every group of another phase that
+// writes one of its perimeter cells (RAW) and, symmetrically, on every group
+// that reads one of the cells it writes (WAR) or writes one of them too (WAW),
+// and on itself.
+mfp_status build_exact_persist(mfp_ctx* c) {
+  RankState& rs = c->ranks[0];
+  const RankPlan& p = rs.plan;
+  const LatticeGeom& L = p.lat;
+  ExactIterArgs& A = c->xargs;
+  A.g0[0] = 0;
+  for (int ph = 0; ph < 4; ph++) {
+    A.B[ph] = (int64_t)p.phase_anchor[ph].size();
+    A.g0[ph + 1] = A.g0[ph] + (A.B[ph] + 7) / 8;
+  }
+  const int64_t ng = A.g0[4];
+  if (ng == 0) return MFP_OK;
+  auto sub_of = [&](int ph, int64_t i, int& lx, int& ly, int& a, int& b) {
+    const uint32_t pk = p.phase_anchor[ph][(size_t)i];
+    a = (int)(pk & 0xffffu); b = (int)(pk >> 16); lx = kH * a; ly = kH * b;
+  };
+  std::vector<std::vector<int32_t>> wr(4, std::vector<int32_t>((size_t)L.cells, -1));
+  for (int ph = 0; ph < 4; ph++)
+    for (int64_t i = 0; i < A.B[ph]; i++) {
+      int lx, ly, a, b;
+      sub_of(ph, i, lx, ly, a, b);
+      const int32_t gid = (int32_t)(A.g0[ph] + i / 8);
+      for (int k = 1; k < kM; k++) {
+        wr[ph][(size_t)(L.offV + (int64_t)(a + 1) * L.strideV + ly + k)] = gid;
+        wr[ph][(size_t)((int64_t)(b + 1) * L.strideH + lx + k)] = gid;
+      }
+    }
+  std::vector<std::vector<int32_t>> dep((size_t)ng);
+  for (int ph = 0; ph < 4; ph++)
+    for (int64_t i = 0; i < A.B[ph]; i++) {
+      int lx, ly, a, b;
+      sub_of(ph, i, lx, ly, a, b);
+      const int32_t gid = (int32_t)(A.g0[ph] + i / 8);
+      // WAW: a cell written in two phases keeps the later phase's value
+      for (int k = 1; k < kM; k++) {
+        const int64_t wc[2] = {L.offV + (int64_t)(a + 1) * L.strideV + ly + k, (int64_t)(b + 1) * L.strideH + lx + k};
+        for (int64_t cell : wc)
+          for (int q = 0; q < 4; q++) {
+            if (q == ph) continue;
+            const int32_t w = wr[q][(size_t)cell];
+            if (w >= 0) { dep[(size_t)gid].push_back(w); dep[(size_t)w].push_back(gid); }
+          }
+      }
+      for (int t = 0; t <= kM; t++) {
+        const int64_t cells[4] = {(int64_t)b * L.strideH + lx + t, L.offV + (int64_t)(a + 2) * L.strideV + ly + t,
+                                  (int64_t)(b + 2) * L.strideH + lx + t, L.offV + (int64_t)a * L.strideV + ly + t};
+        for (int64_t cell : cells)
+          for (int q = 0; q < 4; q++) {
+            if (q == ph) continue;
+            const int32_t w = wr[q][(size_t)cell];
+            if (w >= 0) { dep[(size_t)gid].push_back(w); dep[(size_t)w].push_back(gid); }
+          }
+      }
+    }
+  std::vector<int32_t> off(1, 0), ids;
+  for (int64_t g = 0; g < ng; g++) {
+    auto& d = dep[(size_t)g];
+    d.push_back((int32_t)g);
+    std::sort(d.begin(), d.end());
+    d.erase(std::unique(d.begin(), d.end()), d.end());
+    ids.insert(ids.end(), d.begin(), d.end());
+    off.push_back((int32_t)ids.size());
+  }
+  CK(cudaMalloc((void**)&A.dep_off, off.size() * 4));
+  CK(cudaMalloc((void**)&A.dep_ids, std::max<size_t>(1, ids.size()) * 4));
+  CK(cudaMalloc((void**)&A.done, (size_t)ng * 8 + 64));
+  CK(cudaMemcpy((void*)A.dep_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+  if (!ids.empty()) CK(cudaMemcpy((void*)A.dep_ids, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemset(A.done, 0, (size_t)ng * 8 + 64));
+  A.iter_ctr = A.done + ng;
+  A.ticket = (unsigned int*)(A.done + ng + 1);
+  A.lat = rs.lat;
+  A.L = L;
+  for (int ph = 0; ph < 4; ph++) A.anchors[ph] = rs.anchors[ph];
+  A.HcT = c->dn.HcT;
+  A.K = 1;
+  c->exact_persist = true;
+  return MFP_OK;
+}
+
 // Before a rank frees its IPC-exported region (mfp_destroy), every stencil peer
 // must have finished its last pull from it: peer r stores consumed[r] = e into
 // THIS rank's region after reading exchange e (kernels_p2p.cu).  Poll those
@@ -1079,6 +1175,12 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
   }
   CK(cudaStreamSynchronize(s));
   CK(cudaGetLastError());
+  // MFP_PERSIST=1 (read per context): the exact subsolver on one rank runs each
+  // iteration as ONE persistent dataflow kernel instead of four phase kernels
+  // (NEXT-2; measured slower on one B200, so opt-in)
+  const char* pe = getenv("MFP_PERSIST");
+  if (cfg->subsolver == MFP_EXACT_LAPLACE && c->R == 1 && c->ranks.size() == 1 && pe && pe[0] == '1')
+    if (mfp_status st2 = build_exact_persist(c)) return st2;
   return MFP_OK;
 }
 
@@ -1104,6 +1206,8 @@ void mfp_destroy(mfp_ctx* c) {
     if (c->rank != MFP_ALL_RANKS) p2p_quiesce(c);
   }
   for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
+  for (void* q : {(void*)c->xargs.dep_off, (void*)c->xargs.dep_ids, (void*)c->xargs.done})
+    if (q) cudaFree(q);
   for (auto& rs : c->ranks) {
     if (rs.p2p) cudaFree(rs.p2p);
     if (rs.p2p_tab) cudaFree(rs.p2p_tab);

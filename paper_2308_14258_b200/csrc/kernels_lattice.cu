@@ -53,6 +53,81 @@ void launch_init_lattice(float* lat, const LatticeGeom& L, int nx, int ny, const
 constexpr int kExactWarps = 16;
 constexpr int kExactSub = 8;   // subdomains per warp per round
 
+// One warp's group of kExactSub consecutive subdomains [s0, s0 + 8) of a
+// phase: gather (16-byte loads; CG = L2-coherent loads for the persistent
+// kernel, whose lattice is written by other SMs within the launch), y = H_c g
+// with every H_c^T element feeding 8 FFMA2s, scatter onto the centre lines.
+template <bool CG>
+__device__ __forceinline__ void exact_group(float* __restrict__ lat, const LatticeGeom& L,
+                                            const uint32_t* __restrict__ anchors, int64_t s0, int64_t B,
+                                            const float2* sH, float* g, int lane) {
+  uint32_t pk[kExactSub];
+  float4 gv[kExactSub];
+#pragma unroll
+  for (int j = 0; j < kExactSub; j++) pk[j] = __ldg(anchors + (s0 + j < B ? s0 + j : B - 1));
+#pragma unroll
+  for (int j = 0; j < kExactSub; j++) {   // 8 gathers in flight
+    if constexpr (CG) {
+      int a, b;
+      unpack_anchor(pk[j], a, b);
+      const int lx = kH * a, ly = kH * b, edge = lane >> 3, t0 = 4 * (lane & 7);
+      if (edge == 0) gv[j] = __ldcg(reinterpret_cast<const float4*>(lat + (int64_t)b * L.strideH + lx + t0));
+      else if (edge == 1) gv[j] = __ldcg(reinterpret_cast<const float4*>(lat + L.offV + (int64_t)(a + 2) * L.strideV + ly + t0));
+      else {
+        const float* r = edge == 2 ? lat + (int64_t)(b + 2) * L.strideH + lx + kM - t0
+                                   : lat + L.offV + (int64_t)a * L.strideV + ly + kM - t0;
+        gv[j] = make_float4(__ldcg(r), __ldcg(r - 1), __ldcg(r - 2), __ldcg(r - 3));
+      }
+    } else {
+      gv[j] = gather4(lat, L, pk[j], lane);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kExactSub; j++) reinterpret_cast<float4*>(g + j * kNB)[lane] = gv[j];
+  __syncwarp();
+  f2 y[kExactSub];
+#pragma unroll
+  for (int j = 0; j < kExactSub; j++) y[j] = f2_make(0.f, 0.f);
+#pragma unroll 2
+  for (int k = 0; k < kNB; k += 4) {
+    f2 h[4];
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const float2 hv = sH[(k + t) * 32 + lane];
+      h[t] = f2_make(hv.x, hv.y);
+    }
+#pragma unroll
+    for (int j = 0; j < kExactSub; j++) {
+      const float4 gk = *reinterpret_cast<const float4*>(g + j * kNB + k);
+      y[j] = ffma2(h[0], f2_make(gk.x, gk.x), y[j]);
+      y[j] = ffma2(h[1], f2_make(gk.y, gk.y), y[j]);
+      y[j] = ffma2(h[2], f2_make(gk.z, gk.z), y[j]);
+      y[j] = ffma2(h[3], f2_make(gk.w, gk.w), y[j]);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < kExactSub; j++) {
+    if (s0 + j >= B) continue;
+    float y0, y1;
+    f2_split(y[j], y0, y1);
+    int a, b;
+    unpack_anchor(pk[j], a, b);
+    int64_t dup;
+    const int64_t c0 = centre_cell(a, b, lane, L.strideH, L.strideV, L.offV, &dup);
+    lat[c0] = y0;
+    if (dup >= 0) lat[dup] = y0;
+    if (lane + 32 < kQC) lat[centre_cell(a, b, lane + 32, L.strideH, L.strideV, L.offV, &dup)] = y1;
+  }
+}
+
+__device__ __forceinline__ void load_hct(float2* sH, const float* __restrict__ HcT) {
+  for (int i = threadIdx.x; i < kNB * 32; i += blockDim.x) {
+    const int k = i >> 5, l = i & 31;
+    sH[i] = make_float2(__ldg(HcT + k * 64 + l), __ldg(HcT + k * 64 + 32 + l));
+  }
+}
+
 __global__ void __launch_bounds__(kExactWarps * 32)
 k_exact_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ anchors,
               int64_t B, const float* __restrict__ HcT) {
@@ -62,59 +137,103 @@ k_exact_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict
   // updates both outputs (p = lane, lane + 32) of a subdomain
   float2* sH = reinterpret_cast<float2*>(ex_smem);
   float* sg = ex_smem + kNB * 64;                        // [warp][sub][k]
-  for (int i = threadIdx.x; i < kNB * 32; i += blockDim.x) {
-    const int k = i >> 5, l = i & 31;
-    sH[i] = make_float2(__ldg(HcT + k * 64 + l), __ldg(HcT + k * 64 + 32 + l));
-  }
+  load_hct(sH, HcT);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* g = sg + warp * kExactSub * kNB;
   const int64_t step = (int64_t)gridDim.x * kExactWarps * kExactSub;
-  for (int64_t s0 = ((int64_t)blockIdx.x * kExactWarps + warp) * kExactSub; s0 < B; s0 += step) {
-    uint32_t pk[kExactSub];
-    float4 gv[kExactSub];
-#pragma unroll
-    for (int j = 0; j < kExactSub; j++) pk[j] = __ldg(anchors + (s0 + j < B ? s0 + j : B - 1));
-#pragma unroll
-    for (int j = 0; j < kExactSub; j++) gv[j] = gather4(lat, L, pk[j], lane);   // 8 gathers in flight
-#pragma unroll
-    for (int j = 0; j < kExactSub; j++) reinterpret_cast<float4*>(g + j * kNB)[lane] = gv[j];
-    __syncwarp();
-    f2 y[kExactSub];
-#pragma unroll
-    for (int j = 0; j < kExactSub; j++) y[j] = f2_make(0.f, 0.f);
-#pragma unroll 2
-    for (int k = 0; k < kNB; k += 4) {
-      f2 h[4];
-#pragma unroll
-      for (int t = 0; t < 4; t++) {
-        const float2 hv = sH[(k + t) * 32 + lane];
-        h[t] = f2_make(hv.x, hv.y);
+  for (int64_t s0 = ((int64_t)blockIdx.x * kExactWarps + warp) * kExactSub; s0 < B; s0 += step)
+    exact_group<false>(lat, L, anchors, s0, B, sH, g, lane);
+}
+
+// ---- NEXT-2: the fully persistent exact-subsolver iteration (SURVEY §8(f)
+// "a fully persistent 4-phase kernel; dataflow flags replace grid barriers").
+// ONE launch runs K whole iterations: work item = (iteration, phase, group of 8
+// subdomains); warp w takes groups w, w + W, ... of every phase in stage order
+// (stage = 4 * iteration + phase).  A group may run stage (k, p) once every group of the
+// other phases that writes one of its perimeter cells (RAW) or reads one of the
+// cells it writes (WAR) has finished its latest stage before (k, p), and the
+// group itself has finished (k - 1, p): per-group completion stamps done[g] =
+// absolute stage + 1 (release after the group's stores; the waiting lanes poll
+// with acquire loads, one dependency per lane), so the four phase barriers of
+// an iteration become local waits and the phases of neighbouring iterations
+// overlap wherever the dependencies allow.  Same FMA order per output as
+// k_exact_phase: the field is bit-identical.  Deadlock freedom: every warp takes
+// its items in increasing stage order and every dependency points to an
+// earlier stage; the grid is at most one block per SM (co-resident) and the
+// launch is plainly stream-ordered.  A bounded spin (2^28 polls) traps instead
+// of hanging on a broken plan.
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(kExactWarps * 32)
+k_exact_iter(ExactIterArgs A) {
+  extern __shared__ __align__(16) float ex_smem[];
+  float2* sH = reinterpret_cast<float2*>(ex_smem);
+  float* sg = ex_smem + kNB * 64;
+  load_hct(sH, A.HcT);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* g = sg + warp * kExactSub * kNB;
+  // absolute iteration of this launch (device counter: graph replays advance it)
+  const int64_t iter0 = (int64_t)*(volatile const unsigned long long*)A.iter_ctr;
+  const int64_t W = (int64_t)gridDim.x * kExactWarps;
+  const int64_t wid = (int64_t)blockIdx.x * kExactWarps + warp;
+  // warp w takes groups w, w + W, ... of EVERY phase, in stage order: the i-th
+  // group of each phase covers about the same rows of the domain (anchors are
+  // row-major in every phase), so a group's dependencies are mostly its own
+  // warp's previous group or a neighbouring warp's, progressing in lock step
+  for (int64_t kk = 0; kk < A.K; kk++) {
+    const int64_t k = iter0 + kk;
+    for (int p = 0; p < 4; p++) {
+      for (int64_t gl = wid; gl < A.g0[p + 1] - A.g0[p]; gl += W) {
+        const int64_t gid = A.g0[p] + gl;
+        const unsigned long long stage = (unsigned long long)(4 * k + p);
+        // ---- wait for the dependencies' latest stage before (k, p)
+        const int d0 = __ldg(A.dep_off + gid), d1 = __ldg(A.dep_off + gid + 1);
+        for (int d = d0 + lane; d < d1; d += 32) {
+          const int h = __ldg(A.dep_ids + d);
+          int q = 0;
+          while (h >= A.g0[q + 1]) q++;
+          // latest run of h before (k, p): (k, q) if q < p, else (k - 1, q); stamps are stage + 1
+          const long long need = (q < p ? 4 * k + q : 4 * (k - 1) + q) + 1;
+          if (need > 0) {
+            unsigned int spins = 0;
+            while ((long long)ld_acquire_gpu(A.done + h) < need) {
+              __nanosleep(32);
+              if (++spins > (1u << 28)) __trap();
+            }
+          }
+        }
+        __syncwarp();
+        exact_group<true>(A.lat, A.L, A.anchors[p], gl * kExactSub, A.B[p], sH, g, lane);
+        __syncwarp();
+        __threadfence();   // this warp's scatter before the stamp
+        if (lane == 0)
+          asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(A.done + gid), "l"(stage + 1) : "memory");
       }
-#pragma unroll
-      for (int j = 0; j < kExactSub; j++) {
-        const float4 gk = *reinterpret_cast<const float4*>(g + j * kNB + k);
-        y[j] = ffma2(h[0], f2_make(gk.x, gk.x), y[j]);
-        y[j] = ffma2(h[1], f2_make(gk.y, gk.y), y[j]);
-        y[j] = ffma2(h[2], f2_make(gk.z, gk.z), y[j]);
-        y[j] = ffma2(h[3], f2_make(gk.w, gk.w), y[j]);
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < kExactSub; j++) {
-      if (s0 + j >= B) continue;
-      float y0, y1;
-      f2_split(y[j], y0, y1);
-      int a, b;
-      unpack_anchor(pk[j], a, b);
-      int64_t dup;
-      const int64_t c0 = centre_cell(a, b, lane, L.strideH, L.strideV, L.offV, &dup);
-      lat[c0] = y0;
-      if (dup >= 0) lat[dup] = y0;
-      if (lane + 32 < kQC) lat[centre_cell(a, b, lane + 32, L.strideH, L.strideV, L.offV, &dup)] = y1;
     }
   }
+  // the last block to finish advances the iteration counter for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(A.ticket, 1u) == gridDim.x - 1) {
+      *A.ticket = 0u;
+      *A.iter_ctr = (unsigned long long)(iter0 + A.K);
+    }
+  }
+}
+
+void launch_exact_iter(const ExactIterArgs& a, cudaStream_t s) {
+  if (a.K <= 0 || a.g0[4] <= 0) return;
+  int64_t blocks = (a.g0[4] + kExactWarps - 1) / kExactWarps;
+  if (blocks > num_sms()) blocks = num_sms();   // one co-resident block per SM
+  const size_t smem = sizeof(float) * ((size_t)kNB * 64 + (size_t)kExactWarps * kExactSub * kNB);
+  k_exact_iter<<<(int)blocks, kExactWarps * 32, smem, s>>>(a);
 }
 
 void launch_exact_phase(float* lat, const LatticeGeom& L, const uint32_t* anchors, int64_t B,
@@ -129,6 +248,8 @@ void launch_exact_phase(float* lat, const LatticeGeom& L, const uint32_t* anchor
 
 void exact_kernel_attributes() {
   cudaFuncSetAttribute(k_exact_phase, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(float) * ((size_t)kNB * 64 + (size_t)kExactWarps * kExactSub * kNB)));
+  cudaFuncSetAttribute(k_exact_iter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(float) * ((size_t)kNB * 64 + (size_t)kExactWarps * kExactSub * kNB)));
 }
 

@@ -181,6 +181,24 @@ void launch_exact_phase(float* lat, const LatticeGeom& L, const uint32_t* anchor
 void launch_exact_general(const float* lat, const LatticeGeom& L, const uint32_t* lat_anchors,
                           const float* gb, int64_t B, int q, const float* HT, const Sink& sink,
                           cudaStream_t s);
+// NEXT-2: the persistent exact-subsolver iteration (kernels_lattice.cu
+// k_exact_iter): K iterations per launch, per-group dataflow stamps instead of
+// phase barriers (single-rank contexts).
+struct ExactIterArgs {
+  float* lat;
+  LatticeGeom L;
+  const uint32_t* anchors[4];
+  int64_t B[4];
+  int64_t g0[5];                 // first group id of each phase (groups phase-major), g0[4] = groups
+  const int32_t* dep_off;        // [groups + 1]
+  const int32_t* dep_ids;        // dependency group ids (the group itself included)
+  unsigned long long* done;      // [groups] absolute stage + 1 of the last completed run
+  unsigned long long* iter_ctr;  // absolute iteration of the next launch (advanced on device)
+  unsigned int* ticket;          // last-block ticket
+  const float* HcT;
+  int K;                         // iterations per launch
+};
+void launch_exact_iter(const ExactIterArgs& a, cudaStream_t s);
 void launch_chain_fp32(const float* z, int64_t B, int q, const DevNet& net, const Sink& sink,
                        cudaStream_t s);
 bool chain_tc_available();
