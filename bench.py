@@ -57,9 +57,10 @@ def parse():
     p.add_argument("--no-converge", action="store_true")
     p.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                    help="strong: C5 (4097^2) at every N (default); weak: a 1024x2048 block per GPU")
-    p.add_argument("--halo", default="nccl", choices=["nccl", "p2p"],
-                   help="halo transport for N > 1: grouped NCCL send/recv (default) or the peer-memory "
-                        "kernels of mfp_p2p_open (NEXT-2; IPC handles all-gathered over the process group)")
+    p.add_argument("--halo", default="nccl", choices=["nccl", "p2p", "put"],
+                   help="halo transport for N > 1: grouped NCCL send/recv (default), the peer-memory "
+                        "pack + pull kernels of mfp_p2p_open, or halo puts from the chain epilogue "
+                        "(mfp_p2p_set_mode PUT) (NEXT-2; IPC handles all-gathered over the process group)")
     p.add_argument("--no-extras", action="store_true",
                    help="skip the legs after the timed region (e2e, sweep, boundary IO, CPU baseline): "
                         "used for the ncu launch list of the step")
@@ -449,10 +450,12 @@ def main():
     w = random_weights(0)
     stream = torch.cuda.Stream(device=dev)
     m = mfp.Mfp(cfg, net, w, rank=rank, nccl_comm=comm, stream=stream)
-    if world > 1 and args.halo == "p2p":
+    if world > 1 and args.halo in ("p2p", "put"):
         handles = [None] * world
         dist.all_gather_object(handles, mfp.mfp_p2p_export(m.ctx))
         mfp.mfp_p2p_open(m.ctx, handles)
+        if args.halo == "put":
+            mfp.mfp_p2p_set_mode(m.ctx, mfp.P2P_PUT)
         barrier()
     g_host = gp_boundary(nx, ny, 0)
     g_dev = torch.from_numpy(g_host).to(dev)
