@@ -1511,6 +1511,8 @@ mfp_status mfp_p2p_set_mode(mfp_ctx* c, int32_t mode) {
           base += (int64_t)x.recv_idx.size();
         }
         if (!found) return fail(c, MFP_ERR_INVALID, "p2p_set_mode: asymmetric stencil");
+        if (base + (int64_t)p.peers[i].send_idx.size() >= (1 << 24) || p.peers.size() > 127)
+          return fail(c, MFP_ERR_INVALID, "p2p_set_mode: put slot / peer index out of the 24 / 7-bit encoding");
         const auto& sp = p.peers[i];
         for (size_t k = 0; k < sp.send_idx.size(); k++) {
           if (on_boundary(sp.send_x[k], sp.send_y[k])) continue;   // never rewritten: no put
