@@ -211,6 +211,11 @@ const char* mfp_last_error(const mfp_ctx* ctx);  /* never NULL */
  * rep->last_delta).  u_out: HOST (ny+1)*(nx+1) fp32, required on rank 0
  * (and for MFP_ALL_RANKS), ignored elsewhere; may be NULL to skip the final
  * phase.  rep nullable.  Collective over the communicator.
+ * Execution: whole blocks of check_every iterations replay captured CUDA graphs;
+ * with tol > 0 on a single-process context (one rank or MFP_ALL_RANKS) the
+ * stopping rule itself runs on the device — one graph with a WHILE node repeats
+ * the block until delta <= tol, a non-finite prediction or the budget — so a
+ * converging solve makes no host round trip per block (same field bit for bit).
  * Returns OK, NOT_CONVERGED (u written), NONFINITE, CUDA, NCCL, STATE. */
 mfp_status mfp_solve(mfp_ctx* ctx, const float* g, int32_t max_iters, float tol,
                      float* u_out, mfp_report* rep);
