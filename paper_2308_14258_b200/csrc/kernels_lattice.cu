@@ -57,16 +57,16 @@ constexpr int kExactSub = 8;   // subdomains per warp per round
 // phase: gather (16-byte loads; CG = L2-coherent loads for the persistent
 // kernel, whose lattice is written by other SMs within the launch), y = H_c g
 // with every H_c^T element feeding 8 FFMA2s, scatter onto the centre lines.
-template <bool CG>
+template <bool CG, int SUB = kExactSub>
 __device__ __forceinline__ void exact_group(float* __restrict__ lat, const LatticeGeom& L,
                                             const uint32_t* __restrict__ anchors, int64_t s0, int64_t B,
                                             const float2* sH, float* g, int lane) {
-  uint32_t pk[kExactSub];
-  float4 gv[kExactSub];
+  uint32_t pk[SUB];
+  float4 gv[SUB];
 #pragma unroll
-  for (int j = 0; j < kExactSub; j++) pk[j] = __ldg(anchors + (s0 + j < B ? s0 + j : B - 1));
+  for (int j = 0; j < SUB; j++) pk[j] = __ldg(anchors + (s0 + j < B ? s0 + j : B - 1));
 #pragma unroll
-  for (int j = 0; j < kExactSub; j++) {   // 8 gathers in flight
+  for (int j = 0; j < SUB; j++) {   // 8 gathers in flight
     if constexpr (CG) {
       int a, b;
       unpack_anchor(pk[j], a, b);
@@ -83,11 +83,11 @@ __device__ __forceinline__ void exact_group(float* __restrict__ lat, const Latti
     }
   }
 #pragma unroll
-  for (int j = 0; j < kExactSub; j++) reinterpret_cast<float4*>(g + j * kNB)[lane] = gv[j];
+  for (int j = 0; j < SUB; j++) reinterpret_cast<float4*>(g + j * kNB)[lane] = gv[j];
   __syncwarp();
-  f2 y[kExactSub];
+  f2 y[SUB];
 #pragma unroll
-  for (int j = 0; j < kExactSub; j++) y[j] = f2_make(0.f, 0.f);
+  for (int j = 0; j < SUB; j++) y[j] = f2_make(0.f, 0.f);
 #pragma unroll 2
   for (int k = 0; k < kNB; k += 4) {
     f2 h[4];
@@ -97,7 +97,7 @@ __device__ __forceinline__ void exact_group(float* __restrict__ lat, const Latti
       h[t] = f2_make(hv.x, hv.y);
     }
 #pragma unroll
-    for (int j = 0; j < kExactSub; j++) {
+    for (int j = 0; j < SUB; j++) {
       const float4 gk = *reinterpret_cast<const float4*>(g + j * kNB + k);
       y[j] = ffma2(h[0], f2_make(gk.x, gk.x), y[j]);
       y[j] = ffma2(h[1], f2_make(gk.y, gk.y), y[j]);
@@ -107,7 +107,7 @@ __device__ __forceinline__ void exact_group(float* __restrict__ lat, const Latti
   }
   __syncwarp();
 #pragma unroll
-  for (int j = 0; j < kExactSub; j++) {
+  for (int j = 0; j < SUB; j++) {
     if (s0 + j >= B) continue;
     float y0, y1;
     f2_split(y[j], y0, y1);
@@ -128,6 +128,7 @@ __device__ __forceinline__ void load_hct(float2* sH, const float* __restrict__ H
   }
 }
 
+template <int SUB>
 __global__ void __launch_bounds__(kExactWarps * 32)
 k_exact_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ anchors,
               int64_t B, const float* __restrict__ HcT) {
@@ -140,10 +141,10 @@ k_exact_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict
   load_hct(sH, HcT);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* g = sg + warp * kExactSub * kNB;
-  const int64_t step = (int64_t)gridDim.x * kExactWarps * kExactSub;
-  for (int64_t s0 = ((int64_t)blockIdx.x * kExactWarps + warp) * kExactSub; s0 < B; s0 += step)
-    exact_group<false>(lat, L, anchors, s0, B, sH, g, lane);
+  float* g = sg + warp * SUB * kNB;
+  const int64_t step = (int64_t)gridDim.x * kExactWarps * SUB;
+  for (int64_t s0 = ((int64_t)blockIdx.x * kExactWarps + warp) * SUB; s0 < B; s0 += step)
+    exact_group<false, SUB>(lat, L, anchors, s0, B, sH, g, lane);
 }
 
 // ---- NEXT-2: the fully persistent exact-subsolver iteration (SURVEY §8(f)
@@ -236,19 +237,50 @@ void launch_exact_iter(const ExactIterArgs& a, cudaStream_t s) {
   k_exact_iter<<<(int)blocks, kExactWarps * 32, smem, s>>>(a);
 }
 
+// Subdomains per warp: 8 (every H_c^T smem load feeds 8 FFMA2) while the phase
+// still gives (about) a block of 16 warps per SM; smaller phases — a rank's
+// share at 4-8 GPUs — use 4 / 2 / 1 per warp so the grid still spreads over the
+// SMs (at 8 subdomains per warp a 2,048-subdomain phase ran on 16 SMs).
+// MFP_EXACT_SUB=1|2|4|8 forces one (A/B).
+static int exact_sub(int64_t B) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("MFP_EXACT_SUB");
+    const int v = e ? atoi(e) : 0;
+    forced = (v == 1 || v == 2 || v == 4 || v == 8) ? v : 0;
+  }
+  if (forced) return forced;
+  const int64_t sms = num_sms();
+  int sub = 8;
+  while (sub > 1 && (B + kExactWarps * sub - 1) / (kExactWarps * sub) < (3 * sms) / 4) sub >>= 1;
+  return sub;
+}
+
+static size_t exact_smem(int sub) { return sizeof(float) * ((size_t)kNB * 64 + (size_t)kExactWarps * sub * kNB); }
+
 void launch_exact_phase(float* lat, const LatticeGeom& L, const uint32_t* anchors, int64_t B,
                         const float* HcT, cudaStream_t s) {
   if (B <= 0) return;
-  const int per_block = kExactWarps * kExactSub;
+  const int sub = exact_sub(B);
+  const int per_block = kExactWarps * sub;
   int64_t blocks = (B + per_block - 1) / per_block;
-  if (blocks > num_sms()) blocks = num_sms();
-  const size_t smem = sizeof(float) * ((size_t)kNB * 64 + (size_t)kExactWarps * kExactSub * kNB);
-  k_exact_phase<<<(int)blocks, kExactWarps * 32, smem, s>>>(lat, L, anchors, B, HcT);
+  const int per_sm = sub >= 8 ? 1 : 2;   // 96 KB of smem at 8 per warp, <= 64 KB below
+  if (blocks > per_sm * num_sms()) blocks = per_sm * num_sms();
+#define MFP_EX(S) k_exact_phase<S><<<(int)blocks, kExactWarps * 32, exact_smem(S), s>>>(lat, L, anchors, B, HcT)
+  switch (sub) {
+    case 1: MFP_EX(1); break;
+    case 2: MFP_EX(2); break;
+    case 4: MFP_EX(4); break;
+    default: MFP_EX(8); break;
+  }
+#undef MFP_EX
 }
 
 void exact_kernel_attributes() {
-  cudaFuncSetAttribute(k_exact_phase, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(sizeof(float) * ((size_t)kNB * 64 + (size_t)kExactWarps * kExactSub * kNB)));
+  cudaFuncSetAttribute(k_exact_phase<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(8));
+  cudaFuncSetAttribute(k_exact_phase<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(4));
+  cudaFuncSetAttribute(k_exact_phase<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(2));
+  cudaFuncSetAttribute(k_exact_phase<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(1));
   cudaFuncSetAttribute(k_exact_iter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(float) * ((size_t)kNB * 64 + (size_t)kExactWarps * kExactSub * kNB)));
 }
