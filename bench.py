@@ -69,16 +69,22 @@ def parse():
 
 # ------------------------------------------------------------------ d = 256 leg
 def wide_leg(mfp, torch, stream, cfg, g_dev, u_dev, flush, ppi, peaks, T=16, steps=3, D=256, gelu=1,
-             kernel="k_chain_tc2w (d = 256 hidden GEMM chain)"):
+             kernel="k_chain_tc2w (d = 256 hidden GEMM chain)", rank=0, comm=None,
+             max_over_ranks=lambda x: x, barrier=lambda: None):
     """The same MFP with another SDNet variant — by default the wide SDNet (d = 256,
     SURVEY §8(b)/(d) "report both d values"); with cfg.precision = FP16X the
     accuracy mode: predictions/s over `steps` solves of T iterations (device
     events, L2 flushed between solves, outside the events) and the roofline of its
-    chain (rows x 3 x 2 x d^2 FLOP per launch / the launch's event time)."""
+    chain (rows x 3 x 2 x d^2 FLOP per launch / the launch's event time).  At N > 1
+    every rank runs it on its share (collective), value = whole-job predictions /
+    max-over-ranks device time, so the scaling run carries the d = 256 curve too."""
     from mfp_inputs import random_weights
-    mw = mfp.Mfp(cfg, mfp.make_net(d=D, gelu=gelu), random_weights(0, d=D), stream=stream)
+    mw = mfp.Mfp(cfg, mfp.make_net(d=D, gelu=gelu), random_weights(0, d=D), rank=rank, nccl_comm=comm,
+                 stream=stream)
     for _ in range(2):
         mw.solve_device(g_dev, T, 0.0, u_dev)
+    torch.cuda.synchronize()
+    barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for i in range(steps):
         with torch.cuda.stream(stream):
@@ -88,7 +94,7 @@ def wide_leg(mfp, torch, stream, cfg, g_dev, u_dev, flush, ppi, peaks, T=16, ste
         with torch.cuda.stream(stream):
             ev[i][1].record(stream)
     torch.cuda.synchronize()
-    ms = sum(a.elapsed_time(b) for a, b in ev)
+    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev))
     prof = mw.profile(4)
     chain_ms = prof.chain_ms_total / max(prof.chain_launches, 1)
     flop = prof.chain_rows / max(prof.chain_launches, 1) * 3 * 2 * D * D
@@ -669,8 +675,10 @@ def main():
                 mf.close()
 
     bio = sweep = wide = acc = None
+    if tensor:   # every N: the scaling run carries the d = 256 curve
+        wide = wide_leg(mfp, torch, stream, cfg, g_dev, u_dev, flush, ppi, peaks, rank=rank, comm=comm,
+                        max_over_ranks=max_over_ranks, barrier=barrier)
     if world == 1 and tensor:
-        wide = wide_leg(mfp, torch, stream, cfg, g_dev, u_dev, flush, ppi, peaks)
         # the tensor-core accuracy mode (split fp16 activations + accurate GELU;
         # holds 3e-3 per field with trained weights, tests/test_gpu_fp16x.py): its
         # throughput cost on the same workload
