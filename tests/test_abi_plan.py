@@ -57,6 +57,27 @@ def test_invalid_configs():
 
 def test_param_count():
     assert mfp.mfp_param_count(mfp.make_net()) == oracle.param_count(oracle.NetShape()) == 66522
+    assert mfp.mfp_param_count(mfp.make_net(d=256)) == oracle.param_count(oracle.NetShape(d=256))
+
+
+def test_net_and_precision_validation():
+    """d = 128 | 256; gelu 0 / 1 / 2 (exact, classic tanh, accurate
+    tanh); precisions FP32 / BF16 / FP16 / FP16X — anything else is INVALID."""
+    cfg = mfp.make_config(64, 64)
+    w128 = mfp.mfp_workspace_size(cfg, mfp.make_net(), 0)
+    w256 = mfp.mfp_workspace_size(cfg, mfp.make_net(d=256), 0)
+    assert w256 > w128 > 0
+    for gelu in (0, 1, 2):
+        assert mfp.mfp_workspace_size(cfg, mfp.make_net(gelu=gelu), 0) == w128
+    for net in (mfp.make_net(d=192), mfp.make_net(d=64), mfp.make_net(gelu=3), mfp.make_net(n_hidden=4)):
+        with pytest.raises(mfp.MfpError) as e:
+            mfp.mfp_workspace_size(cfg, net, 0)
+        assert e.value.status == 1
+    for prec in (mfp.FP32, mfp.BF16, mfp.FP16, mfp.FP16X):
+        assert mfp.mfp_workspace_size(mfp.make_config(64, 64, precision=prec), mfp.make_net(), 0) > 0
+    with pytest.raises(mfp.MfpError) as e:
+        mfp.mfp_workspace_size(mfp.make_config(64, 64, precision=4), mfp.make_net(), 0)
+    assert e.value.status == 1
 
 
 @pytest.mark.parametrize("K", [2, 4, 16])

@@ -96,6 +96,13 @@ def test_fp16x_wrand_batch_many_tiles(lib, B):
     m.close()
 
 
+def test_fp16x_rejects_d256(lib):
+    cfg = lib.make_config(128, 128, precision=lib.FP16X, subsolver=lib.SDNET, check_every=1)
+    with pytest.raises(lib.MfpError) as e:
+        lib.Mfp(cfg, lib.make_net(d=256, gelu=2), random_weights(0, d=256))
+    assert e.value.status == 1
+
+
 @pytest.mark.parametrize("precision", [1, 2])
 def test_accurate_gelu_single_rounding_modes(lib, precision):
     """gelu = 2 on the bf16 / fp16 chains (k_chain_tc2 GELU = 2): field parity at
