@@ -425,16 +425,27 @@ void launch_unpack(float* lat, const int32_t* idx, int64_t n, const float* buf, 
 // Atomic-subdomain boundary lines (x or y a multiple of m) of the owned block
 // take the lattice values (DESIGN.md §2 reading F1); interior points are
 // written by the final-phase predictions.
+// Only the line points are visited (≈ 1/16 of the block): the rows y ≡ 0 (mod m)
+// x-fastest from the horizontal lines, then the columns x ≡ 0 (mod m)
+// y-fastest from the vertical lines (crossings written twice, same value).  The
+// block origin (X0, Y0) is a multiple of m.
 __global__ void k_final_lines(const float* __restrict__ lat, LatticeGeom L, int X0, int Y0, int bw,
                               int bh, float* __restrict__ field, int ld) {
-  const int64_t n = (int64_t)bw * bh;
+  const int nr = (bh + kM - 1) / kM, nc = (bw + kM - 1) / kM;
+  const int64_t na = (int64_t)nr * bw, n = na + (int64_t)nc * bh;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(t / bw), i = (int)(t % bw);
-    const int x = X0 + i, y = Y0 + j;
+    int i, j;
     float v;
-    if (y % kM == 0) v = lat[(int64_t)((y - L.RY0) / kH) * L.strideH + (x - L.RX0)];
-    else if (x % kM == 0) v = lat[L.offV + (int64_t)((x - L.RX0) / kH) * L.strideV + (y - L.RY0)];
-    else continue;
+    if (t < na) {
+      j = kM * (int)(t / bw);
+      i = (int)(t % bw);
+      v = lat[(int64_t)((Y0 + j - L.RY0) / kH) * L.strideH + (X0 + i - L.RX0)];
+    } else {
+      const int64_t u = t - na;
+      i = kM * (int)(u / bh);
+      j = (int)(u % bh);
+      v = lat[L.offV + (int64_t)((X0 + i - L.RX0) / kH) * L.strideV + (Y0 + j - L.RY0)];
+    }
     field[(int64_t)j * ld + i] = v;
   }
 }
