@@ -18,6 +18,8 @@
 
 #include <time.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "mfp_internal.h"
 
 
@@ -143,6 +145,15 @@ bool mfp::pdl_enabled() {
 }
 
 namespace {
+
+// NVTX ranges (header-only NVTX 3: no-ops unless a tool such as ncu --nvtx or
+// nsys attaches) around the host-side steps of a solve, so a profile of any
+// caller shows init / blocks of c iterations / convergence loop / final phase /
+// halo exchange / batch calls by name.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 const int kKindGather = 0, kKindChain = 1, kKindExact = 2, kKindHalo = 3, kKindDelta = 4;
 
@@ -488,6 +499,7 @@ mfp_status exchange_begin_p2p(mfp_ctx* c) {
 
 mfp_status exchange_begin(mfp_ctx* c) {
   if (c->R == 1) return MFP_OK;
+  Nvtx nv("mfp: halo exchange (a7)");
   if (c->p2p) return exchange_begin_p2p(c);
   for (auto& rs : c->ranks) {
     launch_pack(rs.lat, rs.send_idx, rs.nsend, rs.sendbuf, c->stream);
@@ -605,6 +617,7 @@ mfp_status reduce_delta(mfp_ctx* c, float* delta, bool* nonfinite) {
 // ends with the snapshot-delta-allreduce of a check iteration (the pinned D2H
 // copy of delta is a graph node; the host reads it after the launch).
 mfp_status run_block(mfp_ctx* c, int kind) {
+  Nvtx nv(kind ? "mfp: block of c iterations + delta (graph)" : "mfp: block of c iterations (graph)");
   const int ce = c->cfg.check_every;
   if (!c->gexec[kind]) {
     const int l0 = c->launches;
@@ -655,6 +668,7 @@ bool device_loop_enabled() {
 }
 
 mfp_status run_loop(mfp_ctx* c, int it, int t, float tol) {
+  Nvtx nv("mfp: on-device convergence loop (WHILE graph)");
   const int ce = c->cfg.check_every;
   if (!c->gloop) {
     cudaGraph_t g = nullptr;
@@ -741,6 +755,7 @@ mfp_status final_phase_banded(mfp_ctx* c, float* u) {
 }
 
 mfp_status final_phase(mfp_ctx* c, float* u) {
+  Nvtx nv("mfp: final phase (a9)");
   if (c->pipe_host && c->R == 1 && c->cfg.subsolver == MFP_SDNET) return final_phase_banded(c, u);
   const int W = c->cfg.nx + 1;
   for (auto& rs : c->ranks) {
@@ -801,6 +816,7 @@ mfp_status final_phase(mfp_ctx* c, float* u) {
 
 mfp_status solve_impl(mfp_ctx* c, const float* g_dev, int32_t t, float tol, float* u_dev, bool do_final,
                       mfp_report* rep) {
+  Nvtx nv("mfp_solve");
   if (c->poisoned) return MFP_ERR_STATE;
   if (t < 1 || !(tol >= 0.f)) return fail(c, MFP_ERR_INVALID, "max_iters >= 1 and tol >= 0 required");
   struct Events {   // destroyed on every return path
@@ -1265,6 +1281,7 @@ mfp_status mfp_solve(mfp_ctx* c, const float* g, int32_t max_iters, float tol, f
 
 mfp_status mfp_sdnet_batch(mfp_ctx* c, const float* gb, int64_t B, int32_t query_set, float* out, void* stream) {
   if (!c) return MFP_ERR_INVALID;
+  Nvtx nv("mfp_sdnet_batch");
   if (c->poisoned) return MFP_ERR_STATE;
   if (B < 0 || (B > 0 && (!gb || !out)) || (query_set != MFP_QUERY_CENTRE && query_set != MFP_QUERY_INTERIOR))
     return fail(c, MFP_ERR_INVALID, "bad sdnet_batch arguments");
