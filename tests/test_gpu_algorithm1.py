@@ -81,3 +81,27 @@ def test_trained_weights_drive_the_hot_path(lib, precision, tol):
     out = m.sdnet_batch(g, 0).cpu().numpy()
     assert np.max(np.abs(out - ref)) <= tol * np.max(np.abs(ref))
     m.close()
+
+
+def test_graph_step_matches_eager():
+    """training/graph_step.py: the step replayed as one CUDA graph (device-side
+    LAMB state) reproduces the eager step's weights over 8 steps on the same
+    batches, to fp32 rounding."""
+    from training.graph_step import DeviceLamb, GraphStep
+    torch.manual_seed(2)
+    net_e = SDNet().cuda()
+    net_g = SDNet().cuda()
+    net_g.load_flat(net_e.flat())
+    prob = Problem(torch.device("cuda"), torch.float32, n_interior=32, n_colloc=16)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(5)
+    batches = [prob.batch(64, gen) for _ in range(8)]
+    opt_e = Lamb(net_e.parameters(), lr=2e-3)
+    opt_g = DeviceLamb(list(net_g.parameters()), lr=2e-3)
+    gs = GraphStep(net_g, opt_g, batches[0], pde_weight=1e-3)
+    for b in batches:
+        ld_e, _ = train_step(net_e, opt_e, b, pde_weight=1e-3)
+        ld_g, _ = gs.step(b)
+        assert abs(float(ld_g) - ld_e) <= 1e-4 * abs(ld_e) + 1e-7
+    we, wg = net_e.flat(), net_g.flat()
+    assert np.max(np.abs(we - wg)) <= 1e-4 * np.max(np.abs(we))

@@ -124,3 +124,23 @@ def test_lr_schedule_and_worker_scaling():
     assert abs(scale_for_workers(1e-3, 1e-3, 4)[0] - 2e-3) < 1e-15  # p = 4: sqrt rule
     assert abs(scale_for_workers(1e-3, 1e-3, 16)[1] - 0.016) < 1e-15  # p = 16: linear warmup rule
     assert scale_for_workers(1e-3, 0.1, 16)[1] == 0.5
+
+
+def test_device_lamb_equals_lamb():
+    """training/graph_step.py DeviceLamb (device-resident t, lr, trust ratio; the
+    CUDA-graph-capturable form) makes the same LAMB updates as Lamb."""
+    from training.graph_step import DeviceLamb
+    torch.manual_seed(11)
+    a, b = SDNet().double(), SDNet().double()
+    b.load_flat(a.flat())
+    oa, ob = Lamb(a.parameters(), lr=2e-3, weight_decay=1e-4), DeviceLamb(list(b.parameters()), lr=2e-3,
+                                                                          weight_decay=1e-4)
+    for it in range(5):
+        g = torch.Generator().manual_seed(it)
+        for pa, pb in zip(a.parameters(), b.parameters()):
+            grad = torch.randn(pa.shape, dtype=torch.float64, generator=g)
+            pa.grad = grad.clone()
+            pb.grad = grad.clone()
+        oa.step()
+        ob.step()
+    assert np.max(np.abs(a.flat() - b.flat())) < 1e-12

@@ -282,6 +282,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--init", default=None)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--graph", action="store_true",
+                    help="replay each step as one CUDA graph (training/graph_step.py; device-side LAMB state)")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -304,9 +306,22 @@ def main():
     t0, log = time.time(), []
     if dev.type == "cuda":
         torch.cuda.synchronize()
+    gstep = None
+    if a.graph and dev.type == "cuda":
+        from training.graph_step import DeviceLamb, GraphStep
+        opt = DeviceLamb(list(net.parameters()), lr=max_lr)
+        gstep = GraphStep(net, opt, prob.batch(a.batch, gen), a.pde_weight, world)
     for step in range(a.steps):
+        lr = lr_at(max_lr, warmup, a.decay, step, a.steps)
+        if gstep is not None:
+            opt.set_lr(lr)
+            ld, lp = (float(x) for x in gstep.step(prob.batch(a.batch, gen)))
+            if rank == 0 and (step % 100 == 0 or step == a.steps - 1):
+                log.append((step, ld, lp))
+                print(f"step {step} data {ld:.3e} pde {lp:.3e}", flush=True)
+            continue
         for grp in opt.param_groups:
-            grp["lr"] = lr_at(max_lr, warmup, a.decay, step, a.steps)
+            grp["lr"] = lr
         ld, lp = train_step(net, opt, prob.batch(a.batch, gen), a.pde_weight, world)
         if rank == 0 and (step % 100 == 0 or step == a.steps - 1):
             log.append((step, ld, lp))
