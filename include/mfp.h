@@ -186,7 +186,8 @@ mfp_status mfp_param_count(const mfp_sdnet_desc* net, int32_t m, size_t* n);
  * exact-solver matrices when subsolver == MFP_EXACT_LAPLACE), precompute the
  * per-query tables Q = X W2^T + b1 (Eq. 5).  `params` may be NULL iff
  * subsolver == MFP_EXACT_LAPLACE.  rank in [0, Py*Px) with a caller-owned
- * ncclComm_t (`nccl_comm`, NULL iff Py*Px == 1), or MFP_ALL_RANKS with
+ * ncclComm_t (`nccl_comm`; required for Py*Px > 1, optional — a 1-rank communicator that
+ * exercises the collective paths — for Py*Px == 1), or MFP_ALL_RANKS with
  * nccl_comm == NULL.  `stream` is a caller-owned cudaStream_t (NULL = legacy).
  * Errors: INVALID, NOT_TILEABLE, NONFINITE (params), WORKSPACE, CUDA. */
 mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net,

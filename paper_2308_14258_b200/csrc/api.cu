@@ -1096,8 +1096,11 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
   c->cfg = *cfg; c->net = *net; c->rank = rank; c->R = gp.R;
   if (gp.R > 1 && rank != MFP_ALL_RANKS && !nccl_comm)
     return fail(c, MFP_ERR_INVALID, "nccl_comm required for a multi-rank grid");
-  if ((gp.R == 1 || rank == MFP_ALL_RANKS) && nccl_comm)
-    return fail(c, MFP_ERR_INVALID, "nccl_comm must be NULL for single-rank / MFP_ALL_RANKS");
+  // (R == 1 may take a 1-rank communicator: the collective code paths — digest
+  // agreement, delta allreduce inside the graphs, the NCCL watchdog — then run
+  // on one GPU, which is how they are tested without a second device)
+  if (rank == MFP_ALL_RANKS && nccl_comm)
+    return fail(c, MFP_ERR_INVALID, "nccl_comm must be NULL for MFP_ALL_RANKS");
   c->comm = (ncclComm_t)nccl_comm;
   c->stream = (cudaStream_t)stream;
   if (cfg->subsolver == MFP_SDNET) {
