@@ -1,8 +1,9 @@
 """GPU parity of the d = 256 SDNet variant (SURVEY §8(b) d = 128 | 256, G7; PAPER.md
 P:239-241 fixes the architecture's form, not its width).
 
-The wide variant runs its own kernels: the SIMT embed and fp32 chain templated on
-d (weights streamed through shared memory in K-chunks at d = 256) and the CTA-pair
+The wide variant runs its own kernels: the tensor-core embed with two W1 halves
+through one TMA-reloaded buffer, the SIMT embed and fp32 chain templated on d
+(weights streamed through shared memory in K-chunks at d = 256), and the CTA-pair
 tcgen05 chain `k_chain_tc2w` (M = N = 256, two tile slots, weight K-chunks streamed
 by TMA through a four-stage ring).  Same bars as d = 128 (north_star): fp32
 <= 1e-5 scale-relative, bf16 / fp16 <= 3e-3 per field after K iterations; batch
@@ -109,4 +110,27 @@ def test_d256_c3_lattice_bf16(lib, w):
                          final=False)
     L = lattice_to_global(m.lines(), nx, ny)
     assert rel_err(L, ref.lines, line_mask(nx, ny)) <= TC_TOL
+    m.close()
+
+
+@pytest.mark.parametrize("d", [128, 256])
+@pytest.mark.parametrize("nh", [1, 2])
+@pytest.mark.parametrize("precision", [1, 3])
+def test_fewer_hidden_layers(lib, d, nh, precision):
+    """n_hidden = 1, 2 (mfp_sdnet_desc allows 1..3) through every tensor-core chain:
+    the weight ring / resident images, the layer loop and the head after fewer
+    layers, vs the oracle (FP16X is d = 128 only)."""
+    import torch
+    if precision == 3 and d == 256:
+        pytest.skip("FP16X supports d = 128")
+    w = random_weights(3, d=d, n_hidden=nh)
+    cfg = lib.make_config(512, 512, precision=precision, subsolver=lib.SDNET, check_every=1)
+    m = lib.Mfp(cfg, lib.make_net(d=d, n_hidden=nh, gelu=2 if precision == 3 else 1), w)
+    gb = random_boundaries(2000, seed=41)
+    out = m.sdnet_batch(torch.from_numpy(gb).cuda(), 0).cpu().numpy()
+    q = oracle.writeset(0, 0)[1]
+    net = oracle.NetShape(d=d, n_hidden=nh)
+    ref = oracle.sdnet_forward(w.astype(np.float64), gb.astype(np.float64), q, net=net)
+    _, S = torch_sdnet(w, gb, q, d=d, n_hidden=nh, return_scale=True)
+    check_batch(out, ref, 2 if precision == 3 else precision, S)
     m.close()
