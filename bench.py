@@ -340,7 +340,7 @@ def boundary_io_bench(mfp, torch, peaks, reps: int = 10, flush_l2: bool = True) 
            "gather": {"kernel": "k_gather_phase (a1)", "us": 1000 * ms_g, "bytes_per_subdomain": gbytes,
                       "note": "512 B perimeter read + 512 B batch write",
                       "gbs": B * gbytes / (ms_g / 1000) / 1e9},
-           "scatter": {"kernel": "k_scatter_phase + k_reduce_max (a6 + a8)", "us": 1000 * ms_s,
+           "scatter": {"kernel": "k_scatter_phase (a6 + the a8 reduction, last block)", "us": 1000 * ms_s,
                        "bytes_per_subdomain": sbytes,
                        "note": "244 B predictions + 244 B old values read, 248 B written (centre twice)",
                        "gbs": B * sbytes / (ms_s / 1000) / 1e9}}

@@ -313,7 +313,7 @@ void carve(mfp_ctx* c, void* base, size_t* total) {
   c->gstage = cv.take<float>((size_t)2 * (c->cfg.nx + c->cfg.ny));
   c->delta = cv.take<unsigned int>(4);
   c->loopst = cv.take<unsigned int>(4);
-  c->iomax = cv.take<unsigned int>(kMaxSMs * 8);   // >= scatter_grid(B) for any B
+  c->iomax = cv.take<unsigned int>(kMaxSMs * 8 + 32);   // >= scatter_grid(B) for any B, + the ticket
   c->ioout = cv.take<unsigned int>(2);
   const bool need_full = (c->rank == MFP_ALL_RANKS || c->rank == 0);
   c->full = need_full ? cv.take<float>((size_t)(c->cfg.nx + 1) * (c->cfg.ny + 1)) : nullptr;
@@ -1155,6 +1155,9 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
   CK(cudaEventCreateWithFlags(&c->ev_packed, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_unpacked, cudaEventDisableTiming));
   cudaStream_t s = c->stream;
+  // scatter block maxima, the last-block ticket and the reduced norm start at 0
+  CK(cudaMemsetAsync(c->iomax, 0, (kMaxSMs * 8 + 32) * sizeof(unsigned int), s));
+  CK(cudaMemsetAsync(c->ioout, 0, 2 * sizeof(unsigned int), s));
   // upload plan tables
   for (auto& rs : c->ranks) {
     const RankPlan& p = rs.plan;
@@ -1356,7 +1359,7 @@ mfp_status mfp_scatter_phase(mfp_ctx* c, int32_t rank, int32_t phase, const floa
   if (B != (int64_t)p.phase_anchor[phase].size() || (B > 0 && !pred))
     return fail(c, MFP_ERR_INVALID, "scatter_phase: B must equal the phase's subdomain count");
   launch_scatter_phase(rs->lat, p.lat, rs->anchors[phase], B, pred, c->iomax, c->ioout, c->stream);
-  c->launches += B > 0 ? 2 : 1;
+  c->launches += B > 0 ? 1 : 0;
   CK(cudaGetLastError());
   if (update_max) {
     unsigned int h[2];

@@ -49,13 +49,31 @@ k_gather_phase(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __r
 // centre-line cells (the centre point in both line arrays), and the block
 // accumulates max |new - old| over the cells it overwrites (warp shuffles, then
 // one shared-memory step).  blockmax[blockIdx.x] = that maximum (fp32 bits) and
-// bit 31 of blockflag set on a non-finite prediction.  Cells of one phase are
-// written by exactly one subdomain, so the result is order independent.
-__global__ void __launch_bounds__(kIoWarps * 32, 5)
+// bit 31 set on a non-finite prediction.  Cells of one phase are written by
+// exactly one subdomain, so the result is order independent.
+//
+// a8 reduction fused: the last block to finish (an atomic ticket, re-armed by
+// that block) reduces the block maxima into out[0] (max, fp32 bits: non-negative
+// floats order like unsigned ints) and out[1] (1 if any prediction was
+// non-finite) — no second kernel and no launch gap.
+//
+// Measured on B200 (bench.py boundary_io, 262,144 subdomains, L2 flushed;
+// tools/gpu/round2/r3m.sh, r3n.sh): the grid is ONE wave of resident blocks
+// (the round-1 grid of 8 blocks per SM ran 1.6 waves at 5 resident), and the
+// most warps per SM win over more subdomains per warp: kScU = 2 subdomains per
+// warp per round at 8 blocks (64 warps) per SM 0.67 of HBM, 4 at 5 blocks 0.59,
+// 8 at 2 blocks 0.56, an anchor prefetch across rounds no better (0.54-0.66),
+// one thread per cell 0.42; + the fused reduction 0.71 (round 1: 0.53).
+constexpr int kScU = 2;      // subdomains per warp per round
+constexpr int kScMinB = 8;   // resident blocks per SM (<= 32 registers)
+
+__global__ void __launch_bounds__(kIoWarps * 32, kScMinB)
 k_scatter_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict__ anchors, int64_t B,
-                const float* __restrict__ pred, unsigned int* __restrict__ blockmax) {
+                const float* __restrict__ pred, unsigned int* __restrict__ blockmax, unsigned int* __restrict__ ticket,
+                unsigned int* __restrict__ out) {
   __shared__ float red[kIoWarps];
   __shared__ int bad_s;
+  __shared__ unsigned int last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) bad_s = 0;
   __syncthreads();
@@ -63,16 +81,14 @@ k_scatter_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restri
   float m = 0.f;
   bool bad = false;
   const bool two = lane + 32 < kQC;
-  // kIoUnroll subdomains per warp per round: every load of the round (predictions
-  // and old values) is issued before the first store, so a warp keeps
-  // 4 x ~0.5 KB in flight instead of one dependent load/store pair at a time.
-  // Cell indices are 32-bit (a rank's lattice holds < 2^31 cells; checked at
-  // launch), which keeps the kernel at <= 48 registers: 5 resident blocks per SM.
-  for (int64_t s0 = ((int64_t)blockIdx.x * kIoWarps + warp) * kIoUnroll; s0 < B; s0 += nw * kIoUnroll) {
-    int32_t c0[kIoUnroll], c1[kIoUnroll], cd[kIoUnroll];   // cd: the centre's second copy or -1
-    float y0[kIoUnroll], y1[kIoUnroll], o0[kIoUnroll], o1[kIoUnroll];
+  // every load of a round (predictions and old values) is issued before its
+  // first store; cell indices are 32-bit (a rank's lattice holds < 2^31 cells;
+  // checked at launch)
+  for (int64_t s0 = ((int64_t)blockIdx.x * kIoWarps + warp) * kScU; s0 < B; s0 += nw * kScU) {
+    int32_t c0[kScU], c1[kScU], cd[kScU];   // cd: the centre's second copy or -1
+    float y0[kScU], y1[kScU], o0[kScU], o1[kScU];
 #pragma unroll
-    for (int u = 0; u < kIoUnroll; u++) {
+    for (int u = 0; u < kScU; u++) {
       const int64_t s = s0 + u < B ? s0 + u : B - 1;   // tail: clamp (stores are skipped)
       int a, b;
       unpack_anchor(__ldg(anchors + s), a, b);
@@ -84,20 +100,16 @@ k_scatter_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restri
       y1[u] = two ? __ldcs(pred + s * kQC + lane + 32) : y0[u];
     }
 #pragma unroll
-    for (int u = 0; u < kIoUnroll; u++) {
+    for (int u = 0; u < kScU; u++) {
       o0[u] = __ldcg(lat + c0[u]);
       o1[u] = two ? __ldcg(lat + c1[u]) : o0[u];
     }
 #pragma unroll
-    for (int u = 0; u < kIoUnroll; u++) {
+    for (int u = 0; u < kScU; u++) {
       if (s0 + u >= B) continue;
       const float d0 = fabsf(y0[u] - o0[u]), d1 = two ? fabsf(y1[u] - o1[u]) : 0.f;
       if (!(d0 <= 3.0e38f) || !(d1 <= 3.0e38f)) bad = true;   // NaN or Inf
       else m = fmaxf(m, fmaxf(d0, d1));
-    }
-#pragma unroll
-    for (int u = 0; u < kIoUnroll; u++) {
-      if (s0 + u >= B) continue;
       lat[c0[u]] = y0[u];
       if (cd[u] >= 0) lat[cd[u]] = y0[u];
       if (two) lat[c1[u]] = y1[u];
@@ -110,42 +122,46 @@ k_scatter_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restri
   if (warp == 0) {
     float v = lane < kIoWarps ? red[lane] : 0.f;
     v = warp_max(v);
-    if (lane == 0) blockmax[blockIdx.x] = __float_as_uint(v) | (bad_s ? 0x80000000u : 0u);
-  }
-}
-
-// ------------------------------------------------------ a8: convergence reduction
-// One block reduces the n block maxima: out[0] = max (fp32 bits; non-negative
-// floats order like unsigned ints), out[1] = 1 if any block saw a non-finite value.
-__global__ void __launch_bounds__(1024) k_reduce_max(const unsigned int* __restrict__ blockmax, int n,
-                                                     unsigned int* __restrict__ out) {
-  __shared__ unsigned int red[32];
-  __shared__ unsigned int anybad;
-  if (threadIdx.x == 0) anybad = 0u;
-  __syncthreads();
-  unsigned int m = 0u, bad = 0u;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const unsigned int v = blockmax[i];
-    bad |= v >> 31;
-    m = max(m, v & 0x7fffffffu);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (__any_sync(0xffffffffu, bad != 0u) && (threadIdx.x & 31) == 0) atomicOr(&anybad, 1u);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    unsigned int v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0u;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (threadIdx.x == 0) {
-      out[0] = v;
-      out[1] = anybad;
+    if (lane == 0) {
+      blockmax[blockIdx.x] = __float_as_uint(v) | (bad_s ? 0x80000000u : 0u);
+      __threadfence();
+      last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
   }
+  __syncthreads();
+  if (!last) return;
+  // the last block: every other block's maximum is visible (fence before ticket)
+  __threadfence();
+  unsigned int mu = 0u, nb = 0u;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+    const unsigned int v = __ldcg(blockmax + i);
+    nb |= v >> 31;
+    mu = max(mu, v & 0x7fffffffu);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mu = max(mu, __shfl_xor_sync(0xffffffffu, mu, o));
+    nb |= __shfl_xor_sync(0xffffffffu, nb, o);
+  }
+  __shared__ unsigned int rm[kIoWarps], rb[kIoWarps];
+  if (lane == 0) {
+    rm[warp] = mu;
+    rb[warp] = nb;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kIoWarps; w++) {
+      mu = max(mu, rm[w]);
+      nb |= rb[w];
+    }
+    out[0] = mu;
+    out[1] = nb;
+    *ticket = 0u;   // re-armed for the next launch (stream order)
+  }
 }
 
-// Grid: a multiple of the SM count (8 warps per block, up to 8 blocks per SM).
+// Grids: a multiple of the SM count.  The gather: 8 warps per block, up to 8
+// blocks per SM.  The scatter: exactly one wave of resident blocks.
 static int io_blocks(int64_t units, int per_block) {
   int64_t b = (units + per_block - 1) / per_block;
   const int64_t cap = (int64_t)(num_sms() < kMaxSMs ? num_sms() : kMaxSMs) * 8;
@@ -153,7 +169,17 @@ static int io_blocks(int64_t units, int per_block) {
   return b < 1 ? 1 : (int)b;
 }
 
-int scatter_grid(int64_t B) { return io_blocks(B, kIoWarps * kIoUnroll); }
+int scatter_grid(int64_t B) {
+  static int occ = 0;
+  if (occ == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter_phase, kIoWarps * 32, 0);
+    occ = occ < 1 ? 1 : occ > 8 ? 8 : occ;
+  }
+  int64_t b = (B + kIoWarps * kScU - 1) / (kIoWarps * kScU);
+  const int64_t cap = (int64_t)(num_sms() < kMaxSMs ? num_sms() : kMaxSMs) * occ;
+  if (b > cap) b = cap;
+  return b < 1 ? 1 : (int)b;
+}
 
 void launch_gather_phase(const float* lat, const LatticeGeom& L, const uint32_t* anchors, int64_t B, float* gb,
                          cudaStream_t s) {
@@ -163,11 +189,13 @@ void launch_gather_phase(const float* lat, const LatticeGeom& L, const uint32_t*
 
 void launch_scatter_phase(float* lat, const LatticeGeom& L, const uint32_t* anchors, int64_t B, const float* pred,
                           unsigned int* blockmax, unsigned int* out, cudaStream_t s) {
-  const int nb = scatter_grid(B);
   if (L.cells >= ((int64_t)1 << 31)) __builtin_trap();   // 32-bit cell indices (never at 16385^2: 3.4e7 cells)
-  if (B > 0) k_scatter_phase<<<nb, kIoWarps * 32, 0, s>>>(lat, L, anchors, B, pred, blockmax);
-  else cudaMemsetAsync(blockmax, 0, sizeof(unsigned int) * nb, s);
-  k_reduce_max<<<1, 1024, 0, s>>>(blockmax, nb, out);
+  if (B <= 0) {
+    cudaMemsetAsync(out, 0, 2 * sizeof(unsigned int), s);
+    return;
+  }
+  k_scatter_phase<<<scatter_grid(B), kIoWarps * 32, 0, s>>>(lat, L, anchors, B, pred, blockmax,
+                                                             blockmax + kMaxSMs * 8, out);
 }
 
 }  // namespace mfp

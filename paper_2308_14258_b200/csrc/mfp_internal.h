@@ -204,12 +204,12 @@ void launch_chain_fp32(const float* z, int64_t B, int q, const DevNet& net, cons
 bool chain_tc_available();
 void launch_chain_tc(const float* z, int64_t B, int q, const DevNet& net, const Sink& sink,
                      int num_sms, cudaStream_t s);
-// standalone boundary IO (kernels_boundary_io.cu): a1 gather, a6 scatter + update norm, a8 reduction
+// standalone boundary IO (kernels_boundary_io.cu): a1 gather, a6 scatter + update norm + a8 reduction (one kernel)
 int scatter_grid(int64_t B);
 void launch_gather_phase(const float* lat, const LatticeGeom& L, const uint32_t* anchors, int64_t B, float* gb,
                          cudaStream_t s);
 void launch_scatter_phase(float* lat, const LatticeGeom& L, const uint32_t* anchors, int64_t B, const float* pred,
-                          unsigned int* blockmax /* scatter_grid(B) */, unsigned int* out /* [2] */,
+                          unsigned int* blockmax /* kMaxSMs * 8 maxima + the ticket */, unsigned int* out /* [2] */,
                           cudaStream_t s);
 void launch_loop_ctl(cudaGraphConditionalHandle h, const unsigned int* delta, unsigned int* st, int ce,
                      cudaStream_t s);

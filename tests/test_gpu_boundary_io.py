@@ -101,6 +101,37 @@ def test_scatter_empty_and_nonfinite(lib):
     assert e.value.status == 1
 
 
+@pytest.mark.parametrize("n", [4096, 8192])
+def test_scatter_many_blocks_norm_rearm(lib, n):
+    """Phases of 16,384 / 65,536 subdomains: every block of the one-wave grid
+    (8 per SM) takes part, so the last-block reduction (a8) combines >= 1,000
+    block maxima; repeated calls re-arm its ticket, and a non-finite call is
+    followed by a finite one whose flag must be clear.  The norm must equal
+    max |after - before| over the whole exported lattice (unwritten cells do
+    not change), bit for bit."""
+    import torch
+    m = exact_ctx(lib, n, n)
+    random_lattice(m, 5)
+    rng = np.random.default_rng(n)
+    for rep, phase in enumerate([0, 1, 0, 3, 2]):
+        b = m.lines()
+        hl0, vl0 = b.hl.copy(), b.vl.copy()
+        B, _ = lib.mfp_gather_phase(m.ctx, 0, phase)
+        pred = (rng.standard_normal((B, 2 * M - 3)) * (rep + 1)).astype(np.float32)
+        if rep == 2:
+            pred[B // 2, 30] = float("inf")
+            with pytest.raises(lib.MfpError) as e:
+                m.scatter_phase(phase, torch.from_numpy(pred).cuda())
+            assert e.value.status == 3
+            m.set_lines(hl0, vl0)   # the inf was written; later phases overlap its cells
+            continue
+        norm = m.scatter_phase(phase, torch.from_numpy(pred).cuda())
+        a = m.lines()
+        want = max(np.max(np.abs(a.hl - hl0)), np.max(np.abs(a.vl - vl0)))
+        assert np.float32(norm) == np.float32(want)
+        assert np.count_nonzero(a.hl != hl0) + np.count_nonzero(a.vl != vl0) <= B * (2 * M - 2)
+
+
 def test_gather_distributed_rank_view(lib):
     """MFP_ALL_RANKS 2x2: each rank gathers from its own lattice copy (D1)."""
     nx = ny = 8 * M
