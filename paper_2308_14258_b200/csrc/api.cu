@@ -1181,7 +1181,26 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
   }
   if (cfg->subsolver == MFP_SDNET) {
     CK(cudaMemcpyAsync(c->params, params, n_params * sizeof(float), cudaMemcpyHostToDevice, s));
-    for (int i = 0; i < 89; i++) c->dn.convw[i] = params[i];   // MFCK order: conv1 w, b, conv2 w, b
+    {
+      // the tensor-core embed's constant-bank conv weights in channel-PAIR order
+      // (kernels_embed_tc.cu conv_stack): [40) conv1 (w[2c][t], w[2c+1][t]) by
+      // (c, t), [40, 48) conv1 biases, [48, 88) conv2 pairs likewise, [88] conv2
+      // bias; conv2 weights halved when the channel activation yields 2 GELU
+      // (gelu 1 / 2; exact power-of-two scaling)
+      const float* c1w = params; const float* c1b = params + 40;
+      const float* c2w = params + 48;
+      const float h2 = net->gelu >= 1 ? 0.5f : 1.0f;
+      for (int cp = 0; cp < kC1 / 2; cp++) {
+        for (int t = 0; t < kK; t++)
+          for (int u = 0; u < 2; u++) {
+            c->dn.convw[2 * (cp * kK + t) + u] = c1w[(2 * cp + u) * kK + t];
+            c->dn.convw[48 + 2 * (cp * kK + t) + u] = h2 * c2w[(2 * cp + u) * kK + t];
+          }
+        c->dn.convw[40 + 2 * cp] = c1b[2 * cp];
+        c->dn.convw[40 + 2 * cp + 1] = c1b[2 * cp + 1];
+      }
+      c->dn.convw[88] = params[88];
+    }
     CK(cudaMemsetAsync((void*)c->dn.Wh_sw2, 0, wimg_elems(net->d, net->n_hidden) * 2, s));
     PrepArgs a;
     a.P = c->params; a.n_hidden = net->n_hidden; a.d = net->d; a.f16 = (cfg->precision == MFP_FP16 || cfg->precision == MFP_FP16X) ? 1 : 0;

@@ -34,30 +34,34 @@ using namespace tcx;
 constexpr int kRowsE = 128;              // subdomains per round (UMMA M)
 constexpr int kThreadsE = 512;           // 16 warps
 constexpr int kImg = kRowsE * kNB * 2;   // 32 KB bf16 image
-constexpr int kPerWarp = kRowsE / 16;
 
 // W1 buffer (hi + lo images of 128 output rows) + A hi / lo + staging + vectors + barriers
 constexpr size_t smem_bytes(int D) { return 4 * (size_t)kImg + (size_t)kRowsE * 576 + 4 * (96 + D) + 8 * 19 + 16; }
 
-// The conv stack of TWO subdomains at once: every value is an fp32 pair
-// (subdomain A, subdomain B) at the same perimeter position, so each weight is
-// one broadcast operand of a packed FFMA2 (half the FMA instructions of the
-// scalar stack, twice the independent work per lane); weights come from the
-// kernel-parameter constant bank (DevNet::convw).
-__device__ __forceinline__ f2 shfl2(f2 v, int src) {
-  return f2{__shfl_sync(0xffffffffu, v.v, src)};
-}
-__device__ __forceinline__ void circ_window2(const f2 (&v)[4], int lane, f2 (&w)[8]) {
-  const int left = (lane + 31) & 31, right = (lane + 1) & 31;
-  w[0] = shfl2(v[2], left);
-  w[1] = shfl2(v[3], left);
-  w[2] = v[0]; w[3] = v[1]; w[4] = v[2]; w[5] = v[3];
-  w[6] = shfl2(v[0], right);
-  w[7] = shfl2(v[1], right);
+// The conv stack (G7: conv1d 1->8 -> GELU -> conv1d 8->1 -> GELU, k = 5,
+// circular) of N subdomains, interleaved for ILP.  Lane l owns perimeter
+// positions 4l..4l+3; the circular windows come from the neighbour lanes by
+// shuffles.  Channels are packed in PAIRS (2c, 2c+1) into fp32x2 values, so
+// every FFMA2 takes its weight pair as ONE 64-bit constant-bank operand
+// (DevNet::convw, pair order) and its input as a scalar broadcast operand:
+// no register moves to build operand pairs.  conv2 accumulates the even and
+// odd channels in the two halves of a pair, added at the end.
+template <int GELU>
+__device__ __forceinline__ f2 ch_act2(f2 x) {   // conv1 outputs: 2 GELU (GELU 1 / 2; conv2 weights hold w / 2) or GELU (0)
+  if constexpr (GELU == 1) {
+    float u0, u1;
+    f2_split(fmul2(x, ffma2(fmul2(x, x), f2_make(kGF1, kGF1), f2_make(kGF0, kGF0))), u0, u1);
+    return ffma2(x, f2_make(tanh_approx(u0), tanh_approx(u1)), x);
+  } else {
+    float a, b;
+    f2_split(x, a, b);
+    if constexpr (GELU == 2) return f2_make(gelu2_acc(a), gelu2_acc(b));
+    else return f2_make(gelu_erf(a), gelu_erf(b));
+  }
 }
 template <int GELU>
-__device__ __forceinline__ f2 emb_act2(f2 x) {
-  if constexpr (GELU == 2) {   // accurate form (device_common.cuh gelu2_acc), halved
+__device__ __forceinline__ f2 emb_act2(f2 x) {   // the embedding itself: GELU (proper scale)
+  if constexpr (GELU == 2) {
     float a, b;
     f2_split(x, a, b);
     return f2_make(0.5f * gelu2_acc(a), 0.5f * gelu2_acc(b));
@@ -72,34 +76,69 @@ __device__ __forceinline__ f2 emb_act2(f2 x) {
     return f2_make(gelu_erf(a), gelu_erf(b));
   }
 }
-template <int GELU>
-__device__ __forceinline__ void conv_stack2(const f2 (&g4)[4], int lane, const DevNet& net, f2 (&e)[4]) {
-  const float* cw = net.convw;
-  f2 win[8];
-  circ_window2(g4, lane, win);
-  f2 acc2[4];
+__device__ __forceinline__ f2 cpair(const DevNet& net, int i) {   // 64-bit constant-bank operand
+  return f2{*reinterpret_cast<const uint64_t*>(net.convw + i)};
+}
+__device__ __forceinline__ f2 bcast(float x) { return f2_make(x, x); }   // FFMA2 scalar (.F32) operand
+__device__ __forceinline__ f2 shfl2(f2 v, int src) { return f2{__shfl_sync(0xffffffffu, v.v, src)}; }
+
+template <int GELU, int N>
+__device__ __forceinline__ void conv_stack(const float (&g)[N][4], int lane, const DevNet& net, float (&e)[N][4]) {
+  const int left = (lane + 31) & 31, right = (lane + 1) & 31;
+  float win[N][8];
 #pragma unroll
-  for (int p = 0; p < 4; p++) acc2[p] = f2_make(cw[88], cw[88]);
+  for (int n = 0; n < N; n++) {
+    win[n][0] = __shfl_sync(0xffffffffu, g[n][2], left);
+    win[n][1] = __shfl_sync(0xffffffffu, g[n][3], left);
 #pragma unroll
-  for (int o = 0; o < kC1; o++) {
-    f2 c1v[4];
+    for (int p = 0; p < 4; p++) win[n][2 + p] = g[n][p];
+    win[n][6] = __shfl_sync(0xffffffffu, g[n][0], right);
+    win[n][7] = __shfl_sync(0xffffffffu, g[n][1], right);
+  }
+  f2 acc[N][4];   // conv2: (even channels, odd channels) per position
 #pragma unroll
-    for (int p = 0; p < 4; p++) {
-      f2 v = f2_make(cw[40 + o], cw[40 + o]);
+  for (int n = 0; n < N; n++)
 #pragma unroll
-      for (int t = 0; t < kK; t++) v = ffma2(f2_make(cw[o * kK + t], cw[o * kK + t]), win[p + t], v);
-      c1v[p] = emb_act2<GELU>(v);
+    for (int p = 0; p < 4; p++) acc[n][p] = f2_make(net.convw[88], 0.0f);
+#pragma unroll
+  for (int cp = 0; cp < kC1 / 2; cp++) {
+    const f2 bias = cpair(net, 40 + 2 * cp);
+    f2 aw[N][8];
+#pragma unroll
+    for (int n = 0; n < N; n++)
+#pragma unroll
+      for (int p = 0; p < 4; p++) {
+        f2 v = ffma2(bcast(win[n][p]), cpair(net, 2 * (cp * kK)), bias);
+#pragma unroll
+        for (int t = 1; t < kK; t++) v = ffma2(bcast(win[n][p + t]), cpair(net, 2 * (cp * kK + t)), v);
+        aw[n][2 + p] = ch_act2<GELU>(v);
+      }
+#pragma unroll
+    for (int n = 0; n < N; n++) {
+      aw[n][0] = shfl2(aw[n][4], left);
+      aw[n][1] = shfl2(aw[n][5], left);
+      aw[n][6] = shfl2(aw[n][2], right);
+      aw[n][7] = shfl2(aw[n][3], right);
     }
-    f2 w2[8];
-    circ_window2(c1v, lane, w2);
 #pragma unroll
-    for (int p = 0; p < 4; p++)
+    for (int n = 0; n < N; n++)
 #pragma unroll
-      for (int t = 0; t < kK; t++)
-        acc2[p] = ffma2(f2_make(cw[48 + o * kK + t], cw[48 + o * kK + t]), w2[p + t], acc2[p]);
+      for (int p = 0; p < 4; p++)
+#pragma unroll
+        for (int t = 0; t < kK; t++) acc[n][p] = ffma2(cpair(net, 48 + 2 * (cp * kK + t)), aw[n][p + t], acc[n][p]);
   }
 #pragma unroll
-  for (int p = 0; p < 4; p++) e[p] = emb_act2<GELU>(acc2[p]);
+  for (int n = 0; n < N; n++) {
+    float s[4];
+#pragma unroll
+    for (int p = 0; p < 4; p++) {
+      float lo, hi;
+      f2_split(acc[n][p], lo, hi);
+      s[p] = lo + hi;
+    }
+    f2_split(emb_act2<GELU>(f2_make(s[0], s[1])), e[n][0], e[n][1]);
+    f2_split(emb_act2<GELU>(f2_make(s[2], s[3])), e[n][2], e[n][3]);
+  }
 }
 
 // Staged perimeter of one subdomain (TMA bulk copies of the four edge
@@ -126,18 +165,13 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
   uint8_t* sAhi = sWlo + kImg;
   uint8_t* sAlo = sAhi + kImg;
   uint8_t* sStage = sAlo + kImg;                         // [128][kSlotB]
-  float* sCw = reinterpret_cast<float*>(sStage + kRowsE * kSlotB);   // c1w[40] c1b[8] c2w[40] c2b[1]
-  float* sB1 = sCw + 96;
+  float* sB1 = reinterpret_cast<float*>(sStage + kRowsE * kSlotB) + 96;   // (96 floats spare)
   uint64_t* bar = reinterpret_cast<uint64_t*>(sB1 + D);   // [0] MMA done, [1] W1 landed, [2] W1 free
   uint64_t* full = bar + 3;                                // [3..18] warp's perimeters landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full + 16);
   constexpr int NH = D / 128;                              // W1 halves
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < D; i += kThreadsE) sB1[i] = __ldg(net.b1 + i);
-  if (threadIdx.x < 40) sCw[threadIdx.x] = __ldg(net.conv1_w + threadIdx.x);
-  if (threadIdx.x < 8) sCw[40 + threadIdx.x] = __ldg(net.conv1_b + threadIdx.x);
-  if (threadIdx.x < 40) sCw[48 + threadIdx.x] = __ldg(net.conv2_w + threadIdx.x);
-  if (threadIdx.x == 0) sCw[88] = __ldg(net.conv2_b);
   if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
@@ -166,11 +200,12 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
   }
   pdl_launch_dependents();
   pdl_wait();      // the lattice (previous phase's scatter) and z's readers complete from here on
-  // `rows` (32, 64, 96 or 128) subdomains per round: small batches (a rank's share
-  // on 8 GPUs) spread over more CTAs with fewer subdomains per warp, so the
-  // serial conv work per warp shrinks with the batch; rows >= `rows` of the
-  // 128-row MMA are don't-care (rows are independent in the MMA, never stored)
-  const int pw = rows >> 4;   // subdomains per warp (even)
+  // `rows` (a multiple of 16, <= 128) subdomains per round: the batch spread
+  // over every SM (C5: 112 rows on 146 CTAs), small batches (a rank's share on
+  // 8 GPUs) with fewer subdomains per warp, so the serial conv work per warp
+  // shrinks with the batch; rows >= `rows` of the 128-row MMA are don't-care
+  // (rows are independent in the MMA, never stored)
+  const int pw = rows >> 4;   // subdomains per warp (1..8)
   const int64_t step = (int64_t)gridDim.x * rows;
 
   // ---- a1: TMA bulk copies of this warp's pw perimeters (four edge segments
@@ -228,34 +263,35 @@ k_embed_tc(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __restr
         }
         return v;
       };
-#pragma unroll
-      for (int jp = 0; jp < kPerWarp; jp += 2) {
-        if (jp >= pw) break;
-        const float4 ga = perim4(jp), gb4 = perim4(jp + 1);
-        const f2 g4[4] = {f2_make(ga.x, gb4.x), f2_make(ga.y, gb4.y), f2_make(ga.z, gb4.z), f2_make(ga.w, gb4.w)};
-        f2 e2[4];
-        conv_stack2<GELU>(g4, lane, net, e2);
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int row = warp * pw + jp + h;
-          float e[4];
-#pragma unroll
-          for (int p = 0; p < 4; p++) {
-            float lo, hi;
-            f2_split(e2[p], lo, hi);
-            e[p] = h ? hi : lo;
-          }
-          // e = e_hi + e_lo, both bf16 (round to nearest)
-          uint32_t h01, h23, l01, l23;
-          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h01) : "f"(e[1]), "f"(e[0]));
-          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h23) : "f"(e[3]), "f"(e[2]));
-          const float r0 = e[0] - __uint_as_float(h01 << 16), r1 = e[1] - __uint_as_float(h01 & 0xffff0000u);
-          const float r2 = e[2] - __uint_as_float(h23 << 16), r3 = e[3] - __uint_as_float(h23 & 0xffff0000u);
-          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l01) : "f"(r1), "f"(r0));
-          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l23) : "f"(r3), "f"(r2));
-          const uint32_t off = sw128_off(row, i0) + (uint32_t)((i0 & 7) * 2);
-          asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a_hi + off), "r"(h01), "r"(h23) : "memory");
-          asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a_lo + off), "r"(l01), "r"(l23) : "memory");
+      // e = e_hi + e_lo, both bf16 (round to nearest), into the two A operands
+      auto store_row = [&](int row, const float (&e)[4]) {
+        uint32_t h01, h23, l01, l23;
+        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h01) : "f"(e[1]), "f"(e[0]));
+        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h23) : "f"(e[3]), "f"(e[2]));
+        const float r0 = e[0] - __uint_as_float(h01 << 16), r1 = e[1] - __uint_as_float(h01 & 0xffff0000u);
+        const float r2 = e[2] - __uint_as_float(h23 << 16), r3 = e[3] - __uint_as_float(h23 & 0xffff0000u);
+        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l01) : "f"(r1), "f"(r0));
+        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l23) : "f"(r3), "f"(r2));
+        const uint32_t off = sw128_off(row, i0) + (uint32_t)((i0 & 7) * 2);
+        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a_hi + off), "r"(h01), "r"(h23) : "memory");
+        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a_lo + off), "r"(l01), "r"(l23) : "memory");
+      };
+      // two subdomains interleaved per step (ILP), an odd last one alone
+#pragma unroll 1
+      for (int jp = 0; jp < pw; jp += 2) {
+        if (jp + 1 < pw) {
+          const float4 ga = perim4(jp), gb4 = perim4(jp + 1);
+          const float g[2][4] = {{ga.x, ga.y, ga.z, ga.w}, {gb4.x, gb4.y, gb4.z, gb4.w}};
+          float e[2][4];
+          conv_stack<GELU, 2>(g, lane, net, e);
+          store_row(warp * pw + jp, e[0]);
+          store_row(warp * pw + jp + 1, e[1]);
+        } else {
+          const float4 ga = perim4(jp);
+          const float g[1][4] = {{ga.x, ga.y, ga.z, ga.w}};
+          float e[1][4];
+          conv_stack<GELU, 1>(g, lane, net, e);
+          store_row(warp * pw + jp, e[0]);
         }
       }
       // next round's perimeters: the slots' generic-proxy reads (long since
@@ -357,12 +393,12 @@ void embed_tc_kernel_attributes() {
 void launch_embed_tc(const float* lat, const LatticeGeom& L, const uint32_t* anchors, const float* gb,
                      int64_t B, const DevNet& net, float* z, cudaStream_t s) {
   if (B <= 0) return;
-  // rows per CTA round: the smallest multiple of 32 that covers B over the SMs
+  // rows per CTA round: the smallest multiple of 16 that covers B over the SMs
   const int sms = num_sms();
   int64_t per = (B + sms - 1) / sms;
-  int rows = (int)((per + 31) / 32) * 32;
+  int rows = (int)((per + 15) / 16) * 16;
   if (rows > emb::kRowsE) rows = emb::kRowsE;
-  if (rows < 32) rows = 32;
+  if (rows < 16) rows = 16;
   int64_t blocks = (B + rows - 1) / rows;
   if (blocks > sms) blocks = sms;
   const size_t sm = emb::smem_bytes(net.d);

@@ -94,10 +94,11 @@ mfp_status validate_config(const mfp_config* cfg, std::string* err);
 // ---- device-side parameter blocks ----------------------------------------
 struct DevNet {
   // fp32 tables (SIMT path + embed)
-  // conv stack weights by value {c1w[40], c1b[8], c2w[40], c2b[1]}: kernel
-  // parameters live in the constant bank, so the tensor-core embed's FMAs take
-  // them as constant operands (no shared-memory loads, no registers)
-  float convw[89];
+  // conv stack weights by value, channel-PAIR order (api.cu, kernels_embed_tc.cu
+  // conv_stack): kernel parameters live in the constant bank, so the tensor-core
+  // embed's FFMA2s take each weight pair as one 64-bit constant operand (no
+  // shared-memory loads, no registers); 8-byte aligned as the first member
+  alignas(8) float convw[89];
   const float* conv1_w;  // [8][5]
   const float* conv1_b;  // [8]
   const float* conv2_w;  // [8][5]
