@@ -23,9 +23,9 @@
 //     16 bit -> st.shared into the swizzled A operand -> fence.proxy.async ->
 //     mbarrier arrive (remote for the odd CTA);
 //   * the layer-1 input is Eq. 5's broadcasted sum GELU(z[s] + W2 x_p): z of
-//     the <= 4 subdomains of a tile staged in smem with W2's constant half
-//     folded in (one FMA per element on the centre lines), prefetched one tile
-//     ahead; the last layer's epilogue stays fp32 (GELU + head dot
+//     the <= 4 subdomains of a tile staged in smem (prefetched one tile ahead),
+//     W2 as constant-bank operand pairs, the next 16 columns of z loaded while
+//     the current ones are activated; the last layer's epilogue stays fp32 (GELU + head dot
 //     y = wo.h + bo; the head cancels strongly) followed by the
 //     fused scatter onto the lattice (a6) or the final-phase field (a9).
 #include <cstdlib>
@@ -290,11 +290,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       uint4* dst = reinterpret_cast<uint4*>(S.W + l * kHalf);
       for (int i = threadIdx.x; i < kHalf / 16; i += kThreads2) dst[i] = __ldg(src + i);
     }
-    for (int i = threadIdx.x; i < kD; i += kThreads2) {
-      S.wo[i] = (GELU >= 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
-      S.w2[i] = __ldg(net.W2 + 2 * i);
-      S.w2[kD + i] = __ldg(net.W2 + 2 * i + 1);
-    }
+    for (int i = threadIdx.x; i < kD; i += kThreads2) S.wo[i] = (GELU >= 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
     if (threadIdx.x < kRows) {
       const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
       const int r = threadIdx.x;
@@ -384,18 +380,9 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       if (sidx > nsub - 1) sidx = nsub - 1;
       return __ldg(reinterpret_cast<const float4*>(z + sidx * kD + zc));
     };
-    // z of the tile's <= 4 subdomains, staged with the constant half of the split
-    // layer folded in: z + W2[:,0]/2 (vertical centre line, x/m = 1/2) and
-    // z + W2[:,1]/2 (horizontal centre line, y/m = 1/2), so that a centre-line
-    // row needs one FMA per element for Eq. 5's broadcasted sum
-    auto z_stage = [&](const float4 v) {
-      const float4 a = *reinterpret_cast<const float4*>(S.w2 + zc);
-      const float4 b = *reinterpret_cast<const float4*>(S.w2 + kD + zc);
-      *reinterpret_cast<float4*>(zb + zi) =
-          make_float4(fmaf(0.5f, a.x, v.x), fmaf(0.5f, a.y, v.y), fmaf(0.5f, a.z, v.z), fmaf(0.5f, a.w, v.w));
-      *reinterpret_cast<float4*>(zb + kZRows * kD + zi) =
-          make_float4(fmaf(0.5f, b.x, v.x), fmaf(0.5f, b.y, v.y), fmaf(0.5f, b.z, v.z), fmaf(0.5f, b.w, v.w));
-    };
+    // z of the tile's <= 4 subdomains, staged in smem (each row reads its
+    // subdomain's 128 values; W2 comes from the constant bank, DevNet::w2c)
+    auto z_stage = [&](const float4 v) { *reinterpret_cast<float4*>(zb + zi) = v; };
     auto arrive_a = [&]() {
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(&S.bars[slot], 0u);
@@ -422,43 +409,40 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       int zo = (int)(sidx - s_first);
       if (zo < 0 || zo >= kZRows) zo = 0;   // rows past the end of the batch (not stored)
 
-      // ---- split layer (Eq. 5, a3): h' = 2 GELU(z[s] + W2 x_p) -> A operand,
-      // 16 columns (8 independent element pairs) per block
-      const bool centre = (q == kQC);
-      const bool vert = p < kM - 1;
-      // centre lines: (z + W2[:,0]/2) + W2[:,1] y  or  (z + W2[:,1]/2) + W2[:,0] x;
-      // general queries (final phase): (z + W2[:,0]/2) + W2[:,0] (x - 1/2) + W2[:,1] y
-      const float* zs = zb + ((centre && !vert) ? kZRows * kD : 0) + zo * kD;
-      const float* w1s = S.w2 + ((centre && vert) ? kD : 0);
-      const float q1 = centre ? (vert ? qy : qx) : qx - 0.5f;
-#pragma unroll 1
-      for (int kh = 0; kh < 2; kh++) {   // K-half of the A image
+      // ---- split layer (Eq. 5, a3): h' = 2 GELU(z[s] + W2[:,0] x_p + W2[:,1] y_p)
+      // -> A operand, 16 columns (8 independent element pairs) per block; the
+      // W2 column pairs are 64-bit constant-bank operands, the row's query
+      // coordinates scalar-broadcast operands of FFMA2, and the next block's z
+      // is loaded from smem while this block's GELUs run (software pipeline)
+      const float* zs = zb + zo * kD;
+      const f2 QX = f2_make(qx, qx), QY = f2_make(qy, qy);
+      auto w2pair = [&](int col, int c) { return f2{*reinterpret_cast<const uint64_t*>(net.w2c + col * kD + c)}; };
+      float4 zbuf2[2][4];
 #pragma unroll
-        for (int j16 = 0; j16 < 4; j16++) {
-          const int c0 = 64 * kh + 16 * j16;
-          float v[16];
-          const f2 Q1 = f2_make(q1, q1);
+      for (int i = 0; i < 4; i++) zbuf2[0][i] = *reinterpret_cast<const float4*>(zs + 4 * i);
 #pragma unroll
-          for (int i = 0; i < 4; i++) {
-            const float4 zz = *reinterpret_cast<const float4*>(zs + c0 + 4 * i);
-            const float4 aa = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
-            f2 v01 = ffma2(f2_make(aa.x, aa.y), Q1, f2_make(zz.x, zz.y));
-            f2 v23 = ffma2(f2_make(aa.z, aa.w), Q1, f2_make(zz.z, zz.w));
-            if (!centre) {
-              const float4 bb = *reinterpret_cast<const float4*>(S.w2 + kD + c0 + 4 * i);
-              const f2 QY = f2_make(qy, qy);
-              v01 = ffma2(f2_make(bb.x, bb.y), QY, v01);
-              v23 = ffma2(f2_make(bb.z, bb.w), QY, v23);
-            }
-            f2_split(v01, v[4 * i], v[4 * i + 1]);
-            f2_split(v23, v[4 * i + 2], v[4 * i + 3]);
-          }
-          uint32_t w[8];
-          act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v), *reinterpret_cast<uint32_t(*)[4]>(w));
-          act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v + 8), *reinterpret_cast<uint32_t(*)[4]>(w + 4));
-          st_shared_v4(a_sw[2 * j16] + ((uint32_t)kh << 14), w[0], w[1], w[2], w[3]);
-          st_shared_v4(a_sw[2 * j16 + 1] + ((uint32_t)kh << 14), w[4], w[5], w[6], w[7]);
+      for (int b = 0; b < kD / 16; b++) {
+        const int c0 = 16 * b;
+        if (b + 1 < kD / 16) {
+#pragma unroll
+          for (int i = 0; i < 4; i++) zbuf2[(b + 1) & 1][i] = *reinterpret_cast<const float4*>(zs + c0 + 16 + 4 * i);
         }
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const float4 zz = zbuf2[b & 1][i];
+          f2 v01 = ffma2(w2pair(0, c0 + 4 * i), QX, f2_make(zz.x, zz.y));
+          f2 v23 = ffma2(w2pair(0, c0 + 4 * i + 2), QX, f2_make(zz.z, zz.w));
+          v01 = ffma2(w2pair(1, c0 + 4 * i), QY, v01);
+          v23 = ffma2(w2pair(1, c0 + 4 * i + 2), QY, v23);
+          f2_split(v01, v[4 * i], v[4 * i + 1]);
+          f2_split(v23, v[4 * i + 2], v[4 * i + 3]);
+        }
+        uint32_t w[8];
+        act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v), *reinterpret_cast<uint32_t(*)[4]>(w));
+        act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v + 8), *reinterpret_cast<uint32_t(*)[4]>(w + 4));
+        st_shared_v4(a_sw[2 * (b & 3)] + ((uint32_t)(b >> 2) << 14), w[0], w[1], w[2], w[3]);
+        st_shared_v4(a_sw[2 * (b & 3) + 1] + ((uint32_t)(b >> 2) << 14), w[4], w[5], w[6], w[7]);
       }
       if (lane == 0) MFP_TR(warp, j, 1, 3);
       fence_proxy_async();
