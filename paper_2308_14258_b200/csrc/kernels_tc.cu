@@ -234,10 +234,10 @@ struct Smem2 {
   uint8_t* W;      // [nh][18 KB]: this CTA's 64-row half + bias block
   uint8_t* A;      // [4][32 KB]
   uint8_t* ones;   // 4 KB
-  float* zbuf;     // [4 slots][2][4 subdomains][128]: z + W2[:,0]/2, z + W2[:,1]/2
+  float* zbuf;     // [4 slots][2 buffers][4 subdomains][128]: z of a tile's subdomains (double-buffered)
   float* w2;       // [2][128]: W2[:,0], W2[:,1]
   float* wo;       // [128]
-  uint64_t* bars;  // a_full[4] (used in the even CTA), d_full[4]
+  uint64_t* bars;  // a_full[4] (used in the even CTA), d_full[4], z_full[4]
   uint32_t* tmem_slot;
 };
 
@@ -250,13 +250,13 @@ __device__ __forceinline__ Smem2 carve2(uint8_t* raw, int nh) {
   s.w2 = s.zbuf + kSlots2 * 2 * kZRows * kD;
   s.wo = s.w2 + 2 * kD;
   s.bars = (uint64_t*)(s.wo + kD);
-  s.tmem_slot = (uint32_t*)(s.bars + 2 * kSlots2);
+  s.tmem_slot = (uint32_t*)(s.bars + 3 * kSlots2);
   return s;
 }
 
 size_t smem_bytes2(int n_hidden) {
   return (size_t)n_hidden * kHalf + kSlots2 * kTile + kOnes + 4 * ((size_t)kSlots2 * 2 * kZRows * kD + 3 * kD) +
-         16 * kSlots2 + 16;
+         24 * kSlots2 + 16;
 }
 
 // MFP_TRACE builds: per-event clock64 stamps of CTAs 0/1 (DESIGN.md §6 timeline).
@@ -303,6 +303,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
     for (int s = 0; s < kSlots2; s++) {
       mbar_init(&S.bars[s], 8);             // a_full[s]: 4 warps x 2 CTAs (elected lanes)
       mbar_init(&S.bars[kSlots2 + s], 1);   // d_full[s]: multicast commit
+      mbar_init(&S.bars[2 * kSlots2 + s], 4);   // z_full[s]: the slot's 4 warps staged the next tile's z
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -371,7 +372,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
 #pragma unroll
     for (int j = 0; j < 8; j++) a_sw[j] = a_row + ((uint32_t)(j ^ r7) << 4);
     const uint32_t t_row = tmem + (uint32_t)(slot * kD) + ((uint32_t)(quad * 32) << 16);
-    float* zb = S.zbuf + slot * 2 * kZRows * kD;
+    float* zb0 = S.zbuf + slot * 2 * kZRows * kD;   // buffer (tile iteration & 1)
     const float bo = __ldg(net.bo);
     const int zi = 4 * row, zr_ = zi >> 7, zc = zi & 127;
     auto row0_of = [&](int64_t j) -> int64_t { return (cid + j * ncl) * (2 * kRows) + rank * kRows; };
@@ -382,19 +383,31 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
     };
     // z of the tile's <= 4 subdomains, staged in smem (each row reads its
     // subdomain's 128 values; W2 comes from the constant bank, DevNet::w2c)
-    auto z_stage = [&](const float4 v) { *reinterpret_cast<float4*>(zb + zi) = v; };
+    // staged into buffer `buf`, then the warp arrives on z_full[slot] (release);
+    // a tile waits for its buffer's phase (acquire) instead of a slot barrier, so
+    // staging the next tile right after this tile's split layer takes the 4
+    // warps' spread out of the critical path.  Two buffers: a warp overwrites
+    // buffer b ^ 1 only after every warp of the slot has finished the split layer
+    // that read it (the MMA barriers of the tile in between order them)
+    auto z_stage = [&](const float4 v, int buf) {
+      *reinterpret_cast<float4*>(zb0 + buf * kZRows * kD + zi) = v;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.bars[2 * kSlots2 + slot]);
+    };
     auto arrive_a = [&]() {
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(&S.bars[slot], 0u);
     };
-    if (slot < nloc) z_stage(z_fetch(slot));
-    uint32_t pd = 0u;
+    if (slot < nloc) z_stage(z_fetch(slot), 0);
+    uint32_t pd = 0u, pz = 0u;
     for (int64_t j = slot; j < nloc; j += kSlots2) {
       if (lane == 0) MFP_TR(warp, j, 0, 3);
       const int64_t row0 = row0_of(j);
       int64_t s_first = row0 / q;
       if (s_first > nsub - 1) s_first = nsub - 1;
-      named_sync(1 + slot, 128);   // this tile's staged z visible to the slot's 4 warps
+      const int zbuf_i = (int)pz;   // buffer of this tile = tile iteration parity
+      mbar_wait(&S.bars[2 * kSlots2 + slot], pz);   // this tile's staged z visible to the slot's 4 warps
+      pz ^= 1u;
       if (lane == 0) MFP_TR(warp, j, 2, 3);
       const bool have_next = j + kSlots2 < nloc;
       float4 znext = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -414,7 +427,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       // W2 column pairs are 64-bit constant-bank operands, the row's query
       // coordinates scalar-broadcast operands of FFMA2, and the next block's z
       // is loaded from smem while this block's GELUs run (software pipeline)
-      const float* zs = zb + zo * kD;
+      const float* zs = zb0 + zbuf_i * kZRows * kD + zo * kD;
       const f2 QX = f2_make(qx, qx), QY = f2_make(qy, qy);
       auto w2pair = [&](int col, int c) { return f2{*reinterpret_cast<const uint64_t*>(net.w2c + col * kD + c)}; };
       float4 zbuf2[2][4];
@@ -448,6 +461,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       fence_proxy_async();
       arrive_a();
       if (lane == 0) MFP_TR(warp, j, 0, 0);
+      if (have_next) z_stage(znext, zbuf_i ^ 1);   // next tile of the slot
 
       // ---- hidden layers (a4) and head (a5): TMEM accumulator -> GELU ->
       // next A operand, or GELU + head dot on the last layer
@@ -502,7 +516,6 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
           if (lane == 0) MFP_TR(warp, j, l + 1, 0);
         }
       }
-      if (have_next) z_stage(znext);
       float y0, y1;
       f2_split(yacc, y0, y1);
       if (valid) sink_store(sink, sidx, p, (y0 + y1) + bo);   // a6 / final-phase field
