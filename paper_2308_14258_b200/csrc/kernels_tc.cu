@@ -237,7 +237,7 @@ struct Smem2 {
   float* zbuf;     // [4 slots][2 buffers][4 subdomains][128]: z of a tile's subdomains (double-buffered)
   float* w2;       // [2][128]: W2[:,0], W2[:,1]
   float* wo;       // [128]
-  uint64_t* bars;  // a_full[4] (used in the even CTA), d_full[4], z_full[4]
+  uint64_t* bars;  // a_full[4] (used in the even CTA), d_full[4], z_full[4], w_full
   uint32_t* tmem_slot;
 };
 
@@ -250,13 +250,13 @@ __device__ __forceinline__ Smem2 carve2(uint8_t* raw, int nh) {
   s.w2 = s.zbuf + kSlots2 * 2 * kZRows * kD;
   s.wo = s.w2 + 2 * kD;
   s.bars = (uint64_t*)(s.wo + kD);
-  s.tmem_slot = (uint32_t*)(s.bars + 3 * kSlots2);
+  s.tmem_slot = (uint32_t*)(s.bars + 3 * kSlots2 + 1);
   return s;
 }
 
 size_t smem_bytes2(int n_hidden) {
   return (size_t)n_hidden * kHalf + kSlots2 * kTile + kOnes + 4 * ((size_t)kSlots2 * 2 * kZRows * kD + 3 * kD) +
-         24 * kSlots2 + 16;
+         24 * kSlots2 + 8 + 16;
 }
 
 // MFP_TRACE builds: per-event clock64 stamps of CTAs 0/1 (DESIGN.md §6 timeline).
@@ -266,8 +266,18 @@ __device__ unsigned long long g_trace[2][18][32][8][4];   // [cta][warp][tile][l
   do {                                                                                            \
     if (blockIdx.x < 2 && (jt) < 32 && (l) < 8) g_trace[blockIdx.x][w][jt][l][ev] = clock64(); \
   } while (0)
+// per-CTA globaltimer stamps (ns): entry, past the prologue + PDL wait, last
+// tile's head done (per warp max), exit
+__device__ unsigned long long g_cta_t[256][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define MFP_CT(ev) do { if (blockIdx.x < 256) atomicMax(&g_cta_t[blockIdx.x][ev], gtimer()); } while (0)
 #else
 #define MFP_TR(w, jt, l, ev) do { } while (0)
+#define MFP_CT(ev) do { } while (0)
 #endif
 
 // Pair tile t of this cluster = rows [256 t, 256 t + 256) of the batch (row =
@@ -280,16 +290,22 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
   const Smem2 S = carve2(smem_raw, nh);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
+  if (threadIdx.x == 0) MFP_CT(0);
 
-  // ---- prologue: this CTA's weight half-images, head / split-layer vectors,
-  // the constant ones block of the bias step, barriers, TMEM
+  // ---- prologue: this CTA's weight half-images (TMA bulk copies issued first,
+  // waited for after the PDL wait, so they land under the barrier / TMEM set-up
+  // and the predecessor's tail), head vector, the constant ones block of the
+  // bias step, barriers, TMEM
+  uint64_t* w_full = S.bars + 3 * kSlots2;
+  if (threadIdx.x == 0) {
+    mbar_init(w_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arrive_expect_tx(w_full, (uint32_t)(nh * kHalf));
+    for (int l = 0; l < nh; l++)
+      bulk_g2s(smem_u32(S.W + l * kHalf),
+               reinterpret_cast<const uint8_t*>(net.Wh_sw2) + (size_t)l * 2 * kHalf + rank * kHalf, kHalf, w_full);
+  }
   {
-    for (int l = 0; l < nh; l++) {
-      const uint4* src =
-          reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(net.Wh_sw2) + (size_t)l * 2 * kHalf + rank * kHalf);
-      uint4* dst = reinterpret_cast<uint4*>(S.W + l * kHalf);
-      for (int i = threadIdx.x; i < kHalf / 16; i += kThreads2) dst[i] = __ldg(src + i);
-    }
     for (int i = threadIdx.x; i < kD; i += kThreads2) S.wo[i] = (GELU >= 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
     if (threadIdx.x < kRows) {
       const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
@@ -321,6 +337,9 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
   const uint32_t tmem = *S.tmem_slot;
   pdl_launch_dependents();
   pdl_wait();      // z (embed) and the lattice (previous phases) complete from here on
+  mbar_wait(w_full, 0u);   // this CTA's weight halves landed
+  cluster_sync();          // ... and the peer CTA's (the pair MMAs read both)
+  if (threadIdx.x == 0) MFP_CT(1);
 
   const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int64_t ntiles = (total_rows + 2 * kRows - 1) / (2 * kRows);
@@ -520,10 +539,12 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       f2_split(yacc, y0, y1);
       if (valid) sink_store(sink, sidx, p, (y0 + y1) + bo);   // a6 / final-phase field
     }
+    if (lane == 0) MFP_CT(2);
   }
   tc_fence_before();
   __syncthreads();
   cluster_sync();
+  if (threadIdx.x == 0) MFP_CT(3);
   if (warp == kAllocWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
@@ -1221,6 +1242,14 @@ bool chain_tc_available() { return true; }
 extern "C" int mfp_debug_trace(void* host, size_t bytes) {
   const size_t n = bytes < sizeof(tc2::g_trace) ? bytes : sizeof(tc2::g_trace);
   return cudaMemcpyFromSymbol(host, tc2::g_trace, n) == cudaSuccess ? (int)n : -1;
+}
+extern "C" int mfp_debug_cta_times(void* host, size_t bytes, int reset) {
+  const size_t n = bytes < sizeof(tc2::g_cta_t) ? bytes : sizeof(tc2::g_cta_t);
+  if (reset) {
+    static unsigned long long zero[256][4];
+    return cudaMemcpyToSymbol(tc2::g_cta_t, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
+  }
+  return cudaMemcpyFromSymbol(host, tc2::g_cta_t, n) == cudaSuccess ? (int)n : -1;
 }
 #endif
 

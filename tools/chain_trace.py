@@ -60,7 +60,23 @@ for tile in range(4, 28):
         nst = min(T[w, tile + 4, 0, 3] for w in ws)
         if nst > 0:
             tails.append(nst - g(L - 1, 1, max))
-m = lambda v: float(np.mean(v)) if v else -1
-print(f"layers {L}: act phase {m(acts):.0f} (compute {m(comp):.0f}, fence+arrive {m(fin):.0f}) | round trip {m(rts):.0f} "
-      f"(issuer wait after CTA0 arrivals {m(iss):.0f}, issue->commit {m(exe):.0f}) | L0: tile start->z sync {m(l0s):.0f}, "
-      f"sync->compute end {m(l0):.0f} | head+tail {m(tails):.0f}")
+mean_ = lambda v: float(np.mean(v)) if v else -1
+print(f"layers {L}: act phase {mean_(acts):.0f} (compute {mean_(comp):.0f}, fence+arrive {mean_(fin):.0f}) | round trip {mean_(rts):.0f} "
+      f"(issuer wait after CTA0 arrivals {mean_(iss):.0f}, issue->commit {mean_(exe):.0f}) | L0: tile start->z sync {mean_(l0s):.0f}, "
+      f"sync->compute end {mean_(l0):.0f} | head+tail {mean_(tails):.0f}")
+
+# per-CTA globaltimer stamps of one more launch: prologue, per-CTA work span, tail
+g = lib._lib.mfp_debug_cta_times
+g.restype = ctypes.c_int
+g.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+ct = np.zeros((256, 4), np.uint64)
+g(ct.ctypes.data, ct.nbytes, 1)
+m.sdnet_batch(gb, 0)
+torch.cuda.synchronize()
+assert g(ct.ctypes.data, ct.nbytes, 0) > 0
+c = ct[:148].astype(np.int64)
+t0 = c[:, 0].min()
+ent, pro, last, ex = (c[:, 0] - t0) / 1e3, (c[:, 1] - t0) / 1e3, (c[:, 2] - t0) / 1e3, (c[:, 3] - t0) / 1e3
+q = lambda v: " ".join(f"{x:.1f}" for x in np.percentile(v, [0, 50, 100]))
+print(f"per-CTA us from the first entry (min/median/max): entry {q(ent)} | past prologue {q(pro)} | last head done {q(last)} | exit {q(ex)}")
+
