@@ -274,7 +274,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define MFP_CT(ev) do { if (blockIdx.x < 256) atomicMax(&g_cta_t[blockIdx.x][ev], gtimer()); } while (0)
+__device__ unsigned long long g_cta_c[256][4];   // clock64 at the same events (SM clock = dclock / dns)
+#define MFP_CT(ev)                                                                       \
+  do {                                                                                   \
+    if (blockIdx.x < 256) {                                                              \
+      atomicMax(&g_cta_t[blockIdx.x][ev], gtimer());                                     \
+      atomicMax(&g_cta_c[blockIdx.x][ev], (unsigned long long)clock64());                \
+    }                                                                                    \
+  } while (0)
 #else
 #define MFP_TR(w, jt, l, ev) do { } while (0)
 #define MFP_CT(ev) do { } while (0)
@@ -953,11 +960,11 @@ struct SmemS {
   uint8_t* A;      // [2][hi 32 KB | lo 32 KB]
   uint8_t* W;      // [nh][18 KB]
   uint8_t* ones;   // 4 KB
-  float* zbuf;     // [2 slots][4 subdomains][128]: z + (W2[:,0] + W2[:,1]) / 2
+  float* zbuf;     // [2 slots][2 buffers][4 subdomains][128]: z of a tile's subdomains (double-buffered)
   float* w2;       // [2][128]
   float* wo;       // [128]
   float* hpart;    // [2][128]
-  uint64_t* bars;  // a_full[2] d_full[2]
+  uint64_t* bars;  // a_full[2] d_full[2] z_full[2]
   uint32_t* tmem_slot;
 };
 __device__ __forceinline__ SmemS carve_s(uint8_t* raw) {
@@ -966,16 +973,16 @@ __device__ __forceinline__ SmemS carve_s(uint8_t* raw) {
   s.W = s.A + kSlots * kAs;
   s.ones = s.W + kMaxHidden * kHalfB;
   s.zbuf = (float*)(s.ones + kOnes);
-  s.w2 = s.zbuf + kSlots * kZRows * kD;
+  s.w2 = s.zbuf + kSlots * 2 * kZRows * kD;
   s.wo = s.w2 + 2 * kD;
   s.hpart = s.wo + kD;
   s.bars = (uint64_t*)(s.hpart + kSlots * kRows);
-  s.tmem_slot = (uint32_t*)(s.bars + 2 * kSlots);
+  s.tmem_slot = (uint32_t*)(s.bars + 3 * kSlots);
   return s;
 }
 constexpr size_t smem_bytes_s() {
   return (size_t)kSlots * kAs + kMaxHidden * kHalfB + kOnes +
-         4 * ((size_t)kSlots * kZRows * kD + 3 * kD + kSlots * kRows) + 16 * kSlots + 16;
+         4 * ((size_t)kSlots * 2 * kZRows * kD + 3 * kD + kSlots * kRows) + 24 * kSlots + 16;
 }
 
 __device__ __forceinline__ void unpack_f16x2(uint32_t w, float& f0, float& f1) {
@@ -1033,6 +1040,7 @@ k_chain_tc2s(const float* __restrict__ z, int64_t total_rows, int q, DevNet net,
     for (int s = 0; s < kSlots; s++) {
       mbar_init(&a_full[s], 16);   // 8 warps x 2 CTAs (elected lanes)
       mbar_init(&d_full[s], 1);
+      mbar_init(&S.bars[2 * kSlots + s], 8);   // z_full[s]: the slot's 8 warps staged the next tile's z
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1098,7 +1106,7 @@ k_chain_tc2s(const float* __restrict__ z, int64_t total_rows, int q, DevNet net,
 #pragma unroll
     for (int j = 0; j < 8; j++) a_sw[j] = a_row + ((uint32_t)(j ^ r7) << 4);
     const uint32_t t_row = tmem + (uint32_t)(slot * kD + ch * 64) + ((uint32_t)(quad * 32) << 16);
-    float* zb = S.zbuf + slot * kZRows * kD;
+    float* zb0 = S.zbuf + slot * 2 * kZRows * kD;   // buffer (tile iteration & 1)
     const float bo = __ldg(net.bo);
     const int zi = 2 * tis, zr_ = zi >> 7, zc = zi & (kD - 1);
     auto row0_of = [&](int64_t j) -> int64_t { return (cid + j * ncl) * (2 * kRows) + rank * kRows; };
@@ -1107,9 +1115,12 @@ k_chain_tc2s(const float* __restrict__ z, int64_t total_rows, int q, DevNet net,
       if (sidx > nsub - 1) sidx = nsub - 1;
       return __ldg(reinterpret_cast<const float2*>(z + sidx * kD + zc));
     };
-    auto z_stage = [&](const float2 v) {
-      *reinterpret_cast<float2*>(zb + zi) = make_float2(fmaf(0.5f, S.w2[zc] + S.w2[kD + zc], v.x),
-                                                        fmaf(0.5f, S.w2[zc + 1] + S.w2[kD + zc + 1], v.y));
+    // plain z, double-buffered and published by z_full[slot] (8 warp arrivals), the
+    // next tile staged right after this tile's split layer (as in tc2)
+    auto z_stage = [&](const float2 v, int buf) {
+      *reinterpret_cast<float2*>(zb0 + buf * kZRows * kD + zi) = v;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.bars[2 * kSlots + slot]);
     };
     auto arrive_a = [&]() {
       __syncwarp();
@@ -1119,13 +1130,15 @@ k_chain_tc2s(const float* __restrict__ z, int64_t total_rows, int q, DevNet net,
       st_shared_v4(a_sw[g], hi[0], hi[1], hi[2], hi[3]);
       st_shared_v4(a_sw[g] + (uint32_t)kTile, lo[0], lo[1], lo[2], lo[3]);
     };
-    if (slot < nloc) z_stage(z_fetch(slot));
-    uint32_t pd = 0u;
+    if (slot < nloc) z_stage(z_fetch(slot), 0);
+    uint32_t pd = 0u, pz = 0u;
     for (int64_t j = slot; j < nloc; j += kSlots) {
       const int64_t row0 = row0_of(j);
       int64_t s_first = row0 / q;
       if (s_first > nsub - 1) s_first = nsub - 1;
-      named_sync(1 + slot, 256);
+      const int zbuf_i = (int)pz;
+      mbar_wait(&S.bars[2 * kSlots + slot], pz);   // this tile's staged z visible to the slot's 8 warps
+      pz ^= 1u;
       const bool have_next = j + kSlots < nloc;
       float2 znext = make_float2(0.f, 0.f);
       if (have_next) znext = z_fetch(j + kSlots);
@@ -1138,40 +1151,50 @@ k_chain_tc2s(const float* __restrict__ z, int64_t total_rows, int q, DevNet net,
       query_xy(q, p, &qx, &qy);
       int zo = (int)(sidx - s_first);
       if (zo < 0 || zo >= kZRows) zo = 0;
-      // ---- split layer (Eq. 5) over this thread's 64 columns (K-atom ch)
-      const bool centre = (q == kQC);
-      const bool vert = p < kM - 1;
-      const float* zs = zb + zo * kD + ch * 64;
-      const float* w1s = S.w2 + ((centre && vert) ? kD : 0) + ch * 64;
-      const float q1 = (centre && vert) ? qy - 0.5f : qx - 0.5f;
+      // ---- split layer (Eq. 5) over this thread's 64 columns (K-atom ch):
+      // x = z + W2[:,0] x_p + W2[:,1] y_p with W2's column pairs as constant-bank
+      // operands (compile-time offsets: one code path per column half), the next
+      // 16 columns of z loaded under the current block's GELUs
+      const float* zs = zb0 + zbuf_i * kZRows * kD + zo * kD + ch * 64;
+      const f2 QX = f2_make(qx, qx), QY = f2_make(qy, qy);
+      auto split_half = [&](auto ch_tag) {
+        constexpr int CH = decltype(ch_tag)::value;
+        auto w2pair = [&](int col, int c) {
+          return f2{*reinterpret_cast<const uint64_t*>(net.w2c + col * kD + CH * 64 + c)};
+        };
+        float4 zq[2][4];
 #pragma unroll
-      for (int j16 = 0; j16 < 4; j16++) {
-        const int c0 = 16 * j16;
-        float v[16];
-        const f2 Q1 = f2_make(q1, q1);
+        for (int i = 0; i < 4; i++) zq[0][i] = *reinterpret_cast<const float4*>(zs + 4 * i);
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
-          const float4 zz = *reinterpret_cast<const float4*>(zs + c0 + 4 * i);
-          const float4 aa = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
-          f2 v01 = ffma2(f2_make(aa.x, aa.y), Q1, f2_make(zz.x, zz.y));
-          f2 v23 = ffma2(f2_make(aa.z, aa.w), Q1, f2_make(zz.z, zz.w));
-          if (!centre) {
-            const float4 bb = *reinterpret_cast<const float4*>(S.w2 + kD + ch * 64 + c0 + 4 * i);
-            const f2 QY = f2_make(qy - 0.5f, qy - 0.5f);
-            v01 = ffma2(f2_make(bb.x, bb.y), QY, v01);
-            v23 = ffma2(f2_make(bb.z, bb.w), QY, v23);
+        for (int j16 = 0; j16 < 4; j16++) {
+          const int c0 = 16 * j16;
+          if (j16 + 1 < 4) {
+#pragma unroll
+            for (int i = 0; i < 4; i++) zq[(j16 + 1) & 1][i] = *reinterpret_cast<const float4*>(zs + c0 + 16 + 4 * i);
           }
-          f2_split(v01, v[4 * i], v[4 * i + 1]);
-          f2_split(v23, v[4 * i + 2], v[4 * i + 3]);
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 4; i++) {
+            const float4 zz = zq[j16 & 1][i];
+            f2 v01 = ffma2(w2pair(0, c0 + 4 * i), QX, f2_make(zz.x, zz.y));
+            f2 v23 = ffma2(w2pair(0, c0 + 4 * i + 2), QX, f2_make(zz.z, zz.w));
+            v01 = ffma2(w2pair(1, c0 + 4 * i), QY, v01);
+            v23 = ffma2(w2pair(1, c0 + 4 * i + 2), QY, v23);
+            f2_split(v01, v[4 * i], v[4 * i + 1]);
+            f2_split(v23, v[4 * i + 2], v[4 * i + 3]);
+          }
+          uint32_t hi[4], lo[4];
+          act8_split<GELU>(*reinterpret_cast<const float(*)[8]>(v), hi, lo);
+          store8(2 * j16, hi, lo);
+          act8_split<GELU>(*reinterpret_cast<const float(*)[8]>(v + 8), hi, lo);
+          store8(2 * j16 + 1, hi, lo);
         }
-        uint32_t hi[4], lo[4];
-        act8_split<GELU>(*reinterpret_cast<const float(*)[8]>(v), hi, lo);
-        store8(2 * j16, hi, lo);
-        act8_split<GELU>(*reinterpret_cast<const float(*)[8]>(v + 8), hi, lo);
-        store8(2 * j16 + 1, hi, lo);
-      }
+      };
+      if (ch == 0) split_half(std::integral_constant<int, 0>{});
+      else split_half(std::integral_constant<int, 1>{});
       fence_proxy_async();
       arrive_a();
+      if (have_next) z_stage(znext, zbuf_i ^ 1);   // next tile of the slot
       // ---- hidden layers (a4) and head (a5)
       f2 yacc = f2_make(0.f, 0.f);
       for (int l = 0; l < nh; l++) {
@@ -1221,7 +1244,6 @@ k_chain_tc2s(const float* __restrict__ z, int64_t total_rows, int q, DevNet net,
       f2_split(yacc, y0, y1);
       if (ch == 1) S.hpart[slot * kRows + row] = y0 + y1;
       named_sync(1 + slot, 256);
-      if (have_next) z_stage(znext);
       if (ch == 0 && valid) sink_store(sink, sidx, p, ((y0 + y1) + S.hpart[slot * kRows + row]) + bo);
     }
   }
@@ -1245,10 +1267,12 @@ extern "C" int mfp_debug_trace(void* host, size_t bytes) {
 }
 extern "C" int mfp_debug_cta_times(void* host, size_t bytes, int reset) {
   const size_t n = bytes < sizeof(tc2::g_cta_t) ? bytes : sizeof(tc2::g_cta_t);
-  if (reset) {
+  if (reset == 1) {
     static unsigned long long zero[256][4];
+    cudaMemcpyToSymbol(tc2::g_cta_c, zero, sizeof(zero));
     return cudaMemcpyToSymbol(tc2::g_cta_t, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
   }
+  if (reset == 2) return cudaMemcpyFromSymbol(host, tc2::g_cta_c, n) == cudaSuccess ? (int)n : -1;
   return cudaMemcpyFromSymbol(host, tc2::g_cta_t, n) == cudaSuccess ? (int)n : -1;
 }
 #endif

@@ -14,7 +14,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from mfp_inputs import random_weights  # noqa: E402
 from paper_2308_14258_b200 import mfp as lib  # noqa: E402
 
-B = 16256
+B = int(os.environ.get("MFP_TRACE_B", "16256"))   # default: one C5 phase
 cfg = lib.make_config(4096, 4096, precision=1, subsolver=lib.SDNET)
 net = lib.make_net(gelu=1)
 w = random_weights(seed=0)
@@ -80,3 +80,8 @@ ent, pro, last, ex = (c[:, 0] - t0) / 1e3, (c[:, 1] - t0) / 1e3, (c[:, 2] - t0) 
 q = lambda v: " ".join(f"{x:.1f}" for x in np.percentile(v, [0, 50, 100]))
 print(f"per-CTA us from the first entry (min/median/max): entry {q(ent)} | past prologue {q(pro)} | last head done {q(last)} | exit {q(ex)}")
 
+cc = np.zeros((256, 4), np.uint64)
+assert g(cc.ctypes.data, cc.nbytes, 2) > 0
+cc = cc[:148].astype(np.int64)
+ghz = (cc[:, 2] - cc[:, 1]) / np.maximum(c[:, 2] - c[:, 1], 1)
+print(f"SM clock over each CTA's work span (GHz, min/median/max): {q(ghz)}")
