@@ -1201,11 +1201,12 @@ mfp_status mfp_init(const mfp_config* cfg, const mfp_sdnet_desc* net, const floa
       }
       c->dn.convw[88] = params[88];
     }
-    if (net->d == kD) {
-      const float* W2h = params + 89 + (int64_t)net->d * kNB;   // [d][2]
-      for (int n = 0; n < kD; n++) {
+    {
+      const int dd = net->d;   // 128 or 256 (check_net)
+      const float* W2h = params + 89 + (int64_t)dd * kNB;   // [d][2]
+      for (int n = 0; n < dd; n++) {
         c->dn.w2c[n] = W2h[2 * n];
-        c->dn.w2c[kD + n] = W2h[2 * n + 1];
+        c->dn.w2c[dd + n] = W2h[2 * n + 1];
       }
     }
     CK(cudaMemsetAsync((void*)c->dn.Wh_sw2, 0, wimg_elems(net->d, net->n_hidden) * 2, s));

@@ -613,11 +613,10 @@ struct SmemW {
   uint8_t* ring;   // [4][16 KB]
   uint8_t* bias;   // [nh][4 KB]
   uint8_t* ones;   // 4 KB
-  float* zbuf;     // [2 slots][4 subdomains][256]: z + (W2[:,0] + W2[:,1]) / 2
-  float* w2;       // [2][256]: W2[:,0], W2[:,1]
+  float* zbuf;     // [2 slots][2 buffers][4 subdomains][256]: z of a tile's subdomains (double-buffered)
   float* wo;       // [256]
   float* hpart;    // [2 slots][128]: head partial dot of the ch = 1 half
-  uint64_t* bars;  // a_full[2] d_full[2] full[4] pfull[4] empty[4]
+  uint64_t* bars;  // a_full[2] d_full[2] full[4] pfull[4] empty[4] z_full[2]
   uint32_t* tmem_slot;
 };
 __device__ __forceinline__ SmemW carve_w(uint8_t* raw) {
@@ -627,16 +626,15 @@ __device__ __forceinline__ SmemW carve_w(uint8_t* raw) {
   s.bias = s.ring + kRing * kChunkB;
   s.ones = s.bias + kMaxHidden * kBiasB;
   s.zbuf = (float*)(s.ones + kOnes);
-  s.w2 = s.zbuf + kSlots * kZRows * D;
-  s.wo = s.w2 + 2 * D;
+  s.wo = s.zbuf + kSlots * 2 * kZRows * D;
   s.hpart = s.wo + D;
   s.bars = (uint64_t*)(s.hpart + kSlots * kRows);
-  s.tmem_slot = (uint32_t*)(s.bars + 4 + 3 * kRing);
+  s.tmem_slot = (uint32_t*)(s.bars + 4 + 3 * kRing + kSlots);
   return s;
 }
 constexpr size_t smem_bytes_w() {
   return (size_t)kSlots * kA + kRing * kChunkB + kMaxHidden * kBiasB + kOnes +
-         4 * ((size_t)kSlots * kZRows * D + 3 * D + kSlots * kRows) + 8 * (4 + 3 * kRing) + 16;
+         4 * ((size_t)kSlots * 2 * kZRows * D + D + kSlots * kRows) + 8 * (4 + 3 * kRing + kSlots) + 16;
 }
 
 template <int GELU, int F16>
@@ -661,11 +659,7 @@ k_chain_tc2w(const float* __restrict__ z, int64_t total_rows, int q, DevNet net,
     uint4* dst = reinterpret_cast<uint4*>(S.bias + l * kBiasB);
     for (int i = threadIdx.x; i < kBiasB / 16; i += kThreads) dst[i] = __ldg(src + i);
   }
-  for (int i = threadIdx.x; i < D; i += kThreads) {
-    S.wo[i] = (GELU >= 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
-    S.w2[i] = __ldg(net.W2 + 2 * i);
-    S.w2[D + i] = __ldg(net.W2 + 2 * i + 1);
-  }
+  for (int i = threadIdx.x; i < D; i += kThreads) S.wo[i] = (GELU >= 1 ? 0.5f : 1.0f) * __ldg(net.wo + i);
   if (threadIdx.x < kRows) {
     const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
     const int r = threadIdx.x;
@@ -677,6 +671,7 @@ k_chain_tc2w(const float* __restrict__ z, int64_t total_rows, int q, DevNet net,
     for (int s = 0; s < kSlots; s++) {
       mbar_init(&a_full[s], 16);   // 8 warps x 2 CTAs (elected lanes)
       mbar_init(&d_full[s], 1);    // multicast commit
+      mbar_init(&S.bars[4 + 3 * kRing + s], 8);   // z_full[s]: the slot's 8 warps staged the next tile's z
     }
     for (int i = 0; i < kRing; i++) {
       mbar_init(&full[i], 1);      // producer's arrive.expect_tx + the chunk's bytes
@@ -782,7 +777,7 @@ k_chain_tc2w(const float* __restrict__ z, int64_t total_rows, int q, DevNet net,
 #pragma unroll
     for (int j = 0; j < 8; j++) a_sw[j] = a_row + ((uint32_t)(j ^ r7) << 4);
     const uint32_t t_row = tmem + (uint32_t)(slot * D + ch * 128) + ((uint32_t)(quad * 32) << 16);
-    float* zb = S.zbuf + slot * kZRows * D;
+    float* zb0 = S.zbuf + slot * 2 * kZRows * D;   // buffer (tile iteration & 1)
     const float bo = __ldg(net.bo);
     const int zi = 4 * tis, zr_ = zi >> 8, zc = zi & (D - 1);
     auto row0_of = [&](int64_t j) -> int64_t { return (cid + j * ncl) * (2 * kRows) + rank * kRows; };
@@ -791,23 +786,27 @@ k_chain_tc2w(const float* __restrict__ z, int64_t total_rows, int q, DevNet net,
       if (sidx > nsub - 1) sidx = nsub - 1;
       return __ldg(reinterpret_cast<const float4*>(z + sidx * D + zc));
     };
-    auto z_stage = [&](const float4 v) {
-      const float4 a = *reinterpret_cast<const float4*>(S.w2 + zc);
-      const float4 b = *reinterpret_cast<const float4*>(S.w2 + D + zc);
-      *reinterpret_cast<float4*>(zb + zi) = make_float4(fmaf(0.5f, a.x + b.x, v.x), fmaf(0.5f, a.y + b.y, v.y),
-                                                        fmaf(0.5f, a.z + b.z, v.z), fmaf(0.5f, a.w + b.w, v.w));
+    // plain z, double-buffered and published by z_full[slot] (8 warp arrivals),
+    // the next tile staged right after this tile's split layer (as in tc2)
+    uint64_t* z_full = S.bars + 4 + 3 * kRing;
+    auto z_stage = [&](const float4 v, int buf) {
+      *reinterpret_cast<float4*>(zb0 + buf * kZRows * D + zi) = v;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&z_full[slot]);
     };
     auto arrive_a = [&]() {
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(&a_full[slot], 0u);
     };
-    if (slot < nloc) z_stage(z_fetch(slot));
-    uint32_t pd = 0u;
+    if (slot < nloc) z_stage(z_fetch(slot), 0);
+    uint32_t pd = 0u, pz = 0u;
     for (int64_t j = slot; j < nloc; j += kSlots) {
       const int64_t row0 = row0_of(j);
       int64_t s_first = row0 / q;
       if (s_first > nsub - 1) s_first = nsub - 1;
-      named_sync(1 + slot, 256);   // this tile's staged z visible to the slot's 8 warps
+      const int zbuf_i = (int)pz;
+      mbar_wait(&z_full[slot], pz);   // this tile's staged z visible to the slot's 8 warps
+      pz ^= 1u;
       const bool have_next = j + kSlots < nloc;
       float4 znext = make_float4(0.f, 0.f, 0.f, 0.f);
       if (have_next) znext = z_fetch(j + kSlots);
@@ -821,47 +820,50 @@ k_chain_tc2w(const float* __restrict__ z, int64_t total_rows, int q, DevNet net,
       int zo = (int)(sidx - s_first);
       if (zo < 0 || zo >= kZRows) zo = 0;
 
-      // ---- split layer (Eq. 5, a3): h' = 2 GELU(z[s] + W2 x_p) over this
-      // thread's 128 columns -> A operand (K-atoms 2 ch, 2 ch + 1)
-      const bool centre = (q == kQC);
-      const bool vert = p < kM - 1;
-      // staged zc = z + (W2[:,0] + W2[:,1]) / 2: vertical centre line (x = 1/2)
-      // zc + W2[:,1] (y - 1/2); horizontal (y = 1/2) zc + W2[:,0] (x - 1/2);
-      // general queries zc + W2[:,0] (x - 1/2) + W2[:,1] (y - 1/2)
-      const float* zs = zb + zo * D + ch * 128;
-      const float* w1s = S.w2 + ((centre && vert) ? D : 0) + ch * 128;
-      const float q1 = (centre && vert) ? qy - 0.5f : qx - 0.5f;
-#pragma unroll 1
-      for (int kh = 0; kh < 2; kh++) {
+      // ---- split layer (Eq. 5, a3): h' = 2 GELU(z[s] + W2[:,0] x_p + W2[:,1] y_p)
+      // over this thread's 128 columns -> A operand (K-atoms 2 ch, 2 ch + 1); W2's
+      // column pairs are constant-bank operands (one code path per column half),
+      // the next 16 columns of z are loaded under the current block's GELUs
+      const float* zs = zb0 + zbuf_i * kZRows * D + zo * D + ch * 128;
+      const f2 QX = f2_make(qx, qx), QY = f2_make(qy, qy);
+      auto split_half = [&](auto ch_tag) {
+        constexpr int CH = decltype(ch_tag)::value;
+        auto w2pair = [&](int col, int c) {
+          return f2{*reinterpret_cast<const uint64_t*>(net.w2c + col * D + CH * 128 + c)};
+        };
+        float4 zq[2][4];
 #pragma unroll
-        for (int j16 = 0; j16 < 4; j16++) {
-          const int c0 = 64 * kh + 16 * j16;
+        for (int i = 0; i < 4; i++) zq[0][i] = *reinterpret_cast<const float4*>(zs + 4 * i);
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+          const int c0 = 16 * b;
+          if (b + 1 < 8) {
+#pragma unroll
+            for (int i = 0; i < 4; i++) zq[(b + 1) & 1][i] = *reinterpret_cast<const float4*>(zs + c0 + 16 + 4 * i);
+          }
           float v[16];
-          const f2 Q1 = f2_make(q1, q1);
 #pragma unroll
           for (int i = 0; i < 4; i++) {
-            const float4 zz = *reinterpret_cast<const float4*>(zs + c0 + 4 * i);
-            const float4 aa = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
-            f2 v01 = ffma2(f2_make(aa.x, aa.y), Q1, f2_make(zz.x, zz.y));
-            f2 v23 = ffma2(f2_make(aa.z, aa.w), Q1, f2_make(zz.z, zz.w));
-            if (!centre) {
-              const float4 bb = *reinterpret_cast<const float4*>(S.w2 + D + ch * 128 + c0 + 4 * i);
-              const f2 QY = f2_make(qy - 0.5f, qy - 0.5f);
-              v01 = ffma2(f2_make(bb.x, bb.y), QY, v01);
-              v23 = ffma2(f2_make(bb.z, bb.w), QY, v23);
-            }
+            const float4 zz = zq[b & 1][i];
+            f2 v01 = ffma2(w2pair(0, c0 + 4 * i), QX, f2_make(zz.x, zz.y));
+            f2 v23 = ffma2(w2pair(0, c0 + 4 * i + 2), QX, f2_make(zz.z, zz.w));
+            v01 = ffma2(w2pair(1, c0 + 4 * i), QY, v01);
+            v23 = ffma2(w2pair(1, c0 + 4 * i + 2), QY, v23);
             f2_split(v01, v[4 * i], v[4 * i + 1]);
             f2_split(v23, v[4 * i + 2], v[4 * i + 3]);
           }
           uint32_t w[8];
           act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v), *reinterpret_cast<uint32_t(*)[4]>(w));
           act8<GELU, F16>(*reinterpret_cast<const float(*)[8]>(v + 8), *reinterpret_cast<uint32_t(*)[4]>(w + 4));
-          st_shared_v4(a_sw[2 * j16] + ((uint32_t)kh << 14), w[0], w[1], w[2], w[3]);
-          st_shared_v4(a_sw[2 * j16 + 1] + ((uint32_t)kh << 14), w[4], w[5], w[6], w[7]);
+          st_shared_v4(a_sw[2 * (b & 3)] + ((uint32_t)(b >> 2) << 14), w[0], w[1], w[2], w[3]);
+          st_shared_v4(a_sw[2 * (b & 3) + 1] + ((uint32_t)(b >> 2) << 14), w[4], w[5], w[6], w[7]);
         }
-      }
+      };
+      if (ch == 0) split_half(std::integral_constant<int, 0>{});
+      else split_half(std::integral_constant<int, 1>{});
       fence_proxy_async();
       arrive_a();
+      if (have_next) z_stage(znext, zbuf_i ^ 1);   // next tile of the slot
 
       // ---- hidden layers (a4) and head (a5)
       f2 yacc = f2_make(0.f, 0.f);
@@ -914,7 +916,6 @@ k_chain_tc2w(const float* __restrict__ z, int64_t total_rows, int q, DevNet net,
       // ---- the row's two partial head dots meet in shared memory
       if (ch == 1) S.hpart[slot * kRows + row] = y0 + y1;
       named_sync(1 + slot, 256);
-      if (have_next) z_stage(znext);   // every thread of the slot is past this tile's split layer
       if (ch == 0 && valid) sink_store(sink, sidx, p, ((y0 + y1) + S.hpart[slot * kRows + row]) + bo);
     }
   }

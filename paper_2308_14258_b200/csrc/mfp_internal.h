@@ -99,9 +99,9 @@ struct DevNet {
   // embed's FFMA2s take each weight pair as one 64-bit constant operand (no
   // shared-memory loads, no registers); 8-byte aligned as the first member
   alignas(8) float convw[89];
-  // d = 128: W2[:,0] then W2[:,1] by value (the split layer of k_chain_tc2 takes
-  // each column pair as one 64-bit constant-bank operand of FFMA2)
-  alignas(8) float w2c[2 * 128];
+  // W2[:,0] then W2[:,1] by value, stride d (the tensor-core chains' split layers
+  // take each column pair as one 64-bit constant-bank operand of FFMA2)
+  alignas(8) float w2c[2 * 256];
   const float* conv1_w;  // [8][5]
   const float* conv1_b;  // [8]
   const float* conv2_w;  // [8][5]
