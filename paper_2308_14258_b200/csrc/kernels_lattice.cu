@@ -138,8 +138,10 @@ k_exact_phase(float* __restrict__ lat, LatticeGeom L, const uint32_t* __restrict
   // updates both outputs (p = lane, lane + 32) of a subdomain
   float2* sH = reinterpret_cast<float2*>(ex_smem);
   float* sg = ex_smem + kNB * 64;                        // [warp][sub][k]
-  load_hct(sH, HcT);
+  load_hct(sH, HcT);   // a constant of the context: loaded before the PDL wait, under the predecessor's tail
   __syncthreads();
+  tcx::pdl_launch_dependents();
+  tcx::pdl_wait();     // the lattice (previous phases) complete from here on
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* g = sg + warp * SUB * kNB;
   const int64_t step = (int64_t)gridDim.x * kExactWarps * SUB;
@@ -266,7 +268,15 @@ void launch_exact_phase(float* lat, const LatticeGeom& L, const uint32_t* anchor
   int64_t blocks = (B + per_block - 1) / per_block;
   const int per_sm = sub >= 8 ? 1 : 2;   // 96 KB of smem at 8 per warp, <= 64 KB below
   if (blocks > per_sm * num_sms()) blocks = per_sm * num_sms();
-#define MFP_EX(S) k_exact_phase<S><<<(int)blocks, kExactWarps * 32, exact_smem(S), s>>>(lat, L, anchors, B, HcT)
+  // PDL (the next phase's H_c^T load under this one's tail) only for full-size phases
+  // (one block per SM): with the small per-rank batches' 2 blocks per SM the early
+  // dependents co-reside and slow the phase down (23 -> 42 us per iteration at the
+  // 8-GPU share, tools/gpu/round2/r4k.sh)
+#define MFP_EX(S)                                                                                     \
+  do {                                                                                                \
+    if (per_sm == 1) launch_pdl(k_exact_phase<S>, (int)blocks, kExactWarps * 32, exact_smem(S), s, lat, L, anchors, B, HcT); \
+    else k_exact_phase<S><<<(int)blocks, kExactWarps * 32, exact_smem(S), s>>>(lat, L, anchors, B, HcT);     \
+  } while (0)
   switch (sub) {
     case 1: MFP_EX(1); break;
     case 2: MFP_EX(2); break;
