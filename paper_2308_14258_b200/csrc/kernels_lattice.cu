@@ -249,12 +249,17 @@ static int exact_sub(int64_t B) {
   if (forced < 0) {
     const char* e = getenv("MFP_EXACT_SUB");
     const int v = e ? atoi(e) : 0;
-    forced = (v == 1 || v == 2 || v == 4 || v == 8) ? v : 0;
+    forced = (v == 1 || v == 2 || v == 4 || v == 7 || v == 8) ? v : 0;
   }
   if (forced) return forced;
   const int64_t sms = num_sms();
   int sub = 8;
   while (sub > 1 && (B + kExactWarps * sub - 1) / (kExactWarps * sub) < (3 * sms) / 4) sub >>= 1;
+  // a full-size phase that leaves SMs idle at 8 per warp (C5: 127 blocks on 148 SMs)
+  // but fits one wave at 7 (146 blocks) takes 7: 1/8 less serial work per warp
+  if (sub == 8 && (B + kExactWarps * 8 - 1) / (kExactWarps * 8) < sms &&
+      (B + kExactWarps * 7 - 1) / (kExactWarps * 7) <= sms)
+    sub = 7;
   return sub;
 }
 
@@ -266,7 +271,7 @@ void launch_exact_phase(float* lat, const LatticeGeom& L, const uint32_t* anchor
   const int sub = exact_sub(B);
   const int per_block = kExactWarps * sub;
   int64_t blocks = (B + per_block - 1) / per_block;
-  const int per_sm = sub >= 8 ? 1 : 2;   // 96 KB of smem at 8 per warp, <= 64 KB below
+  const int per_sm = sub >= 7 ? 1 : 2;   // 88-96 KB of smem at 7-8 per warp, <= 64 KB below
   if (blocks > per_sm * num_sms()) blocks = per_sm * num_sms();
   // PDL (the next phase's H_c^T load under this one's tail) only for full-size phases
   // (one block per SM): with the small per-rank batches' 2 blocks per SM the early
@@ -281,6 +286,7 @@ void launch_exact_phase(float* lat, const LatticeGeom& L, const uint32_t* anchor
     case 1: MFP_EX(1); break;
     case 2: MFP_EX(2); break;
     case 4: MFP_EX(4); break;
+    case 7: MFP_EX(7); break;
     default: MFP_EX(8); break;
   }
 #undef MFP_EX
@@ -288,6 +294,7 @@ void launch_exact_phase(float* lat, const LatticeGeom& L, const uint32_t* anchor
 
 void exact_kernel_attributes() {
   cudaFuncSetAttribute(k_exact_phase<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(8));
+  cudaFuncSetAttribute(k_exact_phase<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(7));
   cudaFuncSetAttribute(k_exact_phase<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(4));
   cudaFuncSetAttribute(k_exact_phase<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(2));
   cudaFuncSetAttribute(k_exact_phase<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(1));
