@@ -51,6 +51,10 @@ void launch_init_lattice(float* lat, const LatticeGeom& L, int nx, int ny, const
 // (one per SM, 16 warps) load H_c^T (32 KB) once.  Each output keeps the plain k-ascending
 // FMA chain (FFMA2 rounds per lane like FFMA), so results are unchanged.
 constexpr int kExactWarps = 16;
+#ifndef MFP_EXACT_UNROLL
+#define MFP_EXACT_UNROLL 8
+#endif
+constexpr int kExactUnroll = MFP_EXACT_UNROLL;   // k-loop unroll of exact_group (A/B builds)
 constexpr int kExactSub = 8;   // subdomains per warp per round
 
 // One warp's group of kExactSub consecutive subdomains [s0, s0 + 8) of a
@@ -88,7 +92,7 @@ __device__ __forceinline__ void exact_group(float* __restrict__ lat, const Latti
   f2 y[SUB];
 #pragma unroll
   for (int j = 0; j < SUB; j++) y[j] = f2_make(0.f, 0.f);
-#pragma unroll 2
+#pragma unroll (kExactUnroll)
   for (int k = 0; k < kNB; k += 4) {
     f2 h[4];
 #pragma unroll
