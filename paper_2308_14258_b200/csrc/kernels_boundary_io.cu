@@ -63,7 +63,10 @@ k_gather_phase(const float* __restrict__ lat, LatticeGeom L, const uint32_t* __r
 // most warps per SM win over more subdomains per warp: kScU = 2 subdomains per
 // warp per round at 8 blocks (64 warps) per SM 0.67 of HBM, 4 at 5 blocks 0.59,
 // 8 at 2 blocks 0.56, an anchor prefetch across rounds no better (0.54-0.66),
-// one thread per cell 0.42; + the fused reduction 0.71 (round 1: 0.53).
+// one thread per cell 0.42; + the fused reduction 0.71 (round 1: 0.53).  Cache
+// hints (session 3, tools/gpu/round2/r4r.sh): any store hint on the lattice
+// (st.cs / st.cg / st.wt) halves it (0.35); ld.cs for the old values 0.67, ld.cv
+// 0.71 — plain stores and ld.cg stay.
 constexpr int kScU = 2;      // subdomains per warp per round
 constexpr int kScMinB = 8;   // resident blocks per SM (<= 32 registers)
 
