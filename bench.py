@@ -562,8 +562,8 @@ def main():
     burst = peaks.get("bf16_tflops", 1630.0)
     roofline = {"bound": "tensor" if tensor else "alu", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                # the chain runs unthrottled (MUFU-bound, well under the power cap), so the
-                # burst figure is the stricter denominator; both are reported
+                # both measured peaks are reported: the sustained one (a kernel timed inside
+                # a long step) and the burst one (the stricter denominator)
                 "frac_vs_burst_peak": achieved / burst if tensor else None,
                 "burst_peak": burst if tensor else None,
                 "kernel": "k_chain_tc2 (hidden GEMM chain a4 + epilogues a3/a5/a6)" if tensor else "k_chain_fp32",
@@ -577,6 +577,20 @@ def main():
                     "delta_per_check": prof.ms_delta,
                     "note": "mfp_profile_iterations: CUDA events around every kernel (no graphs), "
                             "so the iteration here includes launch gaps the graph-replayed solve avoids"}}
+    if tensor:
+        # what actually bounds the d = 128 chain: one MUFU tanh per GELU,
+        # (n_hidden + 1) x d GELUs per row, against 16 MUFU lanes / clk / SM (tools/ubench)
+        # x the SMs x the maximum SM clock (nominal; the chain's own clock under this
+        # load is lower)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        clk_mhz = (clk.summary().get("sm_max_mhz") or 1965)
+        gelus = prof.chain_rows / max(prof.chain_launches, 1) * 4 * 128
+        sfu_peak = 16 * sms * clk_mhz * 1e6 / 1e9
+        sfu_ach = gelus / (chain_ms / 1000.0) / 1e9
+        roofline["sfu_view"] = {"bound": "alu", "unit": "G GELU/s", "achieved": sfu_ach, "peak": sfu_peak,
+                                "frac": sfu_ach / sfu_peak, "gelus_per_launch": gelus,
+                                "peak_source": f"16 MUFU.TANH lanes/clk/SM (tools/ubench) x {sms} SMs x "
+                                               f"{clk_mhz} MHz (max SM clock)"}
 
     # time-to-converge (SDNet bf16, tol 1e-3 max|g|, c = 16)
     ttc = None
