@@ -402,8 +402,14 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
     const float bo = __ldg(net.bo);
     const int zi = 4 * row, zr_ = zi >> 7, zc = zi & 127;
     auto row0_of = [&](int64_t j) -> int64_t { return (cid + j * ncl) * (2 * kRows) + rank * kRows; };
+    // row -> subdomain: 32-bit division whenever the batch allows (always in practice;
+    // a 64-bit division is a ~70-instruction software routine)
+    const bool rows32 = total_rows + 2 * kRows < ((int64_t)1 << 31);
+    auto rdiv = [&](int64_t r) -> int64_t {
+      return rows32 ? (int64_t)((uint32_t)r / (uint32_t)q) : r / q;
+    };
     auto z_fetch = [&](int64_t j) -> float4 {
-      int64_t sidx = row0_of(j) / q + zr_;
+      int64_t sidx = rdiv(row0_of(j)) + zr_;
       if (sidx > nsub - 1) sidx = nsub - 1;
       return __ldg(reinterpret_cast<const float4*>(z + sidx * kD + zc));
     };
@@ -429,7 +435,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
     for (int64_t j = slot; j < nloc; j += kSlots2) {
       if (lane == 0) MFP_TR(warp, j, 0, 3);
       const int64_t row0 = row0_of(j);
-      int64_t s_first = row0 / q;
+      int64_t s_first = rdiv(row0);
       if (s_first > nsub - 1) s_first = nsub - 1;
       const int zbuf_i = (int)pz;   // buffer of this tile = tile iteration parity
       mbar_wait(&S.bars[2 * kSlots2 + slot], pz);   // this tile's staged z visible to the slot's 4 warps
@@ -441,7 +447,7 @@ k_chain_tc2(const float* __restrict__ z, int64_t total_rows, int q, DevNet net, 
       const int64_t grow = row0 + row;
       const bool valid = grow < total_rows;
       const int64_t gr = valid ? grow : total_rows - 1;
-      const int64_t sidx = gr / q;
+      const int64_t sidx = rdiv(gr);
       const int p = (int)(gr - sidx * q);
       float qx, qy;
       query_xy(q, p, &qx, &qy);
